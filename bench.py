@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark: DeepFFM predictions/s on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg1|cfg4|cfg5]
+
+Default workload = BASELINE configs[1] (cfg2): F=24, 1-3 features/field,
+Zipf(1.1) over 2^24 buckets, k=8, MLP 277->64->32->1, f32 weights N(0,0.05),
+batch 1,048,576 examples per GPU (weak scaling across ranks; tables are
+replicated by seeded on-device generation, no collective on the data path).
+A step = one K1 launch over the resident batch; L2 is flushed (a 256 MiB
+write) before every step, outside the per-step CUDA-event window.
+
+``--impl reference`` times the reference algorithm's CPU port (oracle/, the
+reference package cannot travel to the GPU box) on all host cores, rank 0
+only, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+METRIC = "DeepFFM predictions/sec (1/2/4/8 B200) + Adagrad examples/sec; % HBM roofline"
+UNIT = "predictions/s"
+
+
+# ----------------------------------------------------------------------------- helpers
+
+
+def measured_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_tag: str):
+    """Per-launch DRAM bytes from the committed ncu --set full summary, if any."""
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    v = d.get(kernel_tag)
+    return None if v is None else float(v)
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int, period_s: float = 0.01):
+        self.samples, self.reasons = [], 0
+        self.ok = False
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self.period = period_s
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.ok:
+            self.th.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [v for k, v in self.REASONS.items() if self.reasons & k]}
+
+
+def algorithmic_bytes(idx, wl, table_bytes: int, lr_bytes: int) -> int:
+    """sum over features (F*k*s_w + s_lr + 4 idx + 4 val) + 4 out."""
+    import torch
+    n_feat = int((idx >= 0).sum().item())
+    per_feat = wl.n_fields * wl.k * table_bytes + lr_bytes + 8
+    return n_feat * per_feat + 4 * idx.shape[0]
+
+
+# ----------------------------------------------------------------------------- CPU port
+
+
+_CPU_STATE = {}
+
+
+def _cpu_worker(bounds):
+    """Per-example oracle forward + predict_proba (the reference's M:321 loop)."""
+    from oracle import fieldwise_oracle as fo
+    st = _CPU_STATE["store"]
+    idx, val = _CPU_STATE["idx"], _CPU_STATE["val"]
+    out = np.empty(bounds[1] - bounds[0])
+    for i, e in enumerate(range(*bounds)):
+        out[i] = fo.predict_proba(fo.forward(fo.row_to_fields(idx[e], val[e]), st)["logit"])
+    return bounds[0], out
+
+
+def compact_oracle_store(store, idx_host):
+    """Monotone index remap: oracle store over the touched rows."""
+    import torch
+
+    from oracle import fieldwise_oracle as fo
+    u = np.unique(idx_host[idx_host >= 0])
+    bits = max(1, math.ceil(math.log2(max(len(u), 2))))
+    cfg = store.config
+    ost = fo.OracleStore.zeros(cfg.n_fields, cfg.k, cfg.hidden_sizes, bits)
+    ut = torch.as_tensor(u, dtype=torch.int64, device=store.device)
+    if store.wdtype == "u16":
+        from paper_2407_10115_b200.quant import dequantize_tensor
+        hl, bl = store.q_headers["lr"]
+        hf, bf = store.q_headers["ffm"]
+        ost.lr[: len(u)] = dequantize_tensor(store.lr[ut].contiguous(), hl, bl).cpu().numpy()
+        ost.lr[ost.n_features] = dequantize_tensor(store.lr[-1:].contiguous(), hl, bl).item()
+        ost.ffm[: len(u)] = dequantize_tensor(store.ffm[ut].contiguous(), hf, bf).cpu().numpy()
+    else:
+        ost.lr[: len(u)] = store.lr[ut].float().cpu().numpy()
+        ost.lr[ost.n_features] = store.lr[-1].float().item()
+        ost.ffm[: len(u)] = store.ffm[ut].float().cpu().numpy()
+    for i, (w, b) in enumerate(store.nn_layers):
+        ost.layers[i][0][:] = w.cpu().numpy()
+        ost.layers[i][1][:] = b.cpu().numpy()
+    ridx = np.where(idx_host >= 0, np.searchsorted(u, np.maximum(idx_host, 0)), -1)
+    return ost, ridx.astype(np.int32)
+
+
+def run_cpu_port(ost, ridx, val, n_procs):
+    """Fork one process per core; each scores a contiguous shard. -> (probs, wall_s)."""
+    import multiprocessing as mp
+    _CPU_STATE.update(store=ost, idx=ridx, val=val)
+    n = ridx.shape[0]
+    cuts = np.linspace(0, n, n_procs + 1).astype(int)
+    shards = [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+    probs = np.empty(n)
+    t0 = time.perf_counter()
+    if n_procs == 1:
+        res = [_cpu_worker(s) for s in shards]
+    else:
+        with mp.get_context("fork").Pool(n_procs) as pool:
+            res = pool.map(_cpu_worker, shards)
+    wall = time.perf_counter() - t0
+    for a, p in res:
+        probs[a:a + len(p)] = p
+    return probs, wall
+
+
+def cores_available() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- workloads
+
+
+def build_store(wl, device):
+    import torch
+
+    from paper_2407_10115_b200 import synth
+    from paper_2407_10115_b200.model import ModelConfig, WeightStore
+    cfg = ModelConfig(n_fields=wl.n_fields, k=wl.k, hidden_sizes=wl.hidden,
+                      hash_bits=wl.hash_bits)
+    base_dt = "bf16" if wl.weight_dtype == "bf16" else "f32"
+    st = WeightStore(cfg, device, base_dt, with_optimizer=False)
+    gen = torch.Generator(device=device).manual_seed(wl.weight_seed)  # same on every rank
+    chunk = 1 << 28
+    for t in (st.lr, st.ffm):
+        flat = t.view(-1)
+        for c0 in range(0, flat.numel(), chunk):
+            c1 = min(flat.numel(), c0 + chunk)
+            flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=device) * wl.weight_scale)
+    for w, b in st.nn_layers:
+        w.copy_(torch.randn(w.shape, generator=gen, device=device) * wl.weight_scale)
+        b.copy_(torch.randn(b.shape, generator=gen, device=device) * wl.weight_scale)
+    if wl.weight_dtype == "u16":
+        from paper_2407_10115_b200.quant import quantize_store
+        st, _ = quantize_store(st)
+        torch.cuda.empty_cache()
+    return st
+
+
+def build_inputs(wl, n, device, rank, chunk=1 << 20):
+    import torch
+
+    from paper_2407_10115_b200 import synth
+    cdf = synth.zipf_cdf(1 << wl.hash_bits, wl.zipf_alpha, device) if wl.dist == "zipf" else None
+    parts_i, parts_v = [], []
+    for c, c0 in enumerate(range(0, n, chunk)):
+        c1 = min(n, c0 + chunk)
+        i, v = synth.make_examples(wl, c1 - c0, seed=wl.data_seed + 7919 * rank + 104729 * c,
+                                   device=device, cdf=cdf)
+        parts_i.append(i)
+        parts_v.append(v)
+    del cdf
+    return torch.cat(parts_i), torch.cat(parts_v)
+
+
+# ----------------------------------------------------------------------------- arms
+
+
+def run_reference(args, wl):
+    """CPU port of the reference algorithm on all host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import fieldwise_oracle as fo
+    from paper_2407_10115_b200 import synth
+    cores = cores_available()
+    probe_n = 64
+    idx_t, val_t = synth.make_examples(wl, probe_n, device="cpu")
+    idx, val = idx_t.numpy(), val_t.numpy()
+    rng = np.random.default_rng(wl.weight_seed)
+
+    def store_for(ix):
+        u = np.unique(ix[ix >= 0])
+        bits = max(1, math.ceil(math.log2(max(len(u), 2))))
+        ost = fo.random_store(wl.n_fields, wl.k, wl.hidden, bits, seed=int(rng.integers(1 << 30)),
+                              scale=wl.weight_scale)
+        return ost, np.where(ix >= 0, np.searchsorted(u, np.maximum(ix, 0)), -1).astype(np.int32)
+
+    ost, ridx = store_for(idx)
+    _, t1 = run_cpu_port(ost, ridx, val, 1)
+    per_ex = t1 / probe_n
+    steps_total = args.steps + args.warmup
+    step_budget = max(0.5, min(5.0, 150.0 / max(steps_total, 1)))
+    sample = int(max(cores, min(wl.n_examples, step_budget * cores / per_ex)))
+    idx_t, val_t = synth.make_examples(wl, sample, device="cpu")
+    idx, val = idx_t.numpy(), val_t.numpy()
+    ost, ridx = store_for(idx)
+    for _ in range(args.warmup):
+        run_cpu_port(ost, ridx, val, cores)
+    walls = [run_cpu_port(ost, ridx, val, cores)[1] for _ in range(args.steps)]
+    total = sum(walls)
+    value = sample * args.steps / total
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; reference CPU port on host cores)",
+        "config": {"workload": wl.name, "sample_examples_per_step": sample,
+                   "n_fields": wl.n_fields, "k": wl.k, "hidden": list(wl.hidden),
+                   "hash_bits": wl.hash_bits, "parallelism": f"{cores} forked processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{sample} {wl.name} examples per step, per-example "
+                                   "oracle forward+predict_proba (M:300-397 restated)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_10115_b200 import _lib
+    from paper_2407_10115_b200.model import HostPredictor, predict_batch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = wl.n_examples if wl.name != "cfg5_large_bf16" else wl.n_examples // max(world, 1)
+    if args.examples:
+        n = args.examples
+    st = build_store(wl, dev)
+    idx, val = build_inputs(wl, n, dev, rank)
+    prob = torch.empty(n, dtype=torch.float32, device=dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    tbytes = {"f32": 4, "bf16": 2, "u16": 2}[st.wdtype]
+    alg = algorithmic_bytes(idx, wl, tbytes, tbytes)
+    torch.cuda.synchronize()
+
+    def step():
+        predict_batch(idx, val, st, out=prob, check=False)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for s, e in evs:
+            flush.zero_()
+            s.record()
+            step()
+            e.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = [s.elapsed_time(e) for s, e in evs]
+    total_ms = float(sum(times))
+    # parity guard: the status word must be clear and every output finite
+    predict_batch(idx, val, st, out=prob, check=True)
+    assert bool(torch.isfinite(prob).all())
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = n * world * args.steps / (total_ms / 1e3)
+    ms_step = total_ms / args.steps
+    peak, peak_src = measured_peaks()
+    achieved = alg / (ms_step / 1e3) / 1e9
+
+    # e2e: the public host-buffer API (pinned H2D per step + D2H of the probabilities)
+    idx_h = idx.cpu().pin_memory()
+    val_h = val.cpu().pin_memory()
+    out_h = torch.empty(n, dtype=torch.float32).pin_memory()
+    hp = HostPredictor(st, n, idx.shape[2])
+    hp(idx_h, val_h, out_h)
+    e2e_steps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        hp(idx_h, val_h, out_h)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * world / float(te.item())
+    e2e_ok = bool(torch.equal(out_h, prob.cpu()))
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded on-device; Zipf/hashed stand-in for Criteo-like data)",
+        "config": {"workload": wl.name, "examples_per_gpu": n, "n_fields": wl.n_fields,
+                   "k": wl.k, "hidden": list(wl.hidden), "hash_bits": wl.hash_bits,
+                   "max_per_field": int(idx.shape[2]), "table_dtype": st.wdtype,
+                   "mean_features_per_example": int((idx >= 0).sum().item()) / n,
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"batch-sharded x{world}, replicated tables, no collective"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(wl.name),
+                     "algorithmic_bytes_per_step": alg, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": idx.numel() * 4 + val.numel() * 4,
+                "d2h_bytes_per_step": n * 4 + 8, "matches_device_run": e2e_ok},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(st, idx, val, prob, wl)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(st, idx, val, prob, wl, budget_s=12.0):
+    """Oracle port on the host cores over a bounded sample of THIS batch (same
+    inputs, same table rows via the remap); also reports GPU-vs-oracle parity."""
+    cores = cores_available()
+    probe = 64
+    ih = idx[:probe].cpu().numpy()
+    vh = val[:probe].cpu().numpy()
+    ost, ridx = compact_oracle_store(st, ih)
+    _, t1 = run_cpu_port(ost, ridx, vh, 1)
+    sample = int(min(idx.shape[0], max(cores * 16, budget_s * cores / (t1 / probe))))
+    ih = idx[:sample].cpu().numpy()
+    vh = val[:sample].cpu().numpy()
+    ost, ridx = compact_oracle_store(st, ih)
+    ref, wall = run_cpu_port(ost, ridx, vh, cores)
+    gp = prob[:sample].double().cpu().numpy()
+    rel = float(np.max(np.abs(gp - ref) / ref))
+    return {"value": sample / wall, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first {sample} examples of the timed batch, per-example oracle "
+                      f"forward+predict_proba, {cores} forked processes",
+            "gpu_vs_oracle_max_rel_err": rel}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--examples", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    from paper_2407_10115_b200 import configs
+    wl = {"cfg1": configs.CFG1, "cfg2": configs.CFG2, "cfg4": configs.CFG4,
+          "cfg5": configs.CFG5}[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

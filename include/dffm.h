@@ -1,0 +1,165 @@
+/*
+ * dffm.h -- C ABI of libdffm.so, the B200 (sm_100a) DeepFFM hot path.
+ *
+ * The reference (`fieldwise`, /root/reference/pkg/src/fieldwise) has no FFI:
+ * its boundary is the Python API of model.py.  Each entry point below
+ * replaces one reference function (cited file:line) and is what a ctypes /
+ * cffi binding of that Python API calls.
+ *
+ * Conventions
+ *   - Every pointer argument is a caller-owned DEVICE pointer unless named
+ *     *_host.  Nothing here allocates on the hot path or frees caller memory.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on it.  Results that need a host decision (status words) are read back
+ *     by the caller.
+ *   - Return value: DFFM_OK or an error class mirroring fieldwise/errors.py;
+ *     dffm_last_error() gives a thread-local message for the last failure.
+ *   - Device status word (uint64, initialise to all-ones): kernels report
+ *     the first offending example with atomicMin on
+ *         (example_index << 8) | (block << 4) | code
+ *     so the host raises the same exception class, for the same (first)
+ *     example, with the same `block` name as the reference would.
+ */
+#ifndef DFFM_H
+#define DFFM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error classes (E: errors.py) */
+enum dffm_status {
+  DFFM_OK = 0,
+  DFFM_CONTRACT = 1, /* ContractError  E:32  (bad field id, index, label, stale state) */
+  DFFM_FORMAT = 2,   /* FormatError    E:16 */
+  DFFM_NUMERIC = 3,  /* NumericError   E:40  (block code in the status word) */
+  DFFM_SIZING = 4,   /* SizingError    E:36 */
+  DFFM_CUDA = 5      /* CUDA runtime failure */
+};
+
+/* NumericError.block, in the reference's diagnosis order (M:308-318, M:458) */
+enum dffm_block {
+  DFFM_BLOCK_NONE = 0, DFFM_BLOCK_LR = 1, DFFM_BLOCK_FFM = 2, DFFM_BLOCK_MERGE = 3,
+  DFFM_BLOCK_NN = 4, DFFM_BLOCK_LOGIT = 5, DFFM_BLOCK_LOSS = 6
+};
+
+/* storage type of the hashed lr / ffm tables */
+enum dffm_wdtype { DFFM_W_F32 = 0, DFFM_W_BF16 = 1, DFFM_W_U16Q = 2 };
+
+#define DFFM_MAX_LAYERS 5 /* <= 4 hidden layers (M:70-71) + the output layer */
+
+/*
+ * Device-resident model (replaces WeightStore, M:142-230).  Each block is a
+ * separate 256-byte-aligned allocation instead of the reference's one flat
+ * array (whose ffm block starts 4 bytes past a 16-byte boundary, M:182):
+ *   lr   [2^b + 1]        lr weights, bias at index 2^b        (M:148-149)
+ *   ffm  [2^b][F][k]      field-aware latent rows, row-major   (M:150-151)
+ *   W[l] [in][out] f32, b[l] [out] f32 per MLP layer           (M:152, M:198-210)
+ * For DFFM_W_U16Q the lr/ffm tables hold 16-bit bucket indices and are
+ * dequantised inline as  w = q_min + idx * q_bucket  (f32 mul, then f32 add).
+ */
+typedef struct dffm_model {
+  int32_t n_fields;
+  int32_t k;
+  int32_t hash_bits;
+  int32_t n_layers;                    /* 0 (no MLP) or len(hidden)+1 */
+  int32_t dims[DFFM_MAX_LAYERS + 1];   /* dims[0] = 1+F(F-1)/2 ... dims[n_layers] = 1 */
+  int32_t wdtype;                      /* enum dffm_wdtype */
+  int32_t _pad;
+  const void* lr;
+  const void* ffm;
+  const float* W[DFFM_MAX_LAYERS];
+  const float* b[DFFM_MAX_LAYERS];
+  float q_lr_min, q_lr_bucket;         /* per-table FWQ1 headers (u16 only) */
+  float q_ffm_min, q_ffm_bucket;
+} dffm_model;
+
+/* Library identity / diagnostics */
+int dffm_abi_version(void);
+const char* dffm_last_error(void);
+int dffm_device_sm_count(int device);
+
+/*
+ * K1 fused forward, batched: replaces model.forward + predict_proba
+ * (M:300-397) as called per example by training.evaluate_stream
+ * (T:221-236).  Inputs are canonical padded examples (Fe:121-172):
+ *   idx [n][F][max_per_field] int32, -1 = empty slot, indices strictly
+ *   increasing within a field; val same shape, f32.
+ * Outputs prob[n] (clamped sigmoid, M:304-305) and optionally logit[n].
+ * status_base is added to example numbers reported in the status word, so
+ * chunked or sharded launches report the caller's global example index.
+ */
+int dffm_forward(const dffm_model* model, const int32_t* idx, const float* val,
+                 int32_t max_per_field, int64_t n, float* prob, float* logit_opt,
+                 int64_t status_base, uint64_t* status, void* stream);
+
+/*
+ * K3 context-cached scorer (no reference code).  Request r
+ * has ctx fields [0, n_ctx_fields) in ctx_idx[r][n_ctx_fields][ctx_m] and
+ * n_cand candidates with fields [n_ctx_fields, F) in
+ * cand_idx[r][n_cand][F - n_ctx_fields][cand_m].  prob[r][n_cand] equals
+ * forward+predict_proba on the merged example.
+ */
+int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx, const float* ctx_val,
+                   int32_t n_ctx_fields, int32_t ctx_m, const int32_t* cand_idx,
+                   const float* cand_val, int32_t cand_m, int64_t n_requests, int32_t n_cand,
+                   float* prob, uint64_t* status, void* stream);
+
+/*
+ * K2 sequential Adagrad trainer: replaces the predict-then-learn loop of
+ * training._train_lines (T:172-185) = forward (M:321) + predict_proba
+ * (M:300) + backward_update (M:440-533), in the reference's exact example
+ * order, f64 arithmetic over f32 storage.  Mutates the weights of `model`
+ * (which must be DFFM_W_F32) and the accumulators in place.
+ *   lr_acc [2^b+1], ffm_acc [2^b][F][k], W_acc[l], b_acc[l]   f32, same shapes
+ *   labels[n] in {0,1} (else ContractError, M:453-454)
+ *   prob_out[n]: the clamped progressive prediction of each example (f64)
+ *   scratch: device workspace of dffm_train_scratch_bytes() bytes
+ */
+typedef struct dffm_train_state {
+  float* lr_acc;
+  float* ffm_acc;
+  float* W_acc[DFFM_MAX_LAYERS];
+  float* b_acc[DFFM_MAX_LAYERS];
+  double lr_ffm, lr_lr, lr_nn, power_t;
+  int32_t sparse;                      /* M:536-572 sparse skip (results identical) */
+  int32_t _pad;
+} dffm_train_state;
+
+int64_t dffm_train_scratch_bytes(const dffm_model* model, int32_t max_per_field);
+int dffm_train_sequential(const dffm_model* model, const dffm_train_state* state,
+                          const int32_t* idx, const float* val, const uint8_t* labels,
+                          int32_t max_per_field, int64_t n, double* prob_out,
+                          void* scratch, uint64_t* status, void* stream);
+
+/*
+ * K4 16-bit quantisation (formula PAPER.md:291-305).
+ *   fwq_minmax:     minmax_out[2] = {min, max} of w[n] (device); *first_nonfinite
+ *                   (device, initialise to all-ones) = smallest offset of a
+ *                   non-finite weight (SPEC S:317 NumericError "with offset")
+ *   fwq_header:     host-side header from min/max, pinned rounding
+ *   fwq_quantize:   q[i] = clamp(rint((f64(w)-f64(hmin))/f64(hbucket)), 0, 65535)
+ *   fwq_dequantize: out[i] = hmin + q[i]*hbucket  (f32 mul then f32 add, no FMA)
+ */
+int fwq_minmax(const float* w, int64_t n, float* minmax_out, uint64_t* first_nonfinite,
+               void* stream);
+int fwq_header(float wmin, float wmax, int32_t alpha, int32_t beta, float* hmin_host,
+               float* hbucket_host);
+int fwq_quantize(const float* w, int64_t n, float hmin, float hbucket, uint16_t* q,
+                 void* stream);
+int fwq_dequantize(const uint16_t* q, int64_t n, float hmin, float hbucket, float* out,
+                   void* stream);
+
+/*
+ * K5 feature hashing (H:28-50): out[i] = fnv1a32(bytes[off[i]:off[i+1]]) & (2^bits-1)
+ * (bits = 32 returns the raw hash).
+ */
+int fw_hash_fnv1a32(const uint8_t* bytes, const int64_t* offsets, int64_t n, int32_t bits,
+                    uint32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFFM_H */

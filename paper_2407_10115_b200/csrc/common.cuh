@@ -1,0 +1,154 @@
+// Shared device/host helpers for libdffm (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dffm.h"
+
+namespace dffm {
+
+// ------------------------------------------------------------------ host side
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+int sm_count_current();
+int max_smem_optin_current();
+
+#define DFFM_CUDA_TRY(expr, what)                 \
+  do {                                            \
+    cudaError_t _e = (expr);                      \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+// status word: (example << 8) | (block << 4) | code   (see dffm.h)
+__host__ __device__ inline uint64_t status_key(int64_t example, int block, int code) {
+  return ((uint64_t)example << 8) | ((uint64_t)(block & 0xF) << 4) | (uint64_t)(code & 0xF);
+}
+
+// ------------------------------------------------------------------ device side
+struct Deq {
+  float qmin, qb;  // u16 header (ignored for f32/bf16)
+};
+
+__device__ __forceinline__ uint4 ldg_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_stream8(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+// inline dequantisation: w = qmin + q*qb, f32 multiply then f32 add
+__device__ __forceinline__ float deq(uint32_t q, const Deq& d) {
+  return __fadd_rn(d.qmin, __fmul_rn((float)q, d.qb));
+}
+
+// Scalar table element -> float
+template <typename T>
+__device__ __forceinline__ float load_elem(const T* p, const Deq& d);
+template <>
+__device__ __forceinline__ float load_elem<float>(const float* p, const Deq&) {
+  return __ldg(p);
+}
+template <>
+__device__ __forceinline__ float load_elem<__nv_bfloat16>(const __nv_bfloat16* p, const Deq&) {
+  return __bfloat162float(*p);
+}
+template <>
+__device__ __forceinline__ float load_elem<uint16_t>(const uint16_t* p, const Deq& d) {
+  return deq(*p, d);
+}
+
+// Unpack one 16-byte chunk of T into floats
+template <typename T>
+__device__ __forceinline__ void unpack16(const uint4& u, float* o, const Deq& d);
+template <>
+__device__ __forceinline__ void unpack16<float>(const uint4& u, float* o, const Deq&) {
+  o[0] = __uint_as_float(u.x); o[1] = __uint_as_float(u.y);
+  o[2] = __uint_as_float(u.z); o[3] = __uint_as_float(u.w);
+}
+template <>
+__device__ __forceinline__ void unpack16<__nv_bfloat16>(const uint4& u, float* o, const Deq&) {
+  o[0] = bf16lo(u.x); o[1] = bf16hi(u.x); o[2] = bf16lo(u.y); o[3] = bf16hi(u.y);
+  o[4] = bf16lo(u.z); o[5] = bf16hi(u.z); o[6] = bf16lo(u.w); o[7] = bf16hi(u.w);
+}
+template <>
+__device__ __forceinline__ void unpack16<uint16_t>(const uint4& u, float* o, const Deq& d) {
+  o[0] = deq(u.x & 0xFFFF, d); o[1] = deq(u.x >> 16, d);
+  o[2] = deq(u.y & 0xFFFF, d); o[3] = deq(u.y >> 16, d);
+  o[4] = deq(u.z & 0xFFFF, d); o[5] = deq(u.z >> 16, d);
+  o[6] = deq(u.w & 0xFFFF, d); o[7] = deq(u.w >> 16, d);
+}
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint2& u, float* o, const Deq& d) {
+  uint4 w = make_uint4(u.x, u.y, 0, 0);
+  float t[16 / sizeof(T)];
+  unpack16<T>(w, t, d);
+#pragma unroll
+  for (int i = 0; i < (int)(8 / sizeof(T)); ++i) o[i] = t[i];
+}
+
+// Load one k-vector segment (K elements of T, naturally aligned) as floats.
+// K == 0 selects the runtime-k scalar path (tests / unusual k).
+template <int K, typename T>
+struct Seg {
+  static constexpr int BYTES = K * (int)sizeof(T);
+  __device__ __forceinline__ static void load(const T* p, float* o, const Deq& d, int) {
+    if constexpr (BYTES >= 16) {
+      constexpr int PER = 16 / sizeof(T);
+      uint4 u[BYTES / 16];
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c) u[c] = ldg_stream16(p + c * PER);
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c) unpack16<T>(u[c], o + c * PER, d);
+    } else if constexpr (BYTES == 8) {
+      unpack8<T>(ldg_stream8(p), o, d);
+    } else {
+#pragma unroll
+      for (int c = 0; c < K; ++c) o[c] = load_elem<T>(p + c, d);
+    }
+  }
+};
+
+// Runtime-k segment load for the K == 0 instantiation.
+template <typename T>
+struct Seg<0, T> {
+  __device__ __forceinline__ static void load(const T* p, float* o, const Deq& d, int k) {
+    for (int c = 0; c < k; ++c) o[c] = load_elem<T>(p + c, d);
+  }
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_sumf(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Stable clamped sigmoid (M:293-305), f64.
+__device__ __forceinline__ double sigmoid_clamped(double logit) {
+  double p;
+  if (logit >= 0.0) {
+    p = 1.0 / (1.0 + exp(-fmin(logit, 60.0)));
+  } else {
+    double e = exp(fmax(logit, -60.0));
+    p = e / (1.0 + e);
+  }
+  return fmin(fmax(p, 1e-7), 1.0 - 1e-7);
+}
+
+}  // namespace dffm

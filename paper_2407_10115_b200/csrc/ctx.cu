@@ -1,0 +1,310 @@
+// K3: context-cached candidate scorer (no reference code --
+// the truth is model.forward on the merged context+candidate example).
+//
+// One CTA owns a request at a time (persistent over requests):
+//   cache build (once per request, cost independent of the candidate count,
+//   S:257): lr partial over the context features, the context latent
+//   sums Sctx[x][g][:] = sum_{j in x} x_j * ffm[j][g][:] for every context field
+//   x and every target field g, and the ctx x ctx pair values -- all in shared
+//   memory, never written to HBM.
+//   candidates, in tiles of TE: one warp per candidate gathers only the
+//   candidate's own rows; cand x ctx pairs use <S[c][x] (gathered), Sctx[x][c]
+//   (cached)>, cand x cand pairs are formed as in K1, ctx x ctx pairs are
+//   copied from the cache.  MergeNorm and the MLP are not cached and
+//   run through the same phase-B tile code as K1.
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+#include "forward_kernel.cuh"
+
+namespace dffm {
+
+int fill_model_params(const dffm_model* m, FwdParams& p);
+int pick_k_template(int k, int wdtype);
+
+struct CtxParams {
+  FwdParams f;
+  const int32_t* cidx;
+  const float* cval;
+  const int32_t* didx;
+  const float* dval;
+  int Fc, Mc, Fd, Md;
+  int64_t R;
+  int C;
+};
+
+struct CtxSmem {
+  FwdSmem b;
+  int off_S, off_cpair, off_cpres, off_csidx, off_csval, off_lrp, total;
+};
+
+__host__ __device__ inline CtxSmem ctx_smem_layout(const CtxParams& q) {
+  const FwdParams& p = q.f;
+  CtxSmem s;
+  // per-warp slot buffers sized for the candidate part (Fd x Md)
+  s.b = fwd_smem_layout(p.F, 1, p.P, p.D, p.TE, p.XS, p.hmax);
+  int o = s.b.off_sidx;
+  s.b.off_sidx = o; o = align16(o + FWD_WARPS * q.Fd * q.Md * 4);
+  s.b.off_sval = o; o = align16(o + FWD_WARPS * q.Fd * q.Md * 4);
+  s.off_S = o; o = align16(o + q.Fc * p.F * p.k * 4);
+  s.off_cpair = o; o = align16(o + p.P * 4);
+  s.off_cpres = o; o = align16(o + q.Fc);
+  s.off_csidx = o; o = align16(o + q.Fc * q.Mc * 4);
+  s.off_csval = o; o = align16(o + q.Fc * q.Mc * 4);
+  s.off_lrp = o; o = align16(o + 8);
+  s.total = o;
+  return s;
+}
+
+template <int K, int MU, typename T>
+__global__ void __launch_bounds__(FWD_THREADS)
+ctx_kernel(CtxParams q) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const FwdParams& p = q.f;
+  const CtxSmem L = ctx_smem_layout(q);
+  uint16_t* pairtab = (uint16_t*)(smem + L.b.off_pair);
+  float* X = (float*)(smem + L.b.off_X);
+  float* Ha = (float*)(smem + L.b.off_Ha);
+  float* Hb = (float*)(smem + L.b.off_Hb);
+  double* exd = (double*)(smem + L.b.off_exd);
+  int* flag = (int*)(smem + L.b.off_flag);
+  float* Sctx = (float*)(smem + L.off_S);
+  float* cpair = (float*)(smem + L.off_cpair);
+  unsigned char* cpres = smem + L.off_cpres;
+  int* csidx = (int*)(smem + L.off_csidx);
+  float* csval = (float*)(smem + L.off_csval);
+  double* lrp = (double*)(smem + L.off_lrp);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int F = p.F, Fc = q.Fc, Mc = q.Mc, Fd = q.Fd, Md = q.Md;
+  const int DM = Fd * Md;
+  unsigned char* spres = smem + L.b.off_pres + warp * F;
+  int* sidx = (int*)(smem + L.b.off_sidx) + warp * DM;
+  float* sval = (float*)(smem + L.b.off_sval) + warp * DM;
+  const int TE = p.TE, XS = p.XS, P = p.P, D = p.D;
+  constexpr int KA = K ? K : 32;
+  const int k = K ? K : p.k;
+  const T* ffm = (const T*)p.ffm;
+
+  build_pairtab(pairtab, F);
+  const float bias = load_elem<T>((const T*)p.lr + p.n_buckets, p.dlr);
+
+  for (int64_t r = blockIdx.x; r < q.R; r += gridDim.x) {
+    __syncthreads();
+    // ---------------------------------------------- build_context_cache
+    if (warp == 0) {
+      int bad = 0;
+      const double lrs = stage_slots<T>(p, q.cidx + r * Fc * Mc, q.cval + r * Fc * Mc, Fc * Mc,
+                                        csidx, csval, lane, bad);
+      const double tot = warp_sum(lrs);
+      if (lane == 0) *lrp = tot;
+      if (__any_sync(0xffffffffu, bad) && lane == 0)
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(r * q.C, DFFM_BLOCK_NONE, DFFM_CONTRACT));
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < Fc; x += FWD_THREADS) {
+      unsigned char pr = 0;
+      for (int m = 0; m < Mc; ++m) pr |= (csidx[x * Mc + m] >= 0);
+      cpres[x] = pr;
+    }
+    for (int t = threadIdx.x; t < Fc * F * k; t += FWD_THREADS) {
+      const int x = t / (F * k), gk = t % (F * k);
+      float acc = 0.f;
+      for (int m = 0; m < Mc; ++m) {
+        const int j = csidx[x * Mc + m];
+        if (j >= 0) acc = fmaf(csval[x * Mc + m], load_elem<T>(ffm + (int64_t)j * F * k + gk, p.dffm), acc);
+      }
+      Sctx[t] = acc;
+    }
+    __syncthreads();
+    for (int pp = threadIdx.x; pp < P; pp += FWD_THREADS) {
+      const uint32_t pr = pairtab[pp];
+      const int f1 = pr & 0xFF, f2 = pr >> 8;
+      float pv = 0.f;
+      if (f2 < Fc && (cpres[f1] & cpres[f2])) {
+        const float* a = Sctx + (f1 * F + f2) * k;
+        const float* b = Sctx + (f2 * F + f1) * k;
+        for (int c = 0; c < k; ++c) pv = fmaf(a[c], b[c], pv);
+      }
+      cpair[pp] = pv;
+    }
+    __syncthreads();
+    const double lr_ctx = (double)bias + *lrp;
+
+    // ---------------------------------------------- predict_batch
+    for (int c0 = 0; c0 < q.C; c0 += TE) {
+      for (int el = warp; el < TE; el += FWD_WARPS) {
+        const int cand = c0 + el;
+        if (cand >= q.C) { zero_column(X, exd, flag, el, TE, XS, D, lane); continue; }
+        const int64_t e = r * q.C + cand;
+        int bad = 0;
+        const double lrs = stage_slots<T>(p, q.didx + e * DM, q.dval + e * DM, DM, sidx, sval,
+                                          lane, bad);
+        __syncwarp();
+        for (int f = lane; f < Fd; f += 32) {
+          unsigned char pr = 0;
+          for (int m = 0; m < Md; ++m) pr |= (sidx[f * Md + m] >= 0);
+          spres[Fc + f] = pr;
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0)
+          atomicMin((unsigned long long*)p.status,
+                    (unsigned long long)status_key(e, DFFM_BLOCK_NONE, DFFM_CONTRACT));
+        const double lr_out = lr_ctx + warp_sum(lrs);
+        __syncwarp();
+        double s1 = 0.0;
+        int pbad = 0;
+        for (int pp = lane; pp < P; pp += 32) {
+          const uint32_t pr = pairtab[pp];
+          const int f1 = pr & 0xFF, f2 = pr >> 8;
+          float pv;
+          if (f2 < Fc) {
+            pv = cpair[pp];  // ctx x ctx: cached
+          } else {
+            pv = 0.f;
+            const int d2 = f2 - Fc;
+            float a[KA], bb[KA];
+#pragma unroll
+            for (int c = 0; c < KA; ++c) { a[c] = 0.f; bb[c] = 0.f; }
+            if (f1 < Fc) {  // ctx x cand: S[f1][f2] from the cache
+              if (cpres[f1] & spres[f2]) {
+                const float* sc = Sctx + (f1 * F + f2) * k;
+#pragma unroll
+                for (int c = 0; c < KA; ++c)
+                  if (K || c < k) a[c] = sc[c];
+                accum_slots<K, MU, T>(p, sidx + d2 * Md, sval + d2 * Md, Md, f1, bb);
+#pragma unroll
+                for (int c = 0; c < KA; ++c)
+                  if (K || c < k) pv = fmaf(a[c], bb[c], pv);
+              }
+            } else if (spres[f1] & spres[f2]) {  // cand x cand
+              const int d1 = f1 - Fc;
+              accum_slots<K, MU, T>(p, sidx + d1 * Md, sval + d1 * Md, Md, f2, a);
+              accum_slots<K, MU, T>(p, sidx + d2 * Md, sval + d2 * Md, Md, f1, bb);
+#pragma unroll
+              for (int c = 0; c < KA; ++c)
+                if (K || c < k) pv = fmaf(a[c], bb[c], pv);
+            }
+          }
+          X[(pp + 1) * XS + el] = pv;
+          s1 += (double)pv;
+          pbad |= !isfinite(pv);
+        }
+        merge_finish(X, exd, flag, el, TE, XS, P, D, lane, lr_out, s1, pbad);
+      }
+      __syncthreads();
+      const int nvalid = (q.C - c0) < TE ? (q.C - c0) : TE;
+      mlp_tile(p, X, Ha, Hb, exd, flag, r * q.C + c0, nvalid);
+    }
+  }
+}
+
+using CtxKernel = void (*)(CtxParams);
+
+template <typename T>
+static CtxKernel select_ctx(int K, int MU) {
+#define DFFM_SEL(KK)                                   \
+  if (K == KK) {                                       \
+    if (MU == 1) return ctx_kernel<KK, 1, T>;          \
+    if (MU == 4) return ctx_kernel<KK, 4, T>;          \
+    return ctx_kernel<KK, 0, T>;                       \
+  }
+  DFFM_SEL(4)
+  DFFM_SEL(8)
+  DFFM_SEL(16)
+  DFFM_SEL(32)
+  DFFM_SEL(0)
+#undef DFFM_SEL
+  return nullptr;
+}
+
+static int launch_ctx(CtxKernel kern, const CtxParams& q, int smem, cudaStream_t s) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, int> occ_cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = ((uint64_t)(uintptr_t)kern * 1315423911u) ^ ((uint64_t)smem << 8) ^ dev;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ_cache.find(key);
+    if (it != occ_cache.end()) {
+      occ = it->second;
+    } else {
+      DFFM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                    "cudaFuncSetAttribute(ctx)");
+      DFFM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, FWD_THREADS, smem),
+                    "occupancy(ctx)");
+      if (occ < 1) occ = 1;
+      occ_cache[key] = occ;
+    }
+  }
+  const int64_t grid = std::min<int64_t>(q.R, (int64_t)sm_count_current() * occ);
+  kern<<<(unsigned)grid, FWD_THREADS, smem, s>>>(q);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(ctx)");
+  return DFFM_OK;
+}
+
+}  // namespace dffm
+
+using namespace dffm;
+
+extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
+                              const float* ctx_val, int32_t n_ctx_fields, int32_t ctx_m,
+                              const int32_t* cand_idx, const float* cand_val, int32_t cand_m,
+                              int64_t n_requests, int32_t n_cand, float* prob, uint64_t* status,
+                              void* stream) {
+  CtxParams q{};
+  int rc = fill_model_params(model, q.f);
+  if (rc) return rc;
+  FwdParams& p = q.f;
+  if (n_ctx_fields < 0 || n_ctx_fields > p.F || ctx_m < 1 || cand_m < 1 || ctx_m > 64 ||
+      cand_m > 64 || n_requests < 0 || n_cand < 0) {
+    set_error("bad request shape");
+    return DFFM_CONTRACT;
+  }
+  if (n_requests == 0 || n_cand == 0) return DFFM_OK;
+  if (!prob || !status || (n_ctx_fields && (!ctx_idx || !ctx_val)) ||
+      (n_ctx_fields < p.F && (!cand_idx || !cand_val))) {
+    set_error("null buffer");
+    return DFFM_CONTRACT;
+  }
+  q.cidx = ctx_idx;
+  q.cval = ctx_val;
+  q.didx = cand_idx;
+  q.dval = cand_val;
+  q.Fc = n_ctx_fields;
+  q.Mc = ctx_m;
+  q.Fd = p.F - n_ctx_fields;
+  q.Md = cand_m;
+  q.R = n_requests;
+  q.C = n_cand;
+  p.n = n_requests * (int64_t)n_cand;
+  p.M = cand_m;
+  p.prob = prob;
+  p.logit = nullptr;
+  p.status = status;
+  const int smax = max_smem_optin_current();
+  CtxSmem L;
+  int TE = 32;
+  for (;; TE >>= 1) {
+    p.TE = TE;
+    p.XS = TE + 2;
+    L = ctx_smem_layout(q);
+    if (L.total <= smax || TE <= 2) break;
+  }
+  if (L.total > smax) {
+    set_error("context scorer needs %d B shared memory (> %d)", L.total, smax);
+    return DFFM_SIZING;
+  }
+  const int K = pick_k_template(p.k, model->wdtype);
+  const int MU = cand_m == 1 ? 1 : (cand_m <= 4 ? 4 : 0);
+  CtxKernel kern = nullptr;
+  switch (model->wdtype) {
+    case DFFM_W_F32: kern = select_ctx<float>(K, MU); break;
+    case DFFM_W_BF16: kern = select_ctx<__nv_bfloat16>(K, MU); break;
+    default: kern = select_ctx<uint16_t>(K, MU); break;
+  }
+  if (!kern) { set_error("no context kernel for k=%d", p.k); return DFFM_SIZING; }
+  return launch_ctx(kern, q, L.total, (cudaStream_t)stream);
+}

@@ -1,0 +1,119 @@
+// C ABI entry for K1 (dffm_forward): validation, tile sizing, dispatch.
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+#include "forward_kernel.cuh"
+
+namespace dffm {
+
+template <typename T>
+int launch_forward_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s);
+
+// shared with ctx.cu: fills FwdParams' model part, validates
+int fill_model_params(const dffm_model* m, FwdParams& p) {
+  if (!m) { set_error("null model"); return DFFM_CONTRACT; }
+  if (m->n_fields < 1 || m->n_fields > 255) {
+    set_error("n_fields=%d outside [1, 255]", m->n_fields);
+    return DFFM_SIZING;
+  }
+  if (m->k < 1 || m->k > 32) {
+    set_error("k=%d unsupported (1..32)", m->k);
+    return DFFM_SIZING;
+  }
+  if (m->hash_bits < 1 || m->hash_bits > 29) {
+    set_error("hash_bits=%d outside [1, 29]", m->hash_bits);
+    return DFFM_CONTRACT;
+  }
+  if (m->n_layers < 0 || m->n_layers > DFFM_MAX_LAYERS || m->n_layers == 1) {
+    set_error("n_layers=%d invalid", m->n_layers);
+    return DFFM_CONTRACT;
+  }
+  if (m->wdtype < 0 || m->wdtype > 2) { set_error("bad wdtype"); return DFFM_CONTRACT; }
+  if (!m->lr || !m->ffm) { set_error("null table"); return DFFM_CONTRACT; }
+  p.F = m->n_fields;
+  p.k = m->k;
+  p.P = p.F * (p.F - 1) / 2;
+  p.D = 1 + p.P;
+  p.n_buckets = (int64_t)1 << m->hash_bits;
+  p.n_layers = m->n_layers;
+  p.hmax = 0;
+  for (int l = 0; l <= DFFM_MAX_LAYERS; ++l) p.dims[l] = m->dims[l];
+  if (p.n_layers) {
+    if (m->dims[0] != p.D || m->dims[p.n_layers] != 1) {
+      set_error("MLP dims do not match 1+F(F-1)/2 -> ... -> 1");
+      return DFFM_CONTRACT;
+    }
+    for (int l = 0; l < p.n_layers; ++l) {
+      if (!m->W[l] || !m->b[l]) { set_error("null MLP layer %d", l); return DFFM_CONTRACT; }
+      if (((uintptr_t)m->W[l] & 15) || ((uintptr_t)m->b[l] & 15)) {
+        set_error("MLP layer %d not 16-byte aligned", l);
+        return DFFM_CONTRACT;
+      }
+      p.W[l] = m->W[l];
+      p.b[l] = m->b[l];
+      if (l + 1 < p.n_layers) p.hmax = std::max(p.hmax, m->dims[l + 1]);
+    }
+  }
+  p.lr = m->lr;
+  p.ffm = m->ffm;
+  p.dlr = Deq{m->q_lr_min, m->q_lr_bucket};
+  p.dffm = Deq{m->q_ffm_min, m->q_ffm_bucket};
+  return DFFM_OK;
+}
+
+int fwd_dispatch(int wdtype, const FwdParams& p, int K, int MU, int smem, cudaStream_t s) {
+  switch (wdtype) {
+    case DFFM_W_F32: return launch_forward_t<float>(p, K, MU, smem, s);
+    case DFFM_W_BF16: return launch_forward_t<__nv_bfloat16>(p, K, MU, smem, s);
+    default: return launch_forward_t<uint16_t>(p, K, MU, smem, s);
+  }
+}
+
+int pick_k_template(int k, int wdtype) {
+  const int esz = wdtype == DFFM_W_F32 ? 4 : 2;
+  if ((k == 4 || k == 8 || k == 16 || k == 32) && (k * esz) % 8 == 0) return k;
+  return 0;
+}
+
+}  // namespace dffm
+
+using namespace dffm;
+
+extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const float* val,
+                            int32_t max_per_field, int64_t n, float* prob, float* logit_opt,
+                            int64_t status_base, uint64_t* status, void* stream) {
+  FwdParams p{};
+  int rc = fill_model_params(model, p);
+  if (rc) return rc;
+  if (n < 0 || max_per_field < 1 || max_per_field > 64) {
+    set_error("bad batch shape n=%lld M=%d", (long long)n, max_per_field);
+    return DFFM_CONTRACT;
+  }
+  if (n == 0) return DFFM_OK;
+  if (!idx || !val || !prob || !status) { set_error("null buffer"); return DFFM_CONTRACT; }
+  p.idx = idx;
+  p.val = val;
+  p.prob = prob;
+  p.logit = logit_opt;
+  p.status = status;
+  p.n = n;
+  p.status_base = status_base;
+  p.M = max_per_field;
+  const int smax = max_smem_optin_current();
+  int TE = 32;
+  FwdSmem L;
+  for (;; TE >>= 1) {
+    p.TE = TE;
+    p.XS = TE + 2;
+    L = fwd_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax);
+    if (L.total <= smax || TE <= 2) break;
+  }
+  if (L.total > smax) {
+    set_error("forward tile needs %d B shared memory (> %d)", L.total, smax);
+    return DFFM_SIZING;
+  }
+  const int K = pick_k_template(p.k, model->wdtype);
+  const int MU = p.M == 1 ? 1 : (p.M <= 4 ? 4 : 0);
+  return fwd_dispatch(model->wdtype, p, K, MU, L.total, (cudaStream_t)stream);
+}

@@ -1,0 +1,540 @@
+"""Drop-in for ``fieldwise.model`` (M: /root/reference/pkg/src/fieldwise/model.py).
+
+Same names and semantics -- ``ModelConfig``, ``WeightStore``, ``init_model``,
+``forward``, ``predict_proba``, ``backward_update``, ``flat_weight_view``,
+``store_from_bytes``, ``save_model``, ``load_model`` -- plus the batched
+entry points the GPU makes worthwhile (``predict_batch``).
+
+The store lives in HBM as separate, 256-byte-aligned blocks (torch tensors used
+purely as device buffers) laid out exactly like the reference's frozen flat
+array, block by block (M:145-153):
+
+    lr   [2^b + 1]            f32 | bf16 | u16 (bias at 2^b)
+    ffm  [2^b, F, k]          f32 | bf16 | u16   (row = one bucket's F*k latent
+                                                  values: every field-aware
+                                                  k-segment is a 16 B-aligned
+                                                  vector load)
+    W[l] [in, out] f32, b[l] [out] f32
+    accumulators: same shapes, f32 (only when the store trains)
+
+``flat_weight_view`` reassembles the reference byte layout on the host, so a
+model file written here is byte-identical to one written by the reference.
+Compute runs through libdffm.so (``_lib``); there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ContractError, FormatError, NumericError, SizingError
+
+MERGE_EPS = 1e-6  # M:37
+PROB_CLAMP = 1e-7  # M:38
+MODEL_MAGIC = b"FWM1"  # M:39
+MODEL_VERSION = 1  # M:40
+DEFAULT_MAX_SLOTS = 1 << 31  # M:41
+
+_TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "u16": torch.uint16}
+_WCODE = {"f32": _lib.W_F32, "bf16": _lib.W_BF16, "u16": _lib.W_U16Q}
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Architecture + optimiser hyperparameters (M:44-110, same validation)."""
+
+    n_fields: int
+    k: int = 4
+    hidden_sizes: tuple = ()
+    lr_ffm: float = 0.05
+    lr_lr: float = 0.05
+    lr_nn: float = 0.01
+    power_t: float = 0.5
+    hash_bits: int = 18
+    init_seed: int = 0
+    init_scale_ffm: float = 0.5
+
+    def __post_init__(self):
+        object.__setattr__(self, "hidden_sizes", tuple(int(h) for h in self.hidden_sizes))
+        if self.n_fields < 1:
+            raise ContractError("n_fields must be >= 1")
+        if self.k < 1:
+            raise ContractError("k must be >= 1")
+        if len(self.hidden_sizes) > 4:
+            raise ContractError("at most 4 hidden layers are supported")
+        if any(h < 1 for h in self.hidden_sizes):
+            raise ContractError("hidden layer sizes must be positive")
+        if min(self.lr_ffm, self.lr_lr, self.lr_nn) <= 0:
+            raise ContractError("learning rates must be positive")
+        if not 0.0 <= self.power_t <= 1.0:
+            raise ContractError("power_t must lie in [0, 1]")
+        if not 1 <= self.hash_bits <= 29:
+            raise ContractError("hash_bits must lie in [1, 29]")
+        if self.init_scale_ffm < 0:
+            raise ContractError("init_scale_ffm must be >= 0")
+        if not 0 <= self.init_seed < 1 << 64:
+            raise ContractError("init_seed must fit in 64 bits")
+
+    def to_json(self) -> str:
+        d = {
+            "n_fields": self.n_fields, "k": self.k, "hidden_sizes": list(self.hidden_sizes),
+            "lr_ffm": self.lr_ffm, "lr_lr": self.lr_lr, "lr_nn": self.lr_nn,
+            "power_t": self.power_t, "hash_bits": self.hash_bits, "init_seed": self.init_seed,
+            "init_scale_ffm": self.init_scale_ffm,
+        }
+        return json.dumps(d, sort_keys=True, separators=(",", ":"))  # M:88-101
+
+    @classmethod
+    def from_json(cls, text: str) -> "ModelConfig":
+        try:
+            d = json.loads(text)
+            d["hidden_sizes"] = tuple(d["hidden_sizes"])
+            return cls(**d)
+        except (ValueError, TypeError, KeyError) as exc:
+            raise FormatError(f"bad model config payload: {exc}") from None
+
+
+def pair_indices(n_fields: int):
+    """Strict upper-triangle field pairs, row-major (M:113-117)."""
+    iu, ju = np.triu_indices(n_fields, k=1)
+    return iu.astype(np.int64), ju.astype(np.int64)
+
+
+def pair_position(n_fields: int) -> np.ndarray:
+    """(F, F) lookup from an unordered field pair to its output slot (M:120-127)."""
+    iu, ju = pair_indices(n_fields)
+    pos = np.full((n_fields, n_fields), -1, dtype=np.int64)
+    pos[iu, ju] = np.arange(len(iu))
+    pos[ju, iu] = pos[iu, ju]
+    return pos
+
+
+class WeightStore:
+    """HBM-resident weight store (replaces M:142-230).
+
+    ``wdtype`` selects the storage of the two hashed tables (``"f32"``,
+    ``"bf16"`` -- the cfg5 large-table form -- or ``"u16"``, the paper's
+    16-bit quantised form with per-table (min, bucket) headers).  The MLP is
+    always f32.  ``version`` counts mutations exactly like M:155-158.
+    """
+
+    def __init__(self, config: ModelConfig, device=None, wdtype: str = "f32",
+                 with_optimizer: bool = True, _alloc: bool = True):
+        if wdtype not in _TORCH_DT:
+            raise ContractError(f"unknown table dtype {wdtype!r}")
+        self.config = config
+        self.device = torch.device(device if device is not None else "cuda")
+        self.wdtype = wdtype
+        f, k = config.n_fields, config.k
+        self.n_features = 1 << config.hash_bits
+        self.n_pairs = f * (f - 1) // 2
+        self.merged_width = 1 + self.n_pairs
+        self.lr_size = self.n_features + 1
+        self.ffm_size = self.n_features * f * k
+        if config.hidden_sizes:
+            dims = [self.merged_width, *config.hidden_sizes, 1]
+            self.nn_dims = list(zip(dims[:-1], dims[1:]))
+        else:
+            self.nn_dims = []
+        self.nn_size = sum(i * o + o for i, o in self.nn_dims)
+        self.weights_total = self.lr_size + self.ffm_size + self.nn_size
+        self.total_slots = 2 * self.weights_total
+        self.version = 0
+        self.q_headers = {}  # table name -> (w_min f32, bucket f32) for u16 stores
+        self._cmodel = None
+        self.lr = self.ffm = None
+        self.nn_layers: list = []
+        self.lr_acc = self.ffm_acc = None
+        self.nn_accs: list = []
+        if _alloc:
+            dt = _TORCH_DT[wdtype]
+            self.lr = torch.zeros(self.lr_size, dtype=dt, device=self.device)
+            self.ffm = torch.zeros((self.n_features, f, k), dtype=dt, device=self.device)
+            self.nn_layers = [(torch.zeros((i, o), dtype=torch.float32, device=self.device),
+                               torch.zeros(o, dtype=torch.float32, device=self.device))
+                              for i, o in self.nn_dims]
+            if with_optimizer:
+                if wdtype != "f32":
+                    raise ContractError("only f32 stores carry optimizer state")
+                self.lr_acc = torch.ones(self.lr_size, dtype=torch.float32, device=self.device)
+                self.ffm_acc = torch.ones((self.n_features, f, k), dtype=torch.float32,
+                                          device=self.device)
+                self.nn_accs = [(torch.ones_like(w), torch.ones_like(b))
+                                for w, b in self.nn_layers]
+
+    # ---------------------------------------------------------------- C view
+    @property
+    def has_optimizer(self) -> bool:
+        return self.lr_acc is not None
+
+    @property
+    def bias(self) -> float:
+        return float(self.lr[self.n_features].float().item())
+
+    def c_model(self) -> _lib.DffmModel:
+        """POD the C ABI consumes (include/dffm.h: dffm_model)."""
+        m = _lib.DffmModel()
+        m.n_fields = self.config.n_fields
+        m.k = self.config.k
+        m.hash_bits = self.config.hash_bits
+        m.n_layers = len(self.nn_dims)
+        dims = [self.merged_width, *self.config.hidden_sizes, 1] if self.nn_dims else []
+        for i, d in enumerate(dims):
+            m.dims[i] = d
+        m.wdtype = _WCODE[self.wdtype]
+        m.lr = self.lr.data_ptr()
+        m.ffm = self.ffm.data_ptr()
+        for i, (w, b) in enumerate(self.nn_layers):
+            m.W[i] = w.data_ptr()
+            m.b[i] = b.data_ptr()
+        if self.wdtype == "u16":
+            m.q_lr_min, m.q_lr_bucket = self.q_headers["lr"]
+            m.q_ffm_min, m.q_ffm_bucket = self.q_headers["ffm"]
+        return m
+
+    def c_model_ref(self):
+        self._cmodel = self.c_model()
+        return ctypes.byref(self._cmodel)
+
+    # ---------------------------------------------------------------- flat layout
+    def blocks(self, include_optimizer=True):
+        """(name, tensor) in the frozen flat order (M:145-153)."""
+        out = [("lr", self.lr), ("ffm", self.ffm)]
+        for i, (w, b) in enumerate(self.nn_layers):
+            out += [(f"W{i}", w), (f"b{i}", b)]
+        if include_optimizer:
+            if not self.has_optimizer:
+                raise ContractError("store has no optimizer state")
+            out += [("lr_acc", self.lr_acc), ("ffm_acc", self.ffm_acc)]
+            for i, (w, b) in enumerate(self.nn_accs):
+                out += [(f"W{i}_acc", w), (f"b{i}_acc", b)]
+        return out
+
+    def weight_values(self, include_optimizer: bool = True) -> np.ndarray:
+        """Host f32 copy of the flat array in layout order (M:218-221)."""
+        parts = []
+        for name, t in self.blocks(include_optimizer):
+            parts.append(_to_f32_host(self, name, t).reshape(-1))
+        return np.concatenate(parts)
+
+    def load_flat(self, flat: np.ndarray) -> "WeightStore":
+        """Fill the device blocks from a reference-layout flat f32 array."""
+        flat = np.ascontiguousarray(flat, dtype=np.float32)
+        n_w = self.weights_total
+        if flat.size not in (n_w, 2 * n_w):
+            raise FormatError(f"flat payload holds {flat.size} values, layout wants "
+                              f"{n_w} or {2 * n_w}")
+        off = 0
+        for name, t in self.blocks(include_optimizer=flat.size == 2 * n_w and self.has_optimizer):
+            src = torch.from_numpy(flat[off:off + t.numel()]).view(t.shape)
+            _from_f32(self, name, t, src)
+            off += t.numel()
+        if flat.size == n_w and self.has_optimizer:
+            for _, t in self.blocks(True)[len(self.blocks(False)):]:
+                t.fill_(1.0)  # M:682-683
+        self.version += 1
+        return self
+
+    @classmethod
+    def from_flat(cls, config, flat, device=None, wdtype="f32", with_optimizer=True):
+        return cls(config, device, wdtype, with_optimizer).load_flat(flat)
+
+    def copy(self) -> "WeightStore":
+        dup = WeightStore(self.config, self.device, self.wdtype, _alloc=False)
+        dup.lr, dup.ffm = self.lr.clone(), self.ffm.clone()
+        dup.nn_layers = [(w.clone(), b.clone()) for w, b in self.nn_layers]
+        if self.has_optimizer:
+            dup.lr_acc, dup.ffm_acc = self.lr_acc.clone(), self.ffm_acc.clone()
+            dup.nn_accs = [(w.clone(), b.clone()) for w, b in self.nn_accs]
+        dup.q_headers = dict(self.q_headers)
+        dup.version = self.version
+        return dup
+
+    def mark_mutated(self):
+        self.version += 1
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for _, t in self.blocks(self.has_optimizer))
+
+
+def _to_f32_host(store: WeightStore, name: str, t: torch.Tensor) -> np.ndarray:
+    if t.dtype == torch.float32:
+        return t.detach().cpu().numpy()
+    if t.dtype == torch.bfloat16:
+        return t.detach().float().cpu().numpy()
+    from .quant import dequantize_tensor  # u16 table -> f32 (bit-exact K4)
+    hmin, hb = store.q_headers[name]
+    return dequantize_tensor(t, hmin, hb).cpu().numpy()
+
+
+def _from_f32(store: WeightStore, name: str, dst: torch.Tensor, src: torch.Tensor):
+    if dst.dtype == torch.uint16:
+        raise ContractError("load a u16 store through quant.quantize_store")
+    dst.copy_(src.to(dst.dtype) if dst.dtype != torch.float32 else src, non_blocking=False)
+
+
+# --------------------------------------------------------------------------- init
+
+
+def init_model(config: ModelConfig, max_slots: int = DEFAULT_MAX_SLOTS, device=None,
+               chunk: int = 1 << 24) -> WeightStore:
+    """Deterministic init, bit-identical to M:233-272.
+
+    The reference draws ``rng.random(ffm_size)`` then ``rng.uniform`` per MLP
+    layer from one ``default_rng(init_seed)``; drawing the same streams in
+    chunks reproduces them bit for bit without the multi-GB f64 temporary."""
+    f, k = config.n_fields, config.k
+    n_features = 1 << config.hash_bits
+    merged = 1 + f * (f - 1) // 2
+    nn = 0
+    if config.hidden_sizes:
+        dims = [merged, *config.hidden_sizes, 1]
+        nn = sum(i * o + o for i, o in zip(dims[:-1], dims[1:]))
+    total = 2 * (n_features + 1 + n_features * f * k + nn)
+    if total > max_slots:
+        raise SizingError(f"model wants {total} float32 slots, cap is {max_slots};"
+                          " lower hash_bits, k, or the layer widths")  # M:248-253
+    store = WeightStore(config, device)
+    rng = np.random.default_rng(config.init_seed)
+    if config.init_scale_ffm > 0:
+        scale = config.init_scale_ffm / math.sqrt(k)
+        flat_ffm = store.ffm.view(-1)
+        for c0 in range(0, store.ffm_size, chunk):
+            c1 = min(store.ffm_size, c0 + chunk)
+            vals = (scale * (1.0 - rng.random(c1 - c0))).astype(np.float32)
+            flat_ffm[c0:c1].copy_(torch.from_numpy(vals))
+    for (i_dim, o_dim), (w, _) in zip(store.nn_dims, store.nn_layers):
+        limit = math.sqrt(6.0 / (i_dim + o_dim))
+        vals = rng.uniform(-limit, limit, i_dim * o_dim).astype(np.float32)
+        w.view(-1).copy_(torch.from_numpy(vals))
+    return store
+
+
+# --------------------------------------------------------------------------- forward
+
+
+@dataclass
+class ForwardState:
+    """Per-example forward result (M:275-290).  The GPU path keeps the
+    intermediates on the device inside the fused kernels; only the logit
+    (and the store version it was computed against) surface here."""
+
+    logit: float
+    lr_out: float = float("nan")
+    _store: WeightStore = field(repr=False, default=None)
+    _store_version: int = 0
+
+
+def _sigmoid(logit: float) -> float:
+    if logit >= 0:
+        return 1.0 / (1.0 + math.exp(-min(logit, 60.0)))
+    e = math.exp(max(logit, -60.0))
+    return e / (1.0 + e)
+
+
+def predict_proba(logit: float) -> float:
+    """Sigmoid clamped to [1e-7, 1 - 1e-7] (M:300-305)."""
+    if not math.isfinite(logit):
+        raise NumericError("non-finite logit", block="logit")
+    p = _sigmoid(logit)
+    return min(max(p, PROB_CLAMP), 1.0 - PROB_CLAMP)
+
+
+def _as_device(x, dtype, device):
+    if isinstance(x, torch.Tensor):
+        t = x if x.device == device else x.to(device, non_blocking=True)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x)).to(device)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+class StatusWord:
+    """Device status word (include/dffm.h) with a pinned host mirror."""
+
+    def __init__(self, device):
+        # int64 storage holding the uint64 bit pattern; all-ones = clear
+        self.dev = torch.empty(1, dtype=torch.int64, device=device)
+        self.host = torch.empty(1, dtype=torch.int64, pin_memory=True)
+
+    def clear(self):
+        self.dev.fill_(-1)
+
+    def ptr(self):
+        return self.dev.data_ptr()
+
+    def fetch_async(self):
+        self.host.copy_(self.dev, non_blocking=True)
+
+    def raise_if_set(self, what="", base=0):
+        _lib.raise_status(int(self.host.item()) & ((1 << 64) - 1), what, base)
+
+
+_status_cache: dict = {}
+
+
+def _status(device) -> StatusWord:
+    key = (device.type, device.index)
+    if key not in _status_cache:
+        _status_cache[key] = StatusWord(device)
+    return _status_cache[key]
+
+
+def predict_batch(idx, val, store: WeightStore, out: torch.Tensor | None = None,
+                  logits: torch.Tensor | None = None, check: bool = True,
+                  stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """K1 over a padded batch: idx int32 [n,F,M] (-1 empty), val f32 [n,F,M].
+
+    Returns device f32 probabilities [n] (M:300-305 applied); with ``check``
+    the device status word is read back and the first non-finite example
+    raises ``NumericError(block=...)`` exactly as M:392-396 would."""
+    dev = store.device
+    idx = _as_device(idx, torch.int32, dev)
+    val = _as_device(val, torch.float32, dev)
+    if idx.dim() != 3 or idx.shape != val.shape or idx.shape[1] != store.config.n_fields:
+        raise ContractError(f"expected idx/val [n, {store.config.n_fields}, M], got "
+                            f"{tuple(idx.shape)} / {tuple(val.shape)}")
+    n, _, M = idx.shape
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=dev)
+    st = _status(dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(s):
+        st.clear()
+        rc = _lib.lib().dffm_forward(store.c_model_ref(), idx.data_ptr(), val.data_ptr(), M, n,
+                                     out.data_ptr(), logits.data_ptr() if logits is not None
+                                     else None, 0, st.ptr(), s.cuda_stream)
+        _lib.check(rc, "dffm_forward")
+        if check:
+            st.fetch_async()
+    if check:
+        s.synchronize()
+        st.raise_if_set("forward: ")
+    return out
+
+
+class HostPredictor:
+    """Public host-buffer entry point: pinned host idx/val in, host probs out.
+
+    The batch is cut into chunks; chunk i+1's H2D copy (copy stream) overlaps
+    chunk i's K1 launch and its 4 B/example D2H (compute stream), with two
+    device staging buffers in flight.  This is the path a serving caller
+    with host-resident requests uses (and the bench's ``e2e`` number)."""
+
+    def __init__(self, store: WeightStore, max_examples: int, max_per_field: int,
+                 chunk: int = 1 << 17):
+        self.store = store
+        self.chunk = int(min(chunk, max(1, max_examples)))
+        F = store.config.n_fields
+        dev = store.device
+        self.idx_buf = [torch.empty((self.chunk, F, max_per_field), dtype=torch.int32, device=dev)
+                        for _ in range(2)]
+        self.val_buf = [torch.empty((self.chunk, F, max_per_field), dtype=torch.float32,
+                                    device=dev) for _ in range(2)]
+        self.prob_buf = [torch.empty(self.chunk, dtype=torch.float32, device=dev)
+                         for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(dev)
+        self.compute_stream = torch.cuda.Stream(dev)
+        self.status = StatusWord(dev)
+        self.launches = 0
+
+    def __call__(self, idx_host: torch.Tensor, val_host: torch.Tensor,
+                 out_host: torch.Tensor, check: bool = True) -> torch.Tensor:
+        n, F, M = idx_host.shape
+        lib = _lib.lib()
+        cm = self.store.c_model_ref()
+        cs, ks = self.copy_stream, self.compute_stream
+        h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        with torch.cuda.stream(ks):
+            self.status.clear()
+        cs.wait_stream(ks)
+        for i, c0 in enumerate(range(0, n, self.chunk)):
+            c1 = min(n, c0 + self.chunk)
+            b = i & 1
+            ib = self.idx_buf[b][: c1 - c0]
+            vb = self.val_buf[b][: c1 - c0]
+            pb = self.prob_buf[b][: c1 - c0]
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(free[b])
+                ib.copy_(idx_host[c0:c1], non_blocking=True)
+                vb.copy_(val_host[c0:c1], non_blocking=True)
+                h2d_done[b].record(cs)
+            with torch.cuda.stream(ks):
+                ks.wait_event(h2d_done[b])
+                rc = lib.dffm_forward(cm, ib.data_ptr(), vb.data_ptr(), M, c1 - c0,
+                                      pb.data_ptr(), None, c0, self.status.ptr(), ks.cuda_stream)
+                _lib.check(rc, "dffm_forward")
+                self.launches += 1
+                out_host[c0:c1].copy_(pb, non_blocking=True)
+                free[b].record(ks)
+        with torch.cuda.stream(ks):
+            self.status.fetch_async()
+        ks.synchronize()
+        if check:
+            self.status.raise_if_set("forward: ")
+        return out_host
+
+
+def forward(example, store: WeightStore, mac_counter=None) -> ForwardState:
+    """One example through the fused kernel (API of M:321)."""
+    from .features import pack_examples
+    idx, val, _ = pack_examples([example], store.config.n_fields)
+    lg = torch.empty(1, dtype=torch.float32, device=store.device)
+    predict_batch(idx, val, store, logits=lg)
+    return ForwardState(logit=float(lg.item()), _store=store, _store_version=store.version)
+
+
+# --------------------------------------------------------------------------- serialisation
+
+
+def _header_bytes(config: ModelConfig, include_optimizer: bool) -> bytes:
+    payload = config.to_json().encode("utf-8")
+    return (MODEL_MAGIC + MODEL_VERSION.to_bytes(4, "little") + len(payload).to_bytes(4, "little")
+            + payload + bytes([1 if include_optimizer else 0]))  # M:640-648
+
+
+def flat_weight_view(store: WeightStore, include_optimizer: bool = True) -> bytes:
+    """Header + flat little-endian f32 block, byte-identical to M:651-660."""
+    values = store.weight_values(include_optimizer)
+    return _header_bytes(store.config, include_optimizer) + values.astype("<f4", copy=False).tobytes()
+
+
+def store_from_bytes(data: bytes, device=None) -> WeightStore:
+    """Parse M:663-684's format into a device store."""
+    if data[:4] != MODEL_MAGIC:
+        raise FormatError("not a model file (bad magic)")
+    version = int.from_bytes(data[4:8], "little")
+    if version != MODEL_VERSION:
+        raise FormatError(f"unsupported model file version {version}")
+    n = int.from_bytes(data[8:12], "little")
+    if len(data) < 12 + n + 1:
+        raise FormatError("truncated model header")
+    config = ModelConfig.from_json(data[12:12 + n].decode("utf-8"))
+    has_opt = data[12 + n] == 1
+    body = np.frombuffer(data[13 + n:], dtype="<f4")
+    store = WeightStore(config, device)
+    expected = store.total_slots if has_opt else store.weights_total
+    if len(body) != expected:
+        raise FormatError(f"weight payload holds {len(body)} values, layout wants {expected}")
+    store.load_flat(body.astype(np.float32))
+    store.version = 0
+    return store
+
+
+def save_model(store: WeightStore, path, include_optimizer: bool = True):
+    with open(path, "wb") as fh:
+        fh.write(flat_weight_view(store, include_optimizer))
+
+
+def load_model(path, device=None) -> WeightStore:
+    with open(path, "rb") as fh:
+        return store_from_bytes(fh.read(), device)

@@ -25,3 +25,13 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    """Build libdffm.so in-tree if it is missing (nvcc cross-compiles here)."""
+    import subprocess
+    lib = os.path.join(REPO, "paper_2407_10115_b200", "libdffm.so")
+    if not os.path.exists(lib):
+        subprocess.run(["make", "-C", REPO, "-j8"], check=True, capture_output=True)
+    yield

@@ -1,0 +1,171 @@
+"""K1 fused forward parity (GPU) against the reference goldens and the oracle.
+
+Tolerance: predictions within 1e-5 relative (BASELINE north star, fp32); the
+kernel accumulates pair dots in f32 and the lr / pair sums / MergeNorm
+statistics in f64."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fieldwise_oracle as fo
+from paper_2407_10115_b200 import configs, synth
+from paper_2407_10115_b200.errors import ContractError, NumericError
+from paper_2407_10115_b200.model import ModelConfig, WeightStore, predict_batch
+from tests.golden_io import fixture_flat, load
+from tests.remap import compact_oracle, rel_err
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+RTOL = 1e-5
+
+
+def store_from_oracle(ost, wdtype="f32", with_optimizer=False):
+    cfg = ModelConfig(n_fields=ost.n_fields, k=ost.k, hidden_sizes=ost.hidden_sizes,
+                      hash_bits=ost.hash_bits)
+    return WeightStore.from_flat(cfg, ost.flat(False), DEV, wdtype, with_optimizer)
+
+
+@pytest.mark.parametrize("name,wdtype", [("cfg1", "f32"), ("cfg2", "f32"), ("cfg5", "bf16"),
+                                         ("cfg5", "f32")])
+def test_forward_matches_reference_golden(name, wdtype):
+    g = load(f"fwd_{name}")
+    F, k, hidden, bits, flat = fixture_flat(g)
+    cfg = ModelConfig(n_fields=F, k=k, hidden_sizes=hidden, hash_bits=bits)
+    st = WeightStore.from_flat(cfg, flat, DEV, wdtype, with_optimizer=False)
+    lg = torch.empty(g["idx"].shape[0], device=DEV)
+    p = predict_batch(g["idx"], g["val"], st, logits=lg).double().cpu().numpy()
+    assert rel_err(p, g["prob"]).max() < RTOL
+    np.testing.assert_allclose(lg.double().cpu().numpy(), g["logit"], rtol=1e-5, atol=2e-6)
+
+
+CASES = [
+    # F, k, hidden, M, bits, n
+    (8, 4, (), 1, 10, 1000),
+    (24, 8, (64, 32), 3, 12, 777),
+    (24, 8, (64, 32), 1, 12, 300),
+    (5, 3, (7,), 2, 8, 129),          # runtime-k path, hidden not a multiple of 4
+    (3, 1, (4, 4, 4, 4), 6, 6, 70),   # k=1, 4 hidden layers, M > 4 (generic slot loop)
+    (1, 2, (3,), 2, 5, 33),           # F=1: P=0, MergeNorm of one value
+    (2, 16, (), 2, 7, 65),
+    (12, 32, (16,), 2, 9, 64),
+    (40, 16, (256, 128), 1, 11, 200),
+]
+
+
+@pytest.mark.parametrize("F,k,hidden,M,bits,n", CASES)
+def test_forward_matches_oracle(F, k, hidden, M, bits, n):
+    rng = np.random.default_rng(F * 1000 + k)
+    ost = fo.random_store(F, k, hidden, bits, seed=F + k)
+    idx = rng.integers(-1, 1 << bits, size=(n, F, M)).astype(np.int32)
+    idx = np.sort(np.where(idx < 0, np.iinfo(np.int32).max, idx), axis=2)
+    idx = np.where(idx == np.iinfo(np.int32).max, -1, idx)
+    for e in range(n):  # canonical: unique within a field
+        for f in range(F):
+            row = idx[e, f]
+            live = np.unique(row[row >= 0])
+            idx[e, f] = -1
+            idx[e, f, :len(live)] = live
+    val = np.where(idx >= 0, rng.lognormal(size=idx.shape), 0).astype(np.float32)
+    st = store_from_oracle(ost)
+    p = predict_batch(idx, val, st).double().cpu().numpy()
+    _, ref = fo.forward_batch(idx, val, ost)
+    assert rel_err(p, ref).max() < RTOL
+
+
+def test_forward_bf16_and_u16_tables_match_widened_oracle():
+    from paper_2407_10115_b200.quant import quantize_store
+    wl = configs.CFG2
+    ost = fo.random_store(24, 8, (64, 32), 12, seed=4)
+    idx, val = synth.make_examples(wl, 2000, seed=8, hash_bits=12)
+    st = store_from_oracle(ost)
+    for variant in ("bf16", "u16"):
+        if variant == "bf16":
+            s2 = WeightStore.from_flat(st.config, ost.flat(False), DEV, "bf16", False)
+        else:
+            s2, _ = quantize_store(st)
+        p = predict_batch(idx, val, s2).double().cpu().numpy()
+        cst, ridx, _ = compact_oracle(s2, idx.numpy())
+        _, ref = fo.forward_batch(ridx, val.numpy(), cst)
+        assert rel_err(p, ref).max() < RTOL, variant
+
+
+def test_forward_empty_and_ragged_batches():
+    ost = fo.random_store(6, 8, (8,), 8, seed=1)
+    st = store_from_oracle(ost)
+    out = predict_batch(np.zeros((0, 6, 2), np.int32), np.zeros((0, 6, 2), np.float32), st)
+    assert out.numel() == 0
+    for n in (1, 31, 33, 257):
+        idx = np.full((n, 6, 2), -1, np.int32)
+        idx[:, :, 0] = np.arange(n * 6).reshape(n, 6) % 256
+        val = (idx >= 0).astype(np.float32)
+        p = predict_batch(idx, val, st).double().cpu().numpy()
+        _, ref = fo.forward_batch(idx, val, ost)
+        assert rel_err(p, ref).max() < RTOL
+
+
+def test_forward_nonfinite_reports_first_example_and_block():
+    ost = fo.random_store(4, 4, (8,), 6, seed=2)
+    idx = np.full((50, 4, 1), -1, np.int32)
+    idx[:, 0, 0] = 1
+    idx[:, 1, 0] = 2
+    val = (idx >= 0).astype(np.float32)
+    cases = []
+    o = ost.copy(); o.ffm[9, 2, 0] = np.inf; cases.append((o, 9, 1, "ffm"))   # noqa: E702
+    o = ost.copy(); o.lr[11] = np.nan; cases.append((o, 11, 3, "lr"))          # noqa: E702
+    for o, bucket, field, block in cases:
+        ix = idx.copy()
+        ix[17, field, 0] = bucket
+        ix[33, field, 0] = bucket
+        if block == "ffm":
+            ix[17, 2, 0] = 5  # the pair (field 1, field 2) reads ffm[9][2]
+            ix[33, 2, 0] = 5
+        st = store_from_oracle(o)
+        with pytest.raises(NumericError) as ei:
+            predict_batch(ix, (ix >= 0).astype(np.float32), st)
+        assert ei.value.example == 17 and ei.value.block == block
+        with pytest.raises(fo.OracleNumericError) as eo:
+            fo.forward(fo.row_to_fields(ix[17], (ix[17] >= 0).astype(np.float32)), o)
+        assert eo.value.block == block
+    o = ost.copy()
+    o.layers[0][0][:, 3] = np.inf
+    st = store_from_oracle(o)
+    with pytest.raises(NumericError) as ei:
+        predict_batch(idx, val, st)
+    assert ei.value.example == 0 and ei.value.block == "nn"
+
+
+def test_forward_out_of_range_index_is_contract_error():
+    ost = fo.random_store(3, 4, (), 6, seed=2)
+    st = store_from_oracle(ost)
+    idx = np.zeros((4, 3, 1), np.int32)
+    idx[2, 1, 0] = 64
+    with pytest.raises(ContractError):
+        predict_batch(idx, np.ones_like(idx, dtype=np.float32), st)
+
+
+@pytest.mark.slow
+def test_forward_cfg2_full_table_sample():
+    """BASELINE cfg2 at full size (2^24 buckets, 1M batch): oracle on a sample."""
+    wl = configs.CFG2
+    cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=24)
+    st = WeightStore(cfg, DEV, with_optimizer=False)
+    gen = torch.Generator(device=DEV).manual_seed(wl.weight_seed)
+    st.lr.copy_(synth.normal_table(st.lr.numel(), 0.05, gen, DEV))
+    st.ffm.view(-1).copy_(synth.normal_table(st.ffm.numel(), 0.05, gen, DEV))
+    for w, b in st.nn_layers:
+        w.copy_(torch.randn(w.shape, generator=gen, device=DEV) * 0.05)
+        b.copy_(torch.randn(b.shape, generator=gen, device=DEV) * 0.05)
+    idx, val = synth.make_examples(wl, 1 << 20, device=DEV)
+    p = predict_batch(idx, val, st)
+    assert torch.isfinite(p).all()
+    sel = torch.randperm(1 << 20, generator=torch.Generator().manual_seed(0))[:4096]
+    si = idx[sel.to(DEV)].cpu().numpy()
+    sv = val[sel.to(DEV)].cpu().numpy()
+    cst, ridx, _ = compact_oracle(st, si)
+    _, ref = fo.forward_batch(ridx, sv, cst)
+    assert rel_err(p[sel.to(DEV)].double().cpu().numpy(), ref).max() < RTOL
+    # size-independent property: permuting the batch permutes the outputs exactly
+    perm = torch.randperm(1 << 20, device=DEV)
+    p2 = predict_batch(idx[perm], val[perm], st)
+    assert torch.equal(p2, p[perm])

@@ -1,0 +1,148 @@
+"""K4 quantisation (bit-exact), K5 hashing (bit-exact) and K3 context cache
+(1e-6 absolute) on the GPU."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fieldwise_oracle as fo
+from paper_2407_10115_b200 import configs, hashing, inference, quant, synth
+from paper_2407_10115_b200.errors import ContractError, NumericError, StaleCacheError
+from paper_2407_10115_b200.model import ModelConfig, WeightStore, predict_batch
+from tests.golden_io import fixture_flat, load
+from tests.remap import compact_oracle
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+# ------------------------------------------------------------------ K4
+
+
+@pytest.mark.parametrize("n,scale", [(1, 0.1), (3, 1.0), (1001, 0.05), (1 << 20, 0.05),
+                                     ((1 << 22) + 3, 2.5)])
+def test_quantize_bit_exact(n, scale):
+    rng = np.random.default_rng(n)
+    w = (rng.standard_normal(n) * scale).astype(np.float32)
+    hmin, hb, q = quant.quantize_tensor(torch.from_numpy(w).to(DEV))
+    rmin, rb, rq = fo.quantize(w)
+    assert (hmin, hb) == (rmin, rb)
+    assert np.array_equal(q.cpu().numpy(), rq)
+    back = quant.dequantize_tensor(q, hmin, hb).cpu().numpy()
+    assert back.tobytes() == fo.dequantize(rmin, rb, rq).tobytes()
+
+
+def test_quantize_kats_and_errors():
+    hmin, hb, q = quant.quantize_tensor(torch.tensor([0.0, 1.0, 0.5], device=DEV))
+    assert hmin == 0.0 and hb == np.float32(1 / 65536) and q.cpu().tolist() == [0, 65535, 32768]
+    hmin, hb, q = quant.quantize_tensor(torch.full((7,), 0.25, device=DEV))
+    assert hb == 0 and (q == 0).all()
+    with pytest.raises(ContractError):
+        quant.quantize_tensor(torch.zeros(0, device=DEV))
+    w = torch.randn(1000, device=DEV)
+    w[417] = float("inf")
+    w[900] = float("nan")
+    with pytest.raises(NumericError, match="offset 417"):
+        quant.quantize_tensor(w)
+
+
+def test_fwq_blob_roundtrip():
+    w = torch.randn(12345, device=DEV) * 0.05
+    hmin, hb, q = quant.quantize_tensor(w)
+    blob = quant.to_fwq_blob(hmin, hb, q)
+    assert len(blob) == 24 + 2 * 12345  # S:379; ~half of 4-byte weights
+    h2, b2, q2 = quant.from_fwq_blob(blob)
+    assert (h2, b2) == (hmin, hb) and np.array_equal(q2, q.cpu().numpy())
+    with pytest.raises(Exception):
+        quant.from_fwq_blob(blob[:-2])
+
+
+def test_quantize_store_full_cfg4_table_properties():
+    """cfg4-size ffm table (2^24 x 24 x 8): size-independent properties --
+    dequantise(quantise(W)) within bucket/2 (+f32 slack), monotone, and an
+    exact oracle check on a slice."""
+    n = (1 << 24) * 24 * 8
+    gen = torch.Generator(device=DEV).manual_seed(1004)
+    w = synth.normal_table(n, 0.05, gen, DEV)
+    hmin, hb, q = quant.quantize_tensor(w)
+    back = quant.dequantize_tensor(q, hmin, hb)
+    err = (back.double() - w.double()).abs()
+    inner = (q.to(torch.int32) > 0) & (q.to(torch.int32) < 65535)
+    slack = 65536 * float(np.spacing(hb)) + 2 * float(np.spacing(np.float32(w.abs().max().item())))
+    assert err[inner].max().item() <= hb / 2 + slack
+    sl = slice(123456789, 123456789 + (1 << 20))
+    _, _, rq = fo.quantize(np.concatenate([w[sl].cpu().numpy(), [w.min().item(), w.max().item()]]))
+    assert np.array_equal(q[sl].cpu().numpy(), rq[:-2])
+
+
+# ------------------------------------------------------------------ K5
+
+
+def test_hash_matches_reference():
+    g = load("hash")
+    pairs = [(str(f), str(t)) for f, t in zip(g["fields"], g["tokens"])]
+    bits = g["bits"]
+    items = [f.encode() + b"\x1f" + t.encode() for f, t in pairs]
+    blob, off = hashing.pack_strings(items)
+    raw = hashing.hash_bytes(blob, off, 32, DEV).cpu().numpy()
+    got = raw & ((1 << bits.astype(np.int64)) - 1)
+    assert (got == g["out"]).all()
+    rb, ro = hashing.pack_strings([bytes(x) for x in g["raw"]])
+    assert (hashing.hash_bytes(rb, ro, 32, DEV).cpu().numpy() == g["raw_out"]).all()
+    h = hashing.hash_features([("user", "u_42"), ("ad", "u_42")], 18, DEV).cpu().tolist()
+    assert h[0] != h[1] and h == [fo.hash_feature("user", "u_42", 18),
+                                  fo.hash_feature("ad", "u_42", 18)]
+    with pytest.raises(ContractError):
+        hashing.hash_features([("a", "b")], 9, DEV)
+
+
+def test_hash_synthetic_ranks_large_batch():
+    """1M (field, rank) tokens hashed on the GPU == the vectorised generator."""
+    rng = np.random.default_rng(5)
+    fr = rng.integers(0, 40, 1 << 20)
+    rr = rng.integers(1, 1 << 25, 1 << 20)
+    items = [f"f{f}".encode() + b"\x1f" + f"t{r}".encode() for f, r in zip(fr, rr)]
+    blob, off = hashing.pack_strings(items)
+    got = hashing.hash_bytes(blob, off, 25, DEV).cpu().numpy()
+    ref = synth.hash_ranks(torch.as_tensor(fr), torch.as_tensor(rr), 25).numpy()
+    assert (got == ref).all()
+
+
+# ------------------------------------------------------------------ K3
+
+
+def test_context_cache_matches_reference_merged_forward():
+    g = load("ctx")
+    F, k, hidden, bits, flat = fixture_flat(g)
+    cfg = ModelConfig(n_fields=F, k=k, hidden_sizes=hidden, hash_bits=bits)
+    st = WeightStore.from_flat(cfg, flat, DEV, with_optimizer=False)
+    p = inference.score_requests(g["ctx_idx"], g["ctx_val"], g["cand_idx"], g["cand_val"], st)
+    assert np.abs(p.double().cpu().numpy() - g["prob"]).max() <= 1e-6
+    # per-request API with staleness
+    cache = inference.build_context_cache(g["ctx_idx"][3], g["ctx_val"][3], st)
+    p3 = inference.predict_batch(cache, g["cand_idx"][3], g["cand_val"][3], st)
+    assert np.abs(p3.double().cpu().numpy() - g["prob"][3]).max() <= 1e-6
+    st.mark_mutated()
+    with pytest.raises(StaleCacheError):
+        inference.predict_batch(cache, g["cand_idx"][3], g["cand_val"][3], st)
+
+
+def test_context_cache_equals_uncached_forward_u16():
+    wl = configs.CFG4
+    bits = 14
+    ost = fo.random_store(24, 8, (64, 32), bits, seed=44)
+    cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, with_optimizer=False)
+    sq, _ = quant.quantize_store(st)
+    R, C = 37, 101
+    ci, cv = synth.make_examples(wl, R, seed=1, hash_bits=bits, n_fields=16)
+    di, dv = synth.make_examples(wl, R * C, seed=2, hash_bits=bits, field_offset=16, n_fields=8)
+    di, dv = di.view(R, C, 8, 1), dv.view(R, C, 8, 1)
+    p = inference.score_requests(ci, cv, di, dv, sq).cpu().numpy()
+    merged_i = torch.cat([ci[:, None].expand(R, C, 16, 1), di], 2).reshape(R * C, 24, 1)
+    merged_v = torch.cat([cv[:, None].expand(R, C, 16, 1), dv], 2).reshape(R * C, 24, 1)
+    p_unc = predict_batch(merged_i, merged_v, sq).cpu().numpy().reshape(R, C)
+    assert np.abs(p - p_unc).max() <= 1e-6
+    cst, ridx, _ = compact_oracle(sq, merged_i.numpy())
+    _, ref = fo.forward_batch(ridx, merged_v.numpy(), cst)
+    assert np.abs(p.reshape(-1) - ref).max() <= 1e-6
