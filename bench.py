@@ -147,12 +147,12 @@ def compact_oracle_store(store, idx_host):
     ost = fo.OracleStore.zeros(cfg.n_fields, cfg.k, cfg.hidden_sizes, bits)
     ut = torch.as_tensor(u, dtype=torch.int64, device=store.device)
     if store.wdtype == "u16":
-        from paper_2407_10115_b200.quant import dequantize_tensor
+        from paper_2407_10115_b200.quant import dequantize_tensor, take_rows
         hl, bl = store.q_headers["lr"]
         hf, bf = store.q_headers["ffm"]
-        ost.lr[: len(u)] = dequantize_tensor(store.lr[ut].contiguous(), hl, bl).cpu().numpy()
-        ost.lr[ost.n_features] = dequantize_tensor(store.lr[-1:].contiguous(), hl, bl).item()
-        ost.ffm[: len(u)] = dequantize_tensor(store.ffm[ut].contiguous(), hf, bf).cpu().numpy()
+        ost.lr[: len(u)] = dequantize_tensor(take_rows(store.lr, ut), hl, bl).cpu().numpy()
+        ost.lr[ost.n_features] = dequantize_tensor(take_rows(store.lr, ut[-1:] * 0 + store.n_features), hl, bl).item()
+        ost.ffm[: len(u)] = dequantize_tensor(take_rows(store.ffm, ut), hf, bf).cpu().numpy()
     else:
         ost.lr[: len(u)] = store.lr[ut].float().cpu().numpy()
         ost.lr[ost.n_features] = store.lr[-1].float().item()

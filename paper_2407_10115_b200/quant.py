@@ -79,6 +79,13 @@ def dequantize_tensor(q: torch.Tensor, hmin, hb) -> torch.Tensor:
     return out
 
 
+def take_rows(t: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
+    """t[rows] for any table dtype (torch has no CUDA indexing for uint16)."""
+    if t.dtype == torch.uint16:
+        return t.view(torch.int16)[rows].view(torch.uint16).contiguous()
+    return t[rows].contiguous()
+
+
 def quantize_store(store, alpha=DEFAULT_ALPHA, beta=DEFAULT_BETA):
     """f32 WeightStore -> serving store with u16 lr/ffm tables (dequantised
     inline by K1/K3) and MLP weights replaced by their dequantised values.

@@ -15,7 +15,6 @@ def compact_oracle(store, idx, extra_idx=None):
     Buckets are mapped to 0..U-1 in sorted order; the bias keeps its slot at
     the compact store's own 2^b.  Values are the device tables' f32 values
     (bf16 / u16 tables are widened / dequantised exactly as K1 does)."""
-    from paper_2407_10115_b200.model import _to_f32_host
     idx = np.asarray(idx)
     allidx = idx if extra_idx is None else np.concatenate([idx.ravel(), np.asarray(extra_idx).ravel()])
     u = np.unique(allidx[allidx >= 0])
@@ -24,12 +23,12 @@ def compact_oracle(store, idx, extra_idx=None):
     ost = fo.OracleStore.zeros(cfg.n_fields, cfg.k, cfg.hidden_sizes, bits)
     ut = torch.as_tensor(u, dtype=torch.int64, device=store.device)
     if store.wdtype == "u16":
-        from paper_2407_10115_b200.quant import dequantize_tensor
+        from paper_2407_10115_b200.quant import dequantize_tensor, take_rows
         hl, bl = store.q_headers["lr"]
         hf, bf = store.q_headers["ffm"]
-        lr_rows = dequantize_tensor(store.lr[ut].contiguous(), hl, bl).cpu().numpy()
-        bias = dequantize_tensor(store.lr[-1:].contiguous(), hl, bl).cpu().numpy()[0]
-        ffm_rows = dequantize_tensor(store.ffm[ut].contiguous(), hf, bf).cpu().numpy()
+        lr_rows = dequantize_tensor(take_rows(store.lr, ut), hl, bl).cpu().numpy()
+        bias = dequantize_tensor(take_rows(store.lr, ut[-1:] * 0 + store.n_features), hl, bl).cpu().numpy()[0]
+        ffm_rows = dequantize_tensor(take_rows(store.ffm, ut), hf, bf).cpu().numpy()
     else:
         lr_rows = store.lr[ut].float().cpu().numpy()
         bias = store.lr[-1].float().item()
