@@ -50,6 +50,34 @@ int max_smem_optin_current() {
   return v;
 }
 
+int kernel_occupancy(const void* func, int threads, int smem, int* occ) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, int> attr_set, occ_cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int smax = max_smem_optin_current();
+  std::lock_guard<std::mutex> lk(mu);
+  const uint64_t fkey = ((uint64_t)(uintptr_t)func << 8) ^ (uint64_t)dev;
+  if (!attr_set.count(fkey)) {
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smax);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_set[fkey] = 1;
+  }
+  const uint64_t okey = fkey * 1315423911ull ^ ((uint64_t)smem << 40) ^ (uint64_t)threads;
+  auto it = occ_cache.find(okey);
+  if (it != occ_cache.end()) {
+    *occ = it->second;
+    return DFFM_OK;
+  }
+  int v = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, func, threads, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+  if (v < 1) v = 1;
+  occ_cache[okey] = v;
+  *occ = v;
+  return DFFM_OK;
+}
+
 }  // namespace dffm
 
 extern "C" {

@@ -14,6 +14,9 @@ void set_error(const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what);
 int sm_count_current();
 int max_smem_optin_current();
+// Raise the kernel's dynamic-smem limit to the device opt-in maximum (once per
+// kernel and device) and return resident blocks/SM for this smem size (cached).
+int kernel_occupancy(const void* func, int threads, int smem, int* occ);
 
 #define DFFM_CUDA_TRY(expr, what)                 \
   do {                                            \
@@ -31,19 +34,76 @@ struct Deq {
   float qmin, qb;  // u16 header (ignored for f32/bf16)
 };
 
+// Read-only streaming loads of table rows (L1::no_allocate keeps L1 for the
+// MLP weights).  Not volatile: the tables are immutable during a launch, so
+// the compiler may batch these loads ahead of their uses.
 __device__ __forceinline__ uint4 ldg_stream16(const void* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
   return r;
+}
+// 256-bit load (sm_100: LDG.E.ENL2.256): one k=8 f32 / k=16 bf16 segment
+__device__ __forceinline__ void ldg_stream32(const void* p, uint4& a, uint4& b) {
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p));
 }
 __device__ __forceinline__ uint2 ldg_stream8(const void* p) {
   uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p));
   return r;
+}
+
+// ---- mbarrier / TMA-bulk / cp.async primitives (sm_90+, used on sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
@@ -104,7 +164,14 @@ template <int K, typename T>
 struct Seg {
   static constexpr int BYTES = K * (int)sizeof(T);
   __device__ __forceinline__ static void load(const T* p, float* o, const Deq& d, int) {
-    if constexpr (BYTES >= 16) {
+    if constexpr (BYTES >= 32) {
+      constexpr int PER = 16 / sizeof(T);
+      uint4 u[BYTES / 16];
+#pragma unroll
+      for (int c = 0; c < BYTES / 32; ++c) ldg_stream32(p + 2 * c * PER, u[2 * c], u[2 * c + 1]);
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c) unpack16<T>(u[c], o + c * PER, d);
+    } else if constexpr (BYTES == 16) {
       constexpr int PER = 16 / sizeof(T);
       uint4 u[BYTES / 16];
 #pragma unroll

@@ -206,39 +206,23 @@ static CtxKernel select_ctx(int K, int MU) {
 #define DFFM_SEL(KK)                                   \
   if (K == KK) {                                       \
     if (MU == 1) return ctx_kernel<KK, 1, T>;          \
+    if (MU == 2) return ctx_kernel<KK, 2, T>;          \
+    if (MU == 3) return ctx_kernel<KK, 3, T>;          \
     if (MU == 4) return ctx_kernel<KK, 4, T>;          \
     return ctx_kernel<KK, 0, T>;                       \
   }
   DFFM_SEL(4)
   DFFM_SEL(8)
   DFFM_SEL(16)
-  DFFM_SEL(32)
   DFFM_SEL(0)
 #undef DFFM_SEL
   return nullptr;
 }
 
 static int launch_ctx(CtxKernel kern, const CtxParams& q, int smem, cudaStream_t s) {
-  static std::mutex mu;
-  static std::unordered_map<uint64_t, int> occ_cache;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t key = ((uint64_t)(uintptr_t)kern * 1315423911u) ^ ((uint64_t)smem << 8) ^ dev;
   int occ = 0;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = occ_cache.find(key);
-    if (it != occ_cache.end()) {
-      occ = it->second;
-    } else {
-      DFFM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                    "cudaFuncSetAttribute(ctx)");
-      DFFM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, FWD_THREADS, smem),
-                    "occupancy(ctx)");
-      if (occ < 1) occ = 1;
-      occ_cache[key] = occ;
-    }
-  }
+  int rc = kernel_occupancy((const void*)kern, FWD_THREADS, smem, &occ);
+  if (rc) return rc;
   const int64_t grid = std::min<int64_t>(q.R, (int64_t)sm_count_current() * occ);
   kern<<<(unsigned)grid, FWD_THREADS, smem, s>>>(q);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(ctx)");
@@ -298,7 +282,7 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
     return DFFM_SIZING;
   }
   const int K = pick_k_template(p.k, model->wdtype);
-  const int MU = cand_m == 1 ? 1 : (cand_m <= 4 ? 4 : 0);
+  const int MU = cand_m <= 4 ? cand_m : 0;
   CtxKernel kern = nullptr;
   switch (model->wdtype) {
     case DFFM_W_F32: kern = select_ctx<float>(K, MU); break;

@@ -3,12 +3,62 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <stdlib.h>
+#include <string.h>
+
 #include "forward_kernel.cuh"
+#include "forward_tma.cuh"
 
 namespace dffm {
 
 template <typename T>
 int launch_forward_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s);
+template <typename T>
+int launch_forward_tma_t(const TmaParams& q, int K, int smem, cudaStream_t s);
+
+// DFFM_FORWARD_KERNEL=v1 forces the per-warp gather kernel (A/B measurements)
+static bool tma_forward_enabled() {
+  static int cached = -1;
+  if (cached < 0) {
+    const char* v = getenv("DFFM_FORWARD_KERNEL");
+    cached = (v && strcmp(v, "v1") == 0) ? 0 : 1;
+  }
+  return cached == 1;
+}
+
+// Pick K1 v2 (TMA ring) when the shape allows it; returns false to fall
+// through to fwd_kernel.
+static bool try_tma_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
+                            int* rc) {
+  if (!tma_forward_enabled()) return false;
+  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
+  const int k = p.k;
+  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
+  if (p.F * p.M > TMA_MAX_FM) return false;
+  for (int l = 1; l < p.n_layers; ++l)
+    if (p.dims[l] % 4) return false;
+  TmaParams q{};
+  q.row_bytes = p.F * k * esz;
+  q.rs = q.row_bytes + 16;
+  for (int TE = 32; TE >= 8; TE >>= 1) {
+    p.TE = TE;
+    p.XS = TE + 4;
+    const TmaSmem L0 = tma_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.rs, 0);
+    const int rows = (smax - L0.total) / q.rs;
+    if (rows < 2 * p.F * p.M) continue;  // at least two worst-case examples in flight
+    q.ring_rows = rows < 32767 ? rows : 32767;
+    q.f = p;
+    const TmaSmem L = tma_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.rs,
+                                      q.ring_rows);
+    switch (m->wdtype) {
+      case DFFM_W_F32: *rc = launch_forward_tma_t<float>(q, k, L.total, s); break;
+      case DFFM_W_BF16: *rc = launch_forward_tma_t<__nv_bfloat16>(q, k, L.total, s); break;
+      default: *rc = launch_forward_tma_t<uint16_t>(q, k, L.total, s); break;
+    }
+    return true;
+  }
+  return false;
+}
 
 // shared with ctx.cu: fills FwdParams' model part, validates
 int fill_model_params(const dffm_model* m, FwdParams& p) {
@@ -72,7 +122,7 @@ int fwd_dispatch(int wdtype, const FwdParams& p, int K, int MU, int smem, cudaSt
 
 int pick_k_template(int k, int wdtype) {
   const int esz = wdtype == DFFM_W_F32 ? 4 : 2;
-  if ((k == 4 || k == 8 || k == 16 || k == 32) && (k * esz) % 8 == 0) return k;
+  if ((k == 4 || k == 8 || k == 16) && (k * esz) % 8 == 0) return k;
   return 0;
 }
 
@@ -101,6 +151,7 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   p.status_base = status_base;
   p.M = max_per_field;
   const int smax = max_smem_optin_current();
+  if (try_tma_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   int TE = 32;
   FwdSmem L;
   for (;; TE >>= 1) {
@@ -114,6 +165,6 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
     return DFFM_SIZING;
   }
   const int K = pick_k_template(p.k, model->wdtype);
-  const int MU = p.M == 1 ? 1 : (p.M <= 4 ? 4 : 0);
+  const int MU = p.M <= 4 ? p.M : 0;
   return fwd_dispatch(model->wdtype, p, K, MU, L.total, (cudaStream_t)stream);
 }

@@ -80,18 +80,39 @@ __device__ __forceinline__ void accum_slots(const FwdParams& p, const int* si, c
   constexpr int KA = K ? K : 32;
   const int k = K ? K : p.k;
   const T* ffm = (const T*)p.ffm;
-  const int mlim = MU ? MU : M;
+  if constexpr (MU > 0 && K > 0) {
+    // all slot loads first (predicated, zero-filled), then the FMAs: the
+    // segment loads of both sides of a pair are in flight together
+    float seg[MU][KA];
+    float xs[MU];
 #pragma unroll
-  for (int m = 0; m < mlim; ++m) {
-    if (MU && m >= M) break;
-    const int j = si[m];
-    if (j < 0) continue;
-    const float x = sv[m];
-    float seg[KA];
-    Seg<K, T>::load(ffm + ((int64_t)j * p.F + fb) * k, seg, p.dffm, k);
+    for (int m = 0; m < MU; ++m) {
+      const int j = (m < M) ? si[m] : -1;
+      xs[m] = 0.f;
 #pragma unroll
-    for (int c = 0; c < KA; ++c)
-      if (K || c < k) acc[c] = fmaf(x, seg[c], acc[c]);
+      for (int c = 0; c < KA; ++c) seg[m][c] = 0.f;
+      if (j >= 0) {
+        xs[m] = sv[m];
+        Seg<K, T>::load(ffm + ((int64_t)j * p.F + fb) * k, seg[m], p.dffm, k);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MU; ++m)
+#pragma unroll
+      for (int c = 0; c < KA; ++c) acc[c] = fmaf(xs[m], seg[m][c], acc[c]);
+  } else {
+    const int mlim = MU ? MU : M;
+    for (int m = 0; m < mlim; ++m) {
+      if (MU && m >= M) break;
+      const int j = si[m];
+      if (j < 0) continue;
+      const float x = sv[m];
+      float seg[KA];
+      Seg<K, T>::load(ffm + ((int64_t)j * p.F + fb) * k, seg, p.dffm, k);
+#pragma unroll
+      for (int c = 0; c < KA; ++c)
+        if (K || c < k) acc[c] = fmaf(x, seg[c], acc[c]);
+    }
   }
 }
 
