@@ -195,6 +195,9 @@ struct Seg<0, T> {
   }
 };
 
+// np.maximum(z, 0.0) semantics (M:370): NaN propagates (fmaxf would drop it)
+__device__ __forceinline__ float relu_nan(float z) { return z != z ? z : fmaxf(z, 0.f); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -210,7 +210,7 @@ __device__ __forceinline__ void mlp_tile(const FwdParams& p, float* X, float* Ha
           if (!isfinite(acc0[c])) atomicOr(&flag[e0], 8);
           if (!isfinite(acc1[c])) atomicOr(&flag[e0 + 1], 8);
           *(float2*)(outb + (o0 + c) * XS + e0) =
-              make_float2(fmaxf(acc0[c], 0.f), fmaxf(acc1[c], 0.f));
+              make_float2(relu_nan(acc0[c]), relu_nan(acc1[c]));
         }
       }
     }

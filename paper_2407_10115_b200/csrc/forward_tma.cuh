@@ -361,10 +361,10 @@ fwd_tma_kernel(TmaParams q) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             float4 o;
-            o.x = fmaxf(acc[0][c], 0.f);
-            o.y = fmaxf(acc[1][c], 0.f);
-            o.z = fmaxf(acc[2][c], 0.f);
-            o.w = fmaxf(acc[3][c], 0.f);
+            o.x = relu_nan(acc[0][c]);
+            o.y = relu_nan(acc[1][c]);
+            o.z = relu_nan(acc[2][c]);
+            o.w = relu_nan(acc[3][c]);
 #pragma unroll
             for (int r = 0; r < 4; ++r)
               if (!isfinite(acc[r][c])) atomicOr(&flag[e0 + r], 8);
