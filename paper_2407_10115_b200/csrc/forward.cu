@@ -34,7 +34,8 @@ static bool try_tma_forward(const dffm_model* m, FwdParams& p, int smax, cudaStr
   const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
   const int k = p.k;
   if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
-  if (p.F * p.M > TMA_MAX_FM) return false;
+  if (p.F * p.M > TMA_MAX_FM || (p.F * p.M) % 4) return false;  // idx/val slots TMA'd
+  if (((uintptr_t)p.idx & 15) || ((uintptr_t)p.val & 15)) return false;
   for (int l = 1; l < p.n_layers; ++l)
     if (p.dims[l] % 4) return false;
   TmaParams q{};

@@ -36,6 +36,7 @@ constexpr int TMA_WARPS = 1 + TMA_NC + TMA_NM;
 constexpr int TMA_THREADS = TMA_WARPS * 32;
 constexpr int TMA_NS = 16;                          // example slots in flight
 constexpr int TMA_MAX_FM = 128;                     // padded slots per example
+constexpr int TMA_LA = TMA_NS / 2;                  // producer idx/val lookahead
 
 struct TmaParams {
   FwdParams f;
@@ -54,7 +55,7 @@ __host__ __device__ inline TmaSmem tma_smem_layout(int F, int M, int P, int D, i
   TmaSmem s;
   const int FM = F * M;
   int o = 0;
-  s.off_bar = o; o = align16(o + 8 * (2 * TMA_NS + 4));
+  s.off_bar = o; o = align16(o + 8 * (3 * TMA_NS + 4));
   s.off_pair = o; o = align16(o + P * 2);
   s.off_sidx = o; o = align16(o + TMA_NS * FM * 4);
   s.off_sval = o; o = align16(o + TMA_NS * FM * 4);
@@ -110,7 +111,8 @@ fwd_tma_kernel(TmaParams q) {
   const TmaSmem L = tma_smem_layout(F, M, P, D, TE, XS, p.hmax, q.rs, q.ring_rows);
   uint64_t* full = (uint64_t*)(smem + L.off_bar);
   uint64_t* empty = full + TMA_NS;
-  uint64_t* xfull = empty + TMA_NS;
+  uint64_t* metaf = empty + TMA_NS;
+  uint64_t* xfull = metaf + TMA_NS;
   uint64_t* xempty = xfull + 2;
   uint16_t* pairtab = (uint16_t*)(smem + L.off_pair);
   int* sidx_all = (int*)(smem + L.off_sidx);
@@ -137,6 +139,7 @@ fwd_tma_kernel(TmaParams q) {
     for (int s = 0; s < TMA_NS; ++s) {
       mbar_init(&full[s], 1 + 32);  // producer lane 0 (expect_tx) + 32 cp.async arrivals
       mbar_init(&empty[s], 1);
+      mbar_init(&metaf[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&xfull[b], TE);
@@ -154,36 +157,42 @@ fwd_tma_kernel(TmaParams q) {
 
   if (warp == 0) {
     // ======================================================== producer
+    // Two-stage lookahead: stage 1 TMA-copies example (le+LA)'s padded
+    // idx/val slots into its slot; stage 2 reads example le's (landed) slots,
+    // allocates ring rows and issues one bulk copy per feature row plus the
+    // cp.async LR words.  No dependent global load on the issue path.
     const T* ffm = (const T*)p.ffm;
     const int64_t row_elems = (int64_t)F * K;
+    const uint32_t slot_bytes = (uint32_t)FM * 4u;
     int64_t head = 0, tail = 0, ole = 0;
-    int ri[4];
-    float rv[4];
-    auto fetch = [&](int64_t le) {
-      const int64_t e = ((int64_t)blockIdx.x + (le / TE) * gridDim.x) * TE + le % TE;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int s = lane + 32 * c;
-        if (s < FM && e < p.n) {
-          ri[c] = __ldg(p.idx + e * FM + s);
-          rv[c] = __ldg(p.val + e * FM + s);
-        } else {
-          ri[c] = -1;
-          rv[c] = 0.f;
+    for (int64_t step = 0; step < my_ex + TMA_LA; ++step) {
+      const int64_t le1 = step;
+      if (le1 < my_ex && lane == 0) {
+        const int s1 = (int)(le1 % TMA_NS);
+        if (le1 >= TMA_NS) mbar_wait(&empty[s1], (uint32_t)(((le1 / TMA_NS) - 1) & 1));
+        const int64_t e1 = ((int64_t)blockIdx.x + (le1 / TE) * gridDim.x) * TE + le1 % TE;
+        const bool v1 = e1 < p.n;
+        svalid[s1] = v1;
+        mbar_arrive_expect_tx(&metaf[s1], v1 ? 2u * slot_bytes : 0u);
+        if (v1) {
+          tma_load_1d(sidx_all + s1 * FM, p.idx + e1 * FM, slot_bytes, &metaf[s1]);
+          tma_load_1d(sval_all + s1 * FM, p.val + e1 * FM, slot_bytes, &metaf[s1]);
         }
       }
-    };
-    if (my_ex > 0) fetch(0);
-    for (int64_t le = 0; le < my_ex; ++le) {
-      int ci[4];
-      float cv[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) { ci[c] = ri[c]; cv[c] = rv[c]; }
-      if (le + 1 < my_ex) fetch(le + 1);
+      __syncwarp();
+      const int64_t le = step - TMA_LA;
+      if (le < 0) continue;
+      const int s = (int)(le % TMA_NS);
+      mbar_wait(&metaf[s], (uint32_t)((le / TMA_NS) & 1));
       const int64_t e = ((int64_t)blockIdx.x + (le / TE) * gridDim.x) * TE + le % TE;
+      const int* sidx = sidx_all + s * FM;
+      const bool valid = svalid[s];
+      int ci[4];
       int cnt = 0, bad = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
+        const int sl = lane + 32 * c;
+        ci[c] = (valid && sl < FM) ? sidx[sl] : -1;
         if (ci[c] >= p.n_buckets || ci[c] < -1) { bad = 1; ci[c] = -1; }
         cnt += ci[c] >= 0;
       }
@@ -198,14 +207,11 @@ fwd_tma_kernel(TmaParams q) {
         if (lane >= o) incl += v;
       }
       const int total = __shfl_sync(0xffffffffu, incl, 31);
-      const int s = (int)(le % TMA_NS);
-      while (ole + TMA_NS <= le || head + total - tail > RR) {
+      while (head + total - tail > RR) {
         mbar_wait(&empty[ole % TMA_NS], (uint32_t)((ole / TMA_NS) & 1));
         tail = slot_end[ole % TMA_NS];
         ++ole;
       }
-      int* sidx = sidx_all + s * FM;
-      float* sval = sval_all + s * FM;
       int16_t* srow = srow_all + s * FM;
       uint32_t* slr = slr_all + s * FM;
       int64_t r = head + (incl - cnt);
@@ -213,16 +219,11 @@ fwd_tma_kernel(TmaParams q) {
       for (int c = 0; c < 4; ++c) {
         const int sl = lane + 32 * c;
         if (sl < FM) {
-          sidx[sl] = ci[c];
-          sval[sl] = cv[c];
           srow[sl] = ci[c] >= 0 ? (int16_t)(r % RR) : (int16_t)-1;
           if (ci[c] >= 0) ++r;
         }
       }
-      if (lane == 0) {
-        slot_end[s] = head + total;
-        svalid[s] = e < p.n;
-      }
+      if (lane == 0) slot_end[s] = head + total;
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)total * (uint32_t)q.row_bytes);
       __syncwarp();
@@ -257,21 +258,24 @@ fwd_tma_kernel(TmaParams q) {
       double* exd = exd_all + b * 2 * TE;
       int* flag = flag_all + b * TE;
       if (!svalid[s]) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
         zero_column(X, exd, flag, el, TE, XS, D, lane);
       } else {
+        // srow >= 0 marks a slot whose row (and LR word) the producer fetched
         const int* sidx = sidx_all + s * FM;
         const float* sval = sval_all + s * FM;
         const int16_t* srow = srow_all + s * FM;
         const uint32_t* slr = slr_all + s * FM;
         double lrs = 0.0;
         for (int sl = lane; sl < FM; sl += 32) {
-          const int j = sidx[sl];
-          if (j >= 0)
-            lrs += (double)sval[sl] * (double)lr_from_word<T>(slr[sl], j, p.dlr);  // M:338
+          if (srow[sl] >= 0)
+            lrs += (double)sval[sl] *
+                   (double)lr_from_word<T>(slr[sl], sidx[sl], p.dlr);  // M:338
         }
         for (int f = lane; f < F; f += 32) {
           unsigned char pr = 0;
-          for (int m = 0; m < M; ++m) pr |= (sidx[f * M + m] >= 0);
+          for (int m = 0; m < M; ++m) pr |= (srow[f * M + m] >= 0);
           spres[f] = pr;
         }
         const double lr_out = (double)bias + warp_sum(lrs);
@@ -311,13 +315,12 @@ fwd_tma_kernel(TmaParams q) {
           s1 += (double)pv;
           pbad |= !isfinite(pv);
         }
+        __syncwarp();  // ring rows and slot no longer read: hand them back early
+        if (lane == 0) mbar_arrive(&empty[s]);
         merge_finish(X, exd, flag, el, TE, XS, P, D, lane, lr_out, s1, pbad);
       }
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty[s]);
-        mbar_arrive(&xfull[b]);
-      }
+      if (lane == 0) mbar_arrive(&xfull[b]);
     }
   } else {
     // ======================================================== MLP warps
@@ -345,7 +348,7 @@ fwd_tma_kernel(TmaParams q) {
           for (int r = 0; r < 4; ++r) {
             acc[r][0] = bv.x; acc[r][1] = bv.y; acc[r][2] = bv.z; acc[r][3] = bv.w;
           }
-#pragma unroll 4
+#pragma unroll 8
           for (int i = 0; i < I; ++i) {
             const float4 x = *(const float4*)(xin + i * XS + e0);
             const float4 w = __ldg((const float4*)(W + (int64_t)i * O + o0));
