@@ -39,6 +39,10 @@ static bool try_tma_forward(const dffm_model* m, FwdParams& p, int smax, cudaStr
   for (int l = 1; l < p.n_layers; ++l)
     if (p.dims[l] % 4) return false;
   TmaParams q{};
+  {
+    const char* cm = getenv("DFFM_ROW_COPY");
+    q.copy_mode = (cm && strcmp(cm, "tma") == 0) ? 0 : 1;
+  }
   q.row_bytes = p.F * k * esz;
   q.rs = q.row_bytes + 16;
   for (int TE = 32; TE >= 8; TE >>= 1) {

@@ -43,10 +43,11 @@ struct TmaParams {
   int row_bytes;  // F * k * sizeof(T)
   int rs;         // ring row stride (row_bytes + 16: rotates banks row to row)
   int ring_rows;
+  int copy_mode;  // 0 = TMA bulk row copies, 1 = warp-cooperative cp.async 16 B
 };
 
 struct TmaSmem {
-  int off_bar, off_pair, off_sidx, off_sval, off_srow, off_slr, off_end, off_valid, off_pres,
+  int off_bar, off_pair, off_sidx, off_sval, off_srow, off_slr, off_end, off_valid, off_plist, off_pres,
       off_exd, off_flag, off_X, off_Ha, off_Hb, off_ring, total;
 };
 
@@ -63,6 +64,7 @@ __host__ __device__ inline TmaSmem tma_smem_layout(int F, int M, int P, int D, i
   s.off_slr = o; o = align16(o + TMA_NS * FM * 4);
   s.off_end = o; o = align16(o + TMA_NS * 8);
   s.off_valid = o; o = align16(o + TMA_NS * 4);
+  s.off_plist = o; o = align16(o + FM * 8);
   s.off_pres = o; o = align16(o + TMA_NC * F);
   s.off_exd = o; o = align16(o + 2 * 2 * TE * 8);
   s.off_flag = o; o = align16(o + 2 * TE * 4);
@@ -121,6 +123,7 @@ fwd_tma_kernel(TmaParams q) {
   uint32_t* slr_all = (uint32_t*)(smem + L.off_slr);
   int64_t* slot_end = (int64_t*)(smem + L.off_end);
   int* svalid = (int*)(smem + L.off_valid);
+  int2* plist = (int2*)(smem + L.off_plist);
   double* exd_all = (double*)(smem + L.off_exd);
   int* flag_all = (int*)(smem + L.off_flag);
   float* X_all = (float*)(smem + L.off_X);
@@ -225,20 +228,47 @@ fwd_tma_kernel(TmaParams q) {
       }
       if (lane == 0) slot_end[s] = head + total;
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)total * (uint32_t)q.row_bytes);
-      __syncwarp();
       r = head + (incl - cnt);
+      if (q.copy_mode == 0) {
+        // one 1-D TMA bulk copy per feature row
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)total * (uint32_t)q.row_bytes);
+        __syncwarp();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int sl = lane + 32 * c;
-        if (sl < FM && ci[c] >= 0) {
-          const int j = ci[c];
-          tma_load_1d(ring + (size_t)(r % RR) * RS, ffm + (int64_t)j * row_elems,
-                      (uint32_t)q.row_bytes, &full[s]);
-          const T* lp = lrt + j;
-          cp_async4(slr + sl, (const void*)((uintptr_t)lp & ~(uintptr_t)3));
-          ++r;
+        for (int c = 0; c < 4; ++c) {
+          const int sl = lane + 32 * c;
+          if (sl < FM && ci[c] >= 0) {
+            const int j = ci[c];
+            tma_load_1d(ring + (size_t)(r % RR) * RS, ffm + (int64_t)j * row_elems,
+                        (uint32_t)q.row_bytes, &full[s]);
+            cp_async4(slr + sl, (const void*)((uintptr_t)(lrt + j) & ~(uintptr_t)3));
+            ++r;
+          }
         }
+      } else {
+        // warp-cooperative 16-byte cp.async: all 32 lanes stream the rows'
+        // chunks (fully coalesced 512 B per warp instruction, no registers)
+        int pos = incl - cnt;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int sl = lane + 32 * c;
+          if (sl < FM && ci[c] >= 0) {
+            plist[pos++] = make_int2(ci[c], (int)(r % RR));
+            cp_async4(slr + sl, (const void*)((uintptr_t)(lrt + ci[c]) & ~(uintptr_t)3));
+            ++r;
+          }
+        }
+        __syncwarp();
+        const int CH = q.row_bytes >> 4;
+        int rr = lane / CH, ch = lane % CH;
+        for (int qd = lane; qd < total * CH; qd += 32) {
+          const int2 jr = plist[rr];
+          cp_async16(ring + (size_t)jr.y * RS + ch * 16,
+                     (const unsigned char*)(ffm + (int64_t)jr.x * row_elems) + ch * 16);
+          ch += 32;
+          while (ch >= CH) { ch -= CH; ++rr; }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
       }
       cp_async_arrive_noinc(&full[s]);
       head += total;
