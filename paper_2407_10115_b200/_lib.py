@@ -15,7 +15,8 @@ from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_uint8, c_uint
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdffm.so")
+LIB_PATH = os.environ.get("DFFM_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libdffm.so")
 MAX_LAYERS = 5
 
 OK, CONTRACT, FORMAT, NUMERIC, SIZING, CUDA = range(6)

@@ -50,6 +50,27 @@ __device__ __forceinline__ void ldg_stream32(const void* p, uint4& a, uint4& b) 
       : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
       : "l"(p));
 }
+// Predicated, branch-free variants: outputs are zero when !pred, so a whole
+// pair's slot loads are straight-line code the scheduler issues back to back.
+__device__ __forceinline__ void ldg_stream32_pred(const void* p, int pred, uint4& a, uint4& b) {
+  asm("{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %9, 0;\n\t"
+      "mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;\n\t"
+      "mov.b32 %4, 0; mov.b32 %5, 0; mov.b32 %6, 0; mov.b32 %7, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p), "r"(pred));
+}
+__device__ __forceinline__ uint4 ldg_stream16_pred(const void* p, int pred) {
+  uint4 r;
+  asm("{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "r"(pred));
+  return r;
+}
 __device__ __forceinline__ uint2 ldg_stream8(const void* p) {
   uint2 r;
   asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"

@@ -60,7 +60,7 @@ __host__ __device__ inline CtxSmem ctx_smem_layout(const CtxParams& q) {
 template <int K, int MU, typename T>
 __global__ void __launch_bounds__(FWD_THREADS)
 ctx_kernel(CtxParams q) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const FwdParams& p = q.f;
   const CtxSmem L = ctx_smem_layout(q);
   uint16_t* pairtab = (uint16_t*)(smem + L.b.off_pair);

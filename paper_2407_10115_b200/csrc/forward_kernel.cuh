@@ -29,6 +29,9 @@ namespace dffm {
 
 constexpr int FWD_THREADS = 256;
 constexpr int FWD_WARPS = FWD_THREADS / 32;
+#ifndef FWD_MIN_BLOCKS
+#define FWD_MIN_BLOCKS 2  // lets ptxas keep a whole pair's slot loads in flight (<=128 regs)
+#endif
 
 struct FwdParams {
   const int32_t* idx;
@@ -114,6 +117,62 @@ __device__ __forceinline__ void accum_slots(const FwdParams& p, const int* si, c
         if (K || c < k) acc[c] = fmaf(x, seg[c], acc[c]);
     }
   }
+}
+
+template <int NU>
+__device__ __forceinline__ void ldg_chunks_pred(const void* p, int pred, uint4* u) {
+  if constexpr (NU == 1) {
+    u[0] = ldg_stream16_pred(p, pred);
+  } else {
+#pragma unroll
+    for (int c = 0; c < NU; c += 2)
+      ldg_stream32_pred((const unsigned char*)p + 16 * c, pred, u[c], u[c + 1]);
+  }
+}
+
+// <S[fa][fb], S[fb][fa]> for one pair with every slot load of BOTH sides issued
+// before the first FMA (branch-free predicated 128/256-bit loads): one memory
+// round trip per pair instead of one per slot.
+template <int K, int MU, typename T>
+__device__ __forceinline__ float pair_dot_batched(const FwdParams& p, const int* sia,
+                                                  const float* sva, const int* sib,
+                                                  const float* svb, int M, int fa, int fb) {
+  constexpr int SEGB = K * (int)sizeof(T);
+  constexpr int NU = SEGB / 16;
+  constexpr int PER = 16 / (int)sizeof(T);
+  const T* ffm = (const T*)p.ffm;
+  uint4 ra[MU][NU], rb[MU][NU];
+  float xa[MU], xb[MU];
+#pragma unroll
+  for (int m = 0; m < MU; ++m) {
+    const int ja = (m < M) ? sia[m] : -1;
+    const int jb = (m < M) ? sib[m] : -1;
+    xa[m] = ja >= 0 ? sva[m] : 0.f;
+    xb[m] = jb >= 0 ? svb[m] : 0.f;
+    ldg_chunks_pred<NU>(ffm + ((int64_t)(ja > 0 ? ja : 0) * p.F + fb) * K, ja >= 0, ra[m]);
+    ldg_chunks_pred<NU>(ffm + ((int64_t)(jb > 0 ? jb : 0) * p.F + fa) * K, jb >= 0, rb[m]);
+  }
+  float a[K], b[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) { a[c] = 0.f; b[c] = 0.f; }
+#pragma unroll
+  for (int m = 0; m < MU; ++m) {
+    float sa[K], sb[K];
+#pragma unroll
+    for (int c = 0; c < NU; ++c) {
+      unpack16<T>(ra[m][c], sa + c * PER, p.dffm);
+      unpack16<T>(rb[m][c], sb + c * PER, p.dffm);
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      a[c] = fmaf(xa[m], sa[c], a[c]);
+      b[c] = fmaf(xb[m], sb[c], b[c]);
+    }
+  }
+  float pv = 0.f;
+#pragma unroll
+  for (int c = 0; c < K; ++c) pv = fmaf(a[c], b[c], pv);
+  return pv;
 }
 
 // MergeNorm tail for one example held by one warp (M:355-360).  The raw pair
@@ -276,9 +335,9 @@ __device__ __forceinline__ double stage_slots(const FwdParams& p, const int32_t*
 }
 
 template <int K, int MU, typename T>
-__global__ void __launch_bounds__(FWD_THREADS)
+__global__ void __launch_bounds__(FWD_THREADS, FWD_MIN_BLOCKS)
 fwd_kernel(FwdParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const FwdSmem L = fwd_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax);
   uint16_t* pairtab = (uint16_t*)(smem + L.off_pair);
   float* X = (float*)(smem + L.off_X);
@@ -328,15 +387,20 @@ fwd_kernel(FwdParams p) {
         const int f1 = pr & 0xFF, f2 = pr >> 8;
         float pv = 0.f;
         if (spres[f1] & spres[f2]) {  // inactive pairs stay exactly 0 (M:346-351)
-          float a[KA], bb[KA];
-#pragma unroll
-          for (int c = 0; c < KA; ++c) { a[c] = 0.f; bb[c] = 0.f; }
           const int M = p.M;
-          accum_slots<K, MU, T>(p, sidx + f1 * M, sval + f1 * M, M, f2, a);   // S[f1][f2]
-          accum_slots<K, MU, T>(p, sidx + f2 * M, sval + f2 * M, M, f1, bb);  // S[f2][f1]
+          if constexpr (K > 0 && MU > 0 && (K * sizeof(T)) % 16 == 0) {
+            pv = pair_dot_batched<K, MU, T>(p, sidx + f1 * M, sval + f1 * M, sidx + f2 * M,
+                                            sval + f2 * M, M, f1, f2);
+          } else {
+            float a[KA], bb[KA];
 #pragma unroll
-          for (int c = 0; c < KA; ++c)
-            if (K || c < k) pv = fmaf(a[c], bb[c], pv);
+            for (int c = 0; c < KA; ++c) { a[c] = 0.f; bb[c] = 0.f; }
+            accum_slots<K, MU, T>(p, sidx + f1 * M, sval + f1 * M, M, f2, a);   // S[f1][f2]
+            accum_slots<K, MU, T>(p, sidx + f2 * M, sval + f2 * M, M, f1, bb);  // S[f2][f1]
+#pragma unroll
+            for (int c = 0; c < KA; ++c)
+              if (K || c < k) pv = fmaf(a[c], bb[c], pv);
+          }
         }
         X[(pp + 1) * XS + el] = pv;
         s1 += (double)pv;
