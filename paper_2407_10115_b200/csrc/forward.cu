@@ -157,7 +157,15 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   p.M = max_per_field;
   const int smax = max_smem_optin_current();
   if (try_tma_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
-  int TE = 32;
+  // Tile width: 16 keeps the per-block footprint small enough that the MLP
+  // weights stay L1-resident next to three blocks per SM (DFFM_FWD_TE overrides).
+  static int te_env = -1;
+  if (te_env < 0) {
+    const char* v = getenv("DFFM_FWD_TE");
+    te_env = v ? atoi(v) : 16;
+    if (te_env < 2 || te_env > 64 || (te_env & 1)) te_env = 16;
+  }
+  int TE = te_env;
   FwdSmem L;
   for (;; TE >>= 1) {
     p.TE = TE;
