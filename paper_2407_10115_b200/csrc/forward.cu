@@ -8,6 +8,7 @@
 
 #include "forward_kernel.cuh"
 #include "forward_tma.cuh"
+#include "forward_ws.cuh"
 
 namespace dffm {
 
@@ -16,14 +17,46 @@ int launch_forward_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s
 template <typename T>
 int launch_forward_tma_t(const TmaParams& q, int K, int smem, cudaStream_t s);
 
-// DFFM_FORWARD_KERNEL=v1 forces the per-warp gather kernel (A/B measurements)
-static bool tma_forward_enabled() {
+template <typename T>
+int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s);
+
+// Kernel family: "ws" (default, K1 v3), "v1" (CTA-synchronous gather + MLP
+// tile), "tma" (TMA-ring producer/consumer).  DFFM_FORWARD_KERNEL selects one
+// for A/B measurements; shapes a family cannot take fall back to v1.
+enum FwdFamily { FAM_WS = 0, FAM_V1 = 1, FAM_TMA = 2 };
+static int forward_family() {
   static int cached = -1;
   if (cached < 0) {
     const char* v = getenv("DFFM_FORWARD_KERNEL");
-    cached = (v && strcmp(v, "v1") == 0) ? 0 : 1;
+    cached = FAM_WS;
+    if (v && strcmp(v, "v1") == 0) cached = FAM_V1;
+    if (v && strcmp(v, "tma") == 0) cached = FAM_TMA;
   }
-  return cached == 1;
+  return cached;
+}
+static bool tma_forward_enabled() { return forward_family() == FAM_TMA; }
+
+int pick_k_template(int k, int wdtype);
+
+static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc) {
+  if (forward_family() != FAM_WS) return false;
+  for (int l = 1; l < p.n_layers; ++l)
+    if (p.dims[l] % 4) return false;
+  for (int TE = 32; TE >= 8; TE >>= 1) {
+    p.TE = TE;
+    p.XS = TE + 4;
+    const WsSmem L = ws_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax);
+    if (L.total > smax) continue;
+    const int K = pick_k_template(p.k, m->wdtype);
+    const int MU = p.M <= 4 ? p.M : 0;
+    switch (m->wdtype) {
+      case DFFM_W_F32: *rc = launch_forward_ws_t<float>(p, K, MU, L.total, s); break;
+      case DFFM_W_BF16: *rc = launch_forward_ws_t<__nv_bfloat16>(p, K, MU, L.total, s); break;
+      default: *rc = launch_forward_ws_t<uint16_t>(p, K, MU, L.total, s); break;
+    }
+    return true;
+  }
+  return false;
 }
 
 // Pick K1 v2 (TMA ring) when the shape allows it; returns false to fall
@@ -156,6 +189,7 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   p.status_base = status_base;
   p.M = max_per_field;
   const int smax = max_smem_optin_current();
+  if (try_ws_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_tma_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   // Tile width: 16 keeps the per-block footprint small enough that the MLP
   // weights stay L1-resident next to three blocks per SM (DFFM_FWD_TE overrides).

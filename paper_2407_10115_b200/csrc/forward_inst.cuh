@@ -7,6 +7,7 @@
 
 #include "forward_kernel.cuh"
 #include "forward_tma.cuh"
+#include "forward_ws.cuh"
 
 namespace dffm {
 
@@ -74,5 +75,40 @@ int launch_forward_tma_t(const TmaParams& q, int K, int smem, cudaStream_t s) {
 }
 
 template int launch_forward_tma_t<DFFM_INST_T>(const TmaParams&, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------- K1 v3 (warp-specialised)
+template <typename T>
+static FwdKernel select_ws(int K, int MU) {
+#define DFFM_SEL(KK)                                   \
+  if (K == KK) {                                       \
+    if (MU == 1) return fwd_ws_kernel<KK, 1, T>;       \
+    if (MU == 2) return fwd_ws_kernel<KK, 2, T>;       \
+    if (MU == 3) return fwd_ws_kernel<KK, 3, T>;       \
+    if (MU == 4) return fwd_ws_kernel<KK, 4, T>;       \
+    return fwd_ws_kernel<KK, 0, T>;                    \
+  }
+  DFFM_SEL(4)
+  DFFM_SEL(8)
+  DFFM_SEL(16)
+  DFFM_SEL(0)
+#undef DFFM_SEL
+  return nullptr;
+}
+
+template <typename T>
+int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s) {
+  FwdKernel kern = select_ws<T>(K, MU);
+  if (!kern) { set_error("no forward kernel for k=%d", p.k); return DFFM_SIZING; }
+  int occ = 0;
+  int rc = kernel_occupancy((const void*)kern, WS_THREADS, smem, &occ);
+  if (rc) return rc;
+  const int64_t ntiles = (p.n + p.TE - 1) / p.TE;
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current() * occ);
+  kern<<<(unsigned)grid, WS_THREADS, smem, s>>>(p);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_ws)");
+  return DFFM_OK;
+}
+
+template int launch_forward_ws_t<DFFM_INST_T>(const FwdParams&, int, int, int, cudaStream_t);
 
 }  // namespace dffm

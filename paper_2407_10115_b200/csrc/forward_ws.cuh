@@ -1,0 +1,249 @@
+// K1 v3 (default): warp-specialised fused DeepFFM forward, one CTA per SM.
+//
+// Same math as fwd_kernel (forward_kernel.cuh; M:293-397).  Roles:
+//   WS_NG gather warps: each owns one example at a time -- stages its padded
+//     slots, gathers the LR weights, forms the DiagMask pairs with
+//     branch-free predicated 256-bit row-segment loads (every slot load of a
+//     pair in flight together), reduces MergeNorm in f64 and writes the
+//     standardised column into a double-buffered X tile; then arrives on the
+//     tile's `xfull` mbarrier.  Gather warps never stop for the MLP: they
+//     only wait when both X buffers are still being consumed.
+//   WS_NM MLP warps: per tile, register-tiled GEMMs (4 outputs x 4 examples
+//     per thread) through the hidden layers with the weights L1-resident
+//     (the CTA's shared footprint is kept small for that), the output unit,
+//     residual logit and clamped sigmoid; then release the buffer (`xempty`).
+// This removes v1's CTA-wide barrier between gathering and the MLP, and the
+// single-producer issue ceiling of the TMA-ring variant (forward_tma.cuh).
+#pragma once
+
+#include "forward_kernel.cuh"
+
+namespace dffm {
+
+#ifndef DFFM_WS_NG
+#define DFFM_WS_NG 20
+#endif
+constexpr int WS_NG = DFFM_WS_NG;
+constexpr int WS_NM = 4;
+constexpr int WS_THREADS = (WS_NG + WS_NM) * 32;
+
+struct WsSmem {
+  int off_bar, off_pair, off_sidx, off_sval, off_pres, off_exd, off_flag, off_X, off_Ha, off_Hb,
+      total;
+};
+
+__host__ __device__ inline WsSmem ws_smem_layout(int F, int M, int P, int D, int TE, int XS,
+                                                 int hmax) {
+  WsSmem s;
+  const int FM = F * M;
+  int o = 0;
+  s.off_bar = o; o = align16(o + 8 * 4);
+  s.off_pair = o; o = align16(o + P * 2);
+  s.off_sidx = o; o = align16(o + WS_NG * FM * 4);
+  s.off_sval = o; o = align16(o + WS_NG * FM * 4);
+  s.off_pres = o; o = align16(o + WS_NG * F);
+  s.off_exd = o; o = align16(o + 2 * 2 * TE * 8);
+  s.off_flag = o; o = align16(o + 2 * TE * 4);
+  s.off_X = o; o = align16(o + 2 * D * XS * 4);
+  s.off_Ha = o; o = align16(o + hmax * XS * 4);
+  s.off_Hb = o; o = align16(o + hmax * XS * 4);
+  s.total = o;
+  return s;
+}
+
+// MLP over one X tile by NM warps (thread index mt in [0, 32*NM)); named
+// barrier 1 synchronises the MLP warps between layers.
+template <int NM>
+__device__ __forceinline__ void mlp_warps_tile(const FwdParams& p, const float* xin,
+                                               const double* exd, int* flag, float* Ha,
+                                               float* Hb, int64_t base, int mt) {
+  const int TE = p.TE, XS = p.XS;
+  const int lane = mt & 31, mw = mt >> 5;
+  int I = p.D;
+  float* outb = Ha;
+  for (int l = 0; l + 1 < p.n_layers; ++l) {
+    const int O = p.dims[l + 1];
+    const float* __restrict__ W = p.W[l];
+    const float* __restrict__ bl = p.b[l];
+    const int O4 = O >> 2;
+    const int units = O4 * (TE >> 2);
+    for (int u = mt; u < units; u += 32 * NM) {
+      const int o0 = (u % O4) * 4, e0 = (u / O4) * 4;
+      const float4 bv = __ldg((const float4*)(bl + o0));
+      float acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        acc[r][0] = bv.x; acc[r][1] = bv.y; acc[r][2] = bv.z; acc[r][3] = bv.w;
+      }
+#pragma unroll 8
+      for (int i = 0; i < I; ++i) {
+        const float4 x = *(const float4*)(xin + i * XS + e0);
+        const float4 w = __ldg((const float4*)(W + (int64_t)i * O + o0));
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          acc[r][0] = fmaf(xs[r], w.x, acc[r][0]);
+          acc[r][1] = fmaf(xs[r], w.y, acc[r][1]);
+          acc[r][2] = fmaf(xs[r], w.z, acc[r][2]);
+          acc[r][3] = fmaf(xs[r], w.w, acc[r][3]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float4 o;
+        o.x = relu_nan(acc[0][c]);  // M:370
+        o.y = relu_nan(acc[1][c]);
+        o.z = relu_nan(acc[2][c]);
+        o.w = relu_nan(acc[3][c]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (!isfinite(acc[r][c])) atomicOr(&flag[e0 + r], 8);
+        *(float4*)(outb + (o0 + c) * XS + e0) = o;
+      }
+    }
+    named_bar_sync(1, 32 * NM);
+    xin = outb;
+    I = O;
+    outb = (outb == Ha) ? Hb : Ha;
+  }
+  for (int el = mw; el < TE; el += NM) {
+    const int64_t e = base + el;
+    if (e >= p.n) continue;
+    double nn = 0.0;
+    if (p.n_layers > 0) {
+      const float* __restrict__ Wo = p.W[p.n_layers - 1];
+      float sacc = 0.f;
+      for (int i = lane; i < I; i += 32) sacc = fmaf(xin[i * XS + el], __ldg(Wo + i), sacc);
+      sacc = warp_sumf(sacc);
+      nn = (double)sacc + (double)__ldg(p.b[p.n_layers - 1]);  // M:372-373
+    }
+    if (lane == 0) {
+      const double logit = nn + exd[el] + exd[TE + el];  // M:377
+      p.prob[e] = (float)sigmoid_clamped(logit);
+      if (p.logit) p.logit[e] = (float)logit;
+      if (!isfinite(logit)) {
+        const int fl = flag[el];
+        const int blk = (fl & 1) ? DFFM_BLOCK_LR : (fl & 2) ? DFFM_BLOCK_FFM
+                      : (fl & 4) ? DFFM_BLOCK_MERGE : (fl & 8) ? DFFM_BLOCK_NN
+                      : DFFM_BLOCK_LOGIT;
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(p.status_base + e, blk, DFFM_NUMERIC));
+      }
+    }
+  }
+  named_bar_sync(1, 32 * NM);  // Ha/Hb and this X buffer are free again
+}
+
+template <int K, int MU, typename T>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+fwd_ws_kernel(FwdParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int F = p.F, M = p.M, FM = F * M, P = p.P, D = p.D, TE = p.TE, XS = p.XS;
+  const WsSmem L = ws_smem_layout(F, M, P, D, TE, XS, p.hmax);
+  uint64_t* xfull = (uint64_t*)(smem + L.off_bar);
+  uint64_t* xempty = xfull + 2;
+  uint16_t* pairtab = (uint16_t*)(smem + L.off_pair);
+  double* exd_all = (double*)(smem + L.off_exd);
+  int* flag_all = (int*)(smem + L.off_flag);
+  float* X_all = (float*)(smem + L.off_X);
+  float* Ha = (float*)(smem + L.off_Ha);
+  float* Hb = (float*)(smem + L.off_Hb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int KA = K ? K : 32;
+  const int k = K ? K : p.k;
+
+  for (int f1 = threadIdx.x; f1 < F; f1 += WS_THREADS) {
+    const int base = f1 * F - f1 * (f1 + 1) / 2;
+    for (int f2 = f1 + 1; f2 < F; ++f2) pairtab[base + f2 - f1 - 1] = (uint16_t)(f1 | (f2 << 8));
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&xfull[b], TE);
+      mbar_init(&xempty[b], WS_NM);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int64_t ntiles = (p.n + TE - 1) / TE;
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_ex = my_tiles * TE;
+
+  if (warp < WS_NG) {
+    // ======================================================== gather warps
+    int* sidx = (int*)(smem + L.off_sidx) + warp * FM;
+    float* sval = (float*)(smem + L.off_sval) + warp * FM;
+    unsigned char* spres = smem + L.off_pres + warp * F;
+    const float bias = load_elem<T>((const T*)p.lr + p.n_buckets, p.dlr);
+    for (int64_t le = warp; le < my_ex; le += WS_NG) {
+      const int64_t ti = le / TE;
+      const int el = (int)(le % TE);
+      const int b = (int)(ti & 1);
+      const int64_t e = ((int64_t)blockIdx.x + ti * gridDim.x) * TE + el;
+      if (ti >= 2) mbar_wait(&xempty[b], (uint32_t)(((ti >> 1) - 1) & 1));
+      float* X = X_all + b * D * XS;
+      double* exd = exd_all + b * 2 * TE;
+      int* flag = flag_all + b * TE;
+      if (e >= p.n) {
+        zero_column(X, exd, flag, el, TE, XS, D, lane);
+      } else {
+        int bad = 0;
+        const double lrs = stage_slots<T>(p, p.idx + e * FM, p.val + e * FM, FM, sidx, sval,
+                                          lane, bad);
+        __syncwarp();
+        for (int f = lane; f < F; f += 32) {
+          unsigned char pr = 0;
+          for (int m = 0; m < M; ++m) pr |= (sidx[f * M + m] >= 0);
+          spres[f] = pr;
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0)
+          atomicMin((unsigned long long*)p.status,
+                    (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
+                                                   DFFM_CONTRACT));
+        const double lr_out = (double)bias + warp_sum(lrs);  // M:327, M:338
+        __syncwarp();
+        double s1 = 0.0;
+        int pbad = 0;
+        for (int pp = lane; pp < P; pp += 32) {
+          const uint32_t pr = pairtab[pp];
+          const int f1 = pr & 0xFF, f2 = pr >> 8;
+          float pv = 0.f;
+          if (spres[f1] & spres[f2]) {  // inactive pairs stay exactly 0 (M:346-351)
+            if constexpr (K > 0 && MU > 0 && (K * sizeof(T)) % 16 == 0) {
+              pv = pair_dot_batched<K, MU, T>(p, sidx + f1 * M, sval + f1 * M, sidx + f2 * M,
+                                              sval + f2 * M, M, f1, f2);
+            } else {
+              float a[KA], bb[KA];
+#pragma unroll
+              for (int c = 0; c < KA; ++c) { a[c] = 0.f; bb[c] = 0.f; }
+              accum_slots<K, MU, T>(p, sidx + f1 * M, sval + f1 * M, M, f2, a);
+              accum_slots<K, MU, T>(p, sidx + f2 * M, sval + f2 * M, M, f1, bb);
+#pragma unroll
+              for (int c = 0; c < KA; ++c)
+                if (K || c < k) pv = fmaf(a[c], bb[c], pv);
+            }
+          }
+          X[(pp + 1) * XS + el] = pv;
+          s1 += (double)pv;
+          pbad |= !isfinite(pv);
+        }
+        merge_finish(X, exd, flag, el, TE, XS, P, D, lane, lr_out, s1, pbad);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xfull[b]);
+    }
+  } else {
+    // ======================================================== MLP warps
+    const int mt = threadIdx.x - WS_NG * 32;
+    for (int64_t ti = 0; ti < my_tiles; ++ti) {
+      const int b = (int)(ti & 1);
+      mbar_wait(&xfull[b], (uint32_t)((ti >> 1) & 1));
+      const int64_t base = ((int64_t)blockIdx.x + ti * gridDim.x) * TE;
+      mlp_warps_tile<WS_NM>(p, X_all + b * D * XS, exd_all + b * 2 * TE, flag_all + b * TE, Ha,
+                            Hb, base, mt);
+      if ((mt & 31) == 0) mbar_arrive(&xempty[b]);
+    }
+  }
+}
+
+}  // namespace dffm
