@@ -21,7 +21,7 @@
 namespace dffm {
 
 #ifndef DFFM_WS_NG
-#define DFFM_WS_NG 20
+#define DFFM_WS_NG 16
 #endif
 constexpr int WS_NG = DFFM_WS_NG;
 constexpr int WS_NM = 4;
@@ -174,12 +174,40 @@ fwd_ws_kernel(FwdParams p) {
     int* sidx = (int*)(smem + L.off_sidx) + warp * FM;
     float* sval = (float*)(smem + L.off_sval) + warp * FM;
     unsigned char* spres = smem + L.off_pres + warp * F;
-    const float bias = load_elem<T>((const T*)p.lr + p.n_buckets, p.dlr);
+    const T* lrt = (const T*)p.lr;
+    const float bias = load_elem<T>(lrt + p.n_buckets, p.dlr);
+    // Software pipeline across this warp's examples: the NEXT example's
+    // padded slots are loaded into registers while the current one's pairs
+    // are formed, and each example's LR loads are issued at its start but
+    // consumed only at MergeNorm, so only the pair gathers sit on the
+    // critical path.  FM <= 128 -> at most 4 slots per lane.
+    constexpr int SPL = 4;
+    int nidx[SPL];
+    float nval[SPL];
+    auto ex_of = [&](int64_t le) {
+      return ((int64_t)blockIdx.x + (le / TE) * gridDim.x) * TE + le % TE;
+    };
+    auto prefetch = [&](int64_t le) {
+      const int64_t e = le < my_ex ? ex_of(le) : p.n;
+#pragma unroll
+      for (int c = 0; c < SPL; ++c) {
+        const int s = lane + 32 * c;
+        const bool ok = e < p.n && s < FM;
+        nidx[c] = ok ? __ldg(p.idx + e * FM + s) : -1;
+        nval[c] = ok ? __ldg(p.val + e * FM + s) : 0.f;
+      }
+    };
+    prefetch(warp);
     for (int64_t le = warp; le < my_ex; le += WS_NG) {
       const int64_t ti = le / TE;
       const int el = (int)(le % TE);
       const int b = (int)(ti & 1);
-      const int64_t e = ((int64_t)blockIdx.x + ti * gridDim.x) * TE + el;
+      const int64_t e = ex_of(le);
+      int cidx[SPL];
+      float cval[SPL];
+#pragma unroll
+      for (int c = 0; c < SPL; ++c) { cidx[c] = nidx[c]; cval[c] = nval[c]; }
+      prefetch(le + WS_NG);
       if (ti >= 2) mbar_wait(&xempty[b], (uint32_t)(((ti >> 1) - 1) & 1));
       float* X = X_all + b * D * XS;
       double* exd = exd_all + b * 2 * TE;
@@ -188,8 +216,16 @@ fwd_ws_kernel(FwdParams p) {
         zero_column(X, exd, flag, el, TE, XS, D, lane);
       } else {
         int bad = 0;
-        const double lrs = stage_slots<T>(p, p.idx + e * FM, p.val + e * FM, FM, sidx, sval,
-                                          lane, bad);
+        float lrw[SPL];
+#pragma unroll
+        for (int c = 0; c < SPL; ++c) {
+          const int s = lane + 32 * c;
+          int j = cidx[c];
+          if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
+          if (s < FM) { sidx[s] = j; sval[s] = cval[c]; }
+          lrw[c] = j >= 0 ? load_elem<T>(lrt + j, p.dlr) : 0.f;  // consumed at merge time
+          cidx[c] = j;
+        }
         __syncwarp();
         for (int f = lane; f < F; f += 32) {
           unsigned char pr = 0;
@@ -200,7 +236,6 @@ fwd_ws_kernel(FwdParams p) {
           atomicMin((unsigned long long*)p.status,
                     (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
                                                    DFFM_CONTRACT));
-        const double lr_out = (double)bias + warp_sum(lrs);  // M:327, M:338
         __syncwarp();
         double s1 = 0.0;
         int pbad = 0;
@@ -227,6 +262,11 @@ fwd_ws_kernel(FwdParams p) {
           s1 += (double)pv;
           pbad |= !isfinite(pv);
         }
+        double lrs = 0.0;
+#pragma unroll
+        for (int c = 0; c < SPL; ++c)
+          if (cidx[c] >= 0) lrs += (double)cval[c] * (double)lrw[c];  // M:338
+        const double lr_out = (double)bias + warp_sum(lrs);          // M:327
         merge_finish(X, exd, flag, el, TE, XS, P, D, lane, lr_out, s1, pbad);
       }
       __syncwarp();
