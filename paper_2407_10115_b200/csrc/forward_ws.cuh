@@ -181,41 +181,23 @@ fwd_ws_kernel(FwdParams p) {
     // are formed, and each example's LR loads are issued at its start but
     // consumed only at MergeNorm, so only the pair gathers sit on the
     // critical path.  FM <= 128 -> at most 4 slots per lane.
-    // Two examples ahead: the slots of example le+2*NG are loaded into
-    // registers, and the whole latent rows of example le+NG (whose slots
-    // arrived one iteration ago) are prefetched into L2 line by line, so the
-    // scattered pair-segment gathers of the next example hit L2 and DRAM sees
-    // full-line, row-contiguous requests.
     constexpr int SPL = 4;
-    int n1idx[SPL], n2idx[SPL];
-    float n1val[SPL], n2val[SPL];
-    const int row_bytes = F * k * (int)sizeof(T);
+    int nidx[SPL];
+    float nval[SPL];
     auto ex_of = [&](int64_t le) {
       return ((int64_t)blockIdx.x + (le / TE) * gridDim.x) * TE + le % TE;
     };
-    auto load_slots = [&](int64_t le, int* ri, float* rv) {
+    auto prefetch = [&](int64_t le) {
       const int64_t e = le < my_ex ? ex_of(le) : p.n;
 #pragma unroll
       for (int c = 0; c < SPL; ++c) {
         const int s = lane + 32 * c;
         const bool ok = e < p.n && s < FM;
-        ri[c] = ok ? __ldg(p.idx + e * FM + s) : -1;
-        rv[c] = ok ? __ldg(p.val + e * FM + s) : 0.f;
+        nidx[c] = ok ? __ldg(p.idx + e * FM + s) : -1;
+        nval[c] = ok ? __ldg(p.val + e * FM + s) : 0.f;
       }
     };
-    auto prefetch_rows = [&](const int* ri) {
-#pragma unroll
-      for (int c = 0; c < SPL; ++c) {
-        const int j = ri[c];
-        if (j >= 0 && j < p.n_buckets) {
-          const unsigned char* row = (const unsigned char*)((const T*)p.ffm + (int64_t)j * F * k);
-          for (int off = 0; off < row_bytes; off += 128) prefetch_l2(row + off);
-        }
-      }
-    };
-    load_slots(warp, n1idx, n1val);
-    load_slots(warp + WS_NG, n2idx, n2val);
-    prefetch_rows(n1idx);
+    prefetch(warp);
     for (int64_t le = warp; le < my_ex; le += WS_NG) {
       const int64_t ti = le / TE;
       const int el = (int)(le % TE);
@@ -224,12 +206,8 @@ fwd_ws_kernel(FwdParams p) {
       int cidx[SPL];
       float cval[SPL];
 #pragma unroll
-      for (int c = 0; c < SPL; ++c) {
-        cidx[c] = n1idx[c]; cval[c] = n1val[c];
-        n1idx[c] = n2idx[c]; n1val[c] = n2val[c];
-      }
-      load_slots(le + 2 * WS_NG, n2idx, n2val);
-      prefetch_rows(n1idx);
+      for (int c = 0; c < SPL; ++c) { cidx[c] = nidx[c]; cval[c] = nval[c]; }
+      prefetch(le + WS_NG);
       if (ti >= 2) mbar_wait(&xempty[b], (uint32_t)(((ti >> 1) - 1) & 1));
       float* X = X_all + b * D * XS;
       double* exd = exd_all + b * 2 * TE;
