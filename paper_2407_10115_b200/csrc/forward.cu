@@ -9,6 +9,7 @@
 #include "forward_kernel.cuh"
 #include "forward_tma.cuh"
 #include "forward_ws.cuh"
+#include "forward_rows.cuh"
 
 namespace dffm {
 
@@ -23,12 +24,16 @@ int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_
 // Kernel family: "ws" (default, K1 v3), "v1" (CTA-synchronous gather + MLP
 // tile), "tma" (TMA-ring producer/consumer).  DFFM_FORWARD_KERNEL selects one
 // for A/B measurements; shapes a family cannot take fall back to v1.
-enum FwdFamily { FAM_WS = 0, FAM_V1 = 1, FAM_TMA = 2 };
+template <typename T>
+int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s);
+
+enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3 };
 static int forward_family() {
   static int cached = -1;
   if (cached < 0) {
     const char* v = getenv("DFFM_FORWARD_KERNEL");
-    cached = FAM_WS;
+    cached = FAM_ROWS;
+    if (v && strcmp(v, "ws") == 0) cached = FAM_WS;
     if (v && strcmp(v, "v1") == 0) cached = FAM_V1;
     if (v && strcmp(v, "tma") == 0) cached = FAM_TMA;
   }
@@ -38,8 +43,39 @@ static bool tma_forward_enabled() { return forward_family() == FAM_TMA; }
 
 int pick_k_template(int k, int wdtype);
 
+// K1 v4: row-coalesced gather (F <= 32, 16/32/64-byte segments)
+static bool try_rows_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
+                             int* rc) {
+  if (forward_family() != FAM_ROWS) return false;
+  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
+  const int k = p.k;
+  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
+  if (p.F > 32 || p.F * p.M > 128) return false;
+  for (int l = 1; l < p.n_layers; ++l)
+    if (p.dims[l] % 4) return false;
+  static int te_env = -1;
+  if (te_env < 0) {
+    const char* v = getenv("DFFM_ROWS_TE");
+    te_env = v ? atoi(v) : 16;
+    if (te_env < 4 || te_env > 64 || (te_env & 3)) te_env = 16;
+  }
+  for (int TE = te_env; TE >= 4; TE >>= 1) {
+    p.TE = TE;
+    p.XS = TE + 4;
+    const RwSmem L = rw_smem_layout(p.F, p.M, p.P, p.D, k, p.TE, p.XS, p.hmax);
+    if (L.total > smax) continue;
+    switch (m->wdtype) {
+      case DFFM_W_F32: *rc = launch_forward_rows_t<float>(p, k, L.total, s); break;
+      case DFFM_W_BF16: *rc = launch_forward_rows_t<__nv_bfloat16>(p, k, L.total, s); break;
+      default: *rc = launch_forward_rows_t<uint16_t>(p, k, L.total, s); break;
+    }
+    return true;
+  }
+  return false;
+}
+
 static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc) {
-  if (forward_family() != FAM_WS) return false;
+  if (forward_family() != FAM_WS && forward_family() != FAM_ROWS) return false;
   for (int l = 1; l < p.n_layers; ++l)
     if (p.dims[l] % 4) return false;
   for (int TE = 32; TE >= 8; TE >>= 1) {
@@ -189,6 +225,7 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   p.status_base = status_base;
   p.M = max_per_field;
   const int smax = max_smem_optin_current();
+  if (try_rows_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_ws_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_tma_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   // Tile width: 16 keeps the per-block footprint small enough that the MLP

@@ -8,6 +8,7 @@
 #include "forward_kernel.cuh"
 #include "forward_tma.cuh"
 #include "forward_ws.cuh"
+#include "forward_rows.cuh"
 
 namespace dffm {
 
@@ -110,5 +111,32 @@ int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_
 }
 
 template int launch_forward_ws_t<DFFM_INST_T>(const FwdParams&, int, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------- K1 v4 (row-coalesced)
+template <typename T>
+static FwdKernel select_rows(int K) {
+  if constexpr (sizeof(T) == 4) {
+    if (K == 4) return fwd_rows_kernel<4, T>;
+  }
+  if (K == 8) return fwd_rows_kernel<8, T>;
+  if (K == 16) return fwd_rows_kernel<16, T>;
+  return nullptr;
+}
+
+template <typename T>
+int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s) {
+  FwdKernel kern = select_rows<T>(K);
+  if (!kern) { set_error("no row-coalesced kernel for k=%d", K); return DFFM_SIZING; }
+  int occ = 0;
+  int rc = kernel_occupancy((const void*)kern, RW_THREADS, smem, &occ);
+  if (rc) return rc;
+  const int64_t ntiles = (p.n + p.TE - 1) / p.TE;
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current() * occ);
+  kern<<<(unsigned)grid, RW_THREADS, smem, s>>>(p);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rows)");
+  return DFFM_OK;
+}
+
+template int launch_forward_rows_t<DFFM_INST_T>(const FwdParams&, int, int, cudaStream_t);
 
 }  // namespace dffm
