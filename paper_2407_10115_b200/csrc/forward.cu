@@ -50,7 +50,7 @@ static bool try_rows_forward(const dffm_model* m, FwdParams& p, int smax, cudaSt
   const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
   const int k = p.k;
   if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
-  if (p.F > 32 || p.F * p.M > 128) return false;
+  if (p.F > 32 || p.M > 4 || p.F * p.M > 128) return false;
   for (int l = 1; l < p.n_layers; ++l)
     if (p.dims[l] % 4) return false;
   static int te_env = -1;

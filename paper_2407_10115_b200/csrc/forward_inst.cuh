@@ -113,19 +113,30 @@ int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_
 template int launch_forward_ws_t<DFFM_INST_T>(const FwdParams&, int, int, int, cudaStream_t);
 
 // ---------------------------------------------------------------- K1 v4 (row-coalesced)
-template <typename T>
-static FwdKernel select_rows(int K) {
-  if constexpr (sizeof(T) == 4) {
-    if (K == 4) return fwd_rows_kernel<4, T>;
+template <int K, typename T>
+static FwdKernel select_rows_m(int MU) {
+  switch (MU) {
+    case 1: return fwd_rows_kernel<K, 1, T>;
+    case 2: return fwd_rows_kernel<K, 2, T>;
+    case 3: return fwd_rows_kernel<K, 3, T>;
+    case 4: return fwd_rows_kernel<K, 4, T>;
+    default: return nullptr;
   }
-  if (K == 8) return fwd_rows_kernel<8, T>;
-  if (K == 16) return fwd_rows_kernel<16, T>;
+}
+
+template <typename T>
+static FwdKernel select_rows(int K, int MU) {
+  if constexpr (sizeof(T) == 4) {
+    if (K == 4) return select_rows_m<4, T>(MU);
+  }
+  if (K == 8) return select_rows_m<8, T>(MU);
+  if (K == 16) return select_rows_m<16, T>(MU);
   return nullptr;
 }
 
 template <typename T>
 int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s) {
-  FwdKernel kern = select_rows<T>(K);
+  FwdKernel kern = select_rows<T>(K, p.M);
   if (!kern) { set_error("no row-coalesced kernel for k=%d", K); return DFFM_SIZING; }
   int occ = 0;
   int rc = kernel_occupancy((const void*)kern, RW_THREADS, smem, &occ);

@@ -26,7 +26,7 @@ constexpr int RW_NM = 4;  // MLP warps
 constexpr int RW_THREADS = (RW_NG + RW_NM) * 32;
 
 struct RwSmem {
-  int off_bar, off_sidx, off_sval, off_pres, off_rowj, off_rowx, off_rowf, off_U, off_exd,
+  int off_bar, off_sidx, off_sval, off_pres, off_U, off_exd,
       off_flag, off_X, off_Ha, off_Hb, total;
 };
 
@@ -39,9 +39,6 @@ __host__ __device__ inline RwSmem rw_smem_layout(int F, int M, int P, int D, int
   s.off_sidx = o; o = align16(o + RW_NG * FM * 4);
   s.off_sval = o; o = align16(o + RW_NG * FM * 4);
   s.off_pres = o; o = align16(o + RW_NG * 32);
-  s.off_rowj = o; o = align16(o + RW_NG * FM * 4);
-  s.off_rowx = o; o = align16(o + RW_NG * FM * 4);
-  s.off_rowf = o; o = align16(o + RW_NG * FM);
   s.off_U = o; o = align16(o + RW_NG * P * k * 4);
   s.off_exd = o; o = align16(o + 2 * 2 * TE * 8);
   s.off_flag = o; o = align16(o + 2 * TE * 4);
@@ -56,16 +53,16 @@ __device__ __forceinline__ int pair_pos(int a, int b, int F) {  // a < b, M:113-
   return a * F - a * (a + 1) / 2 + (b - a - 1);
 }
 
-template <int K, typename T>
+template <int K, int MU, typename T>
 __global__ void __launch_bounds__(RW_THREADS, 1)
 fwd_rows_kernel(FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int SEGB = K * (int)sizeof(T);
   constexpr int NU = SEGB / 16;         // 16-byte chunks per segment
   constexpr int PER = 16 / (int)sizeof(T);
-  constexpr int W = 24 / NU;            // rows per wave (~96 registers of loads)
-  const int F = p.F, M = p.M, FM = F * M, P = p.P, D = p.D, TE = p.TE, XS = p.XS;
-  const RwSmem L = rw_smem_layout(F, M, P, D, K, TE, XS, p.hmax);
+  constexpr int FW = (24 / NU) / MU > 0 ? (24 / NU) / MU : 1;  // fields per wave (~96 regs)
+  const int F = p.F, FM = F * MU, P = p.P, D = p.D, TE = p.TE, XS = p.XS;
+  const RwSmem L = rw_smem_layout(F, MU, P, D, K, TE, XS, p.hmax);
   uint64_t* xfull = (uint64_t*)(smem + L.off_bar);
   uint64_t* xempty = xfull + 2;
   double* exd_all = (double*)(smem + L.off_exd);
@@ -93,9 +90,6 @@ fwd_rows_kernel(FwdParams p) {
     int* sidx = (int*)(smem + L.off_sidx) + warp * FM;
     float* sval = (float*)(smem + L.off_sval) + warp * FM;
     unsigned char* spres = smem + L.off_pres + warp * 32;
-    int* rowj = (int*)(smem + L.off_rowj) + warp * FM;
-    float* rowx = (float*)(smem + L.off_rowx) + warp * FM;
-    unsigned char* rowf = smem + L.off_rowf + warp * FM;
     float* U = (float*)(smem + L.off_U) + (size_t)warp * P * K;
     const T* lrt = (const T*)p.lr;
     const T* ffm = (const T*)p.ffm;
@@ -134,25 +128,17 @@ fwd_rows_kernel(FwdParams p) {
       if (e >= p.n) {
         zero_column(X, exd, flag, el, TE, XS, D, lane);
       } else {
-        // ---- stage slots, LR loads (consumed at merge), compact the row list
-        int bad = 0, nrows = 0;
+        // ---- stage slots; LR loads issued now, consumed at MergeNorm
+        int bad = 0;
         float lrw[SPL];
 #pragma unroll
         for (int c = 0; c < SPL; ++c) {
           const int s = lane + 32 * c;
           int j = cidx[c];
           if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
-          if (s < FM) { sidx[s] = j; sval[s] = cval[c]; }
+          if (s < FM) { sidx[s] = j; sval[s] = j >= 0 ? cval[c] : 0.f; }
           lrw[c] = j >= 0 ? load_elem<T>(lrt + j, p.dlr) : 0.f;
           cidx[c] = j;
-          const unsigned vb = __ballot_sync(0xffffffffu, s < FM && j >= 0);
-          if (s < FM && j >= 0) {
-            const int pos = nrows + __popc(vb & ((1u << lane) - 1u));
-            rowj[pos] = j;
-            rowx[pos] = cval[c];
-            rowf[pos] = (unsigned char)(s / M);
-          }
-          nrows += __popc(vb);
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0)
           atomicMin((unsigned long long*)p.status,
@@ -161,70 +147,71 @@ fwd_rows_kernel(FwdParams p) {
         __syncwarp();
         if (lane < F) {
           unsigned char pr = 0;
-          for (int m = 0; m < M; ++m) pr |= (sidx[lane * M + m] >= 0);
+#pragma unroll
+          for (int m = 0; m < MU; ++m) pr |= (sidx[lane * MU + m] >= 0);
           spres[lane] = pr;
         }
         __syncwarp();
         const bool my_pres = lane < F && spres[lane];
-        // ---- stream rows: lane g owns target segment g
-        float acc[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = 0.f;
-        int cur_f = 0;
+        const int gl = lane < F ? lane : 0;
         double s1 = 0.0;
         int pbad = 0;
-        auto flush = [&](int f) {  // field f complete: acc = S[f][lane]
-          const bool fp = spres[f];
-          if (lane < F && lane > f) {
-            float* u = U + pair_pos(f, lane, F) * K;
+        // ---- stream whole rows, FW fields (FW*MU slots) per wave; lane g
+        // owns target segment g; one flush per completed field
+        for (int f0 = 0; f0 < F; f0 += FW) {
+          uint4 raw[FW][MU][NU];
 #pragma unroll
-            for (int c = 0; c < K; c += 4)
-              *(float4*)(u + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          } else if (lane < f) {
-            const int pp = pair_pos(lane, f, F);
-            float pv = 0.f;
-            if (fp && my_pres) {  // inactive pairs stay exactly 0 (M:346-351)
-              const float* u = U + pp * K;  // S[lane][f]
+          for (int fw = 0; fw < FW; ++fw) {
 #pragma unroll
-              for (int c = 0; c < K; c += 4) {
-                const float4 a = *(const float4*)(u + c);
-                pv = fmaf(a.x, acc[c], pv);
-                pv = fmaf(a.y, acc[c + 1], pv);
-                pv = fmaf(a.z, acc[c + 2], pv);
-                pv = fmaf(a.w, acc[c + 3], pv);
-              }
+            for (int m = 0; m < MU; ++m) {
+              const int f = f0 + fw;
+              const int j = f < F ? sidx[f * MU + m] : -1;
+              ldg_chunks_pred<NU>(ffm + ((int64_t)(j > 0 ? j : 0) * F + gl) * K,
+                                  j >= 0 && lane < F, raw[fw][m]);
             }
-            X[(pp + 1) * XS + el] = pv;
-            s1 += (double)pv;
-            pbad |= !isfinite(pv);
           }
 #pragma unroll
-          for (int c = 0; c < K; ++c) acc[c] = 0.f;
-        };
-        for (int r0 = 0; r0 < nrows; r0 += W) {
-          uint4 raw[W][NU];
+          for (int fw = 0; fw < FW; ++fw) {
+            const int f = f0 + fw;
+            if (f >= F) break;
+            float acc[K];
 #pragma unroll
-          for (int u = 0; u < W; ++u) {
-            const int r = r0 + u;
-            const bool ok = r < nrows && lane < F;
-            const int j = r < nrows ? rowj[r] : 0;
-            ldg_chunks_pred<NU>(ffm + ((int64_t)j * F + (lane < F ? lane : 0)) * K, ok, raw[u]);
-          }
+            for (int c = 0; c < K; ++c) acc[c] = 0.f;
 #pragma unroll
-          for (int u = 0; u < W; ++u) {
-            const int r = r0 + u;
-            if (r >= nrows) break;
-            const int f = rowf[r];
-            while (cur_f < f) flush(cur_f++);
-            const float x = rowx[r];
-            float seg[K];
+            for (int m = 0; m < MU; ++m) {
+              const float x = sval[f * MU + m];
+              float seg[K];
 #pragma unroll
-            for (int c = 0; c < NU; ++c) unpack16<T>(raw[u][c], seg + c * PER, p.dffm);
+              for (int c = 0; c < NU; ++c) unpack16<T>(raw[fw][m][c], seg + c * PER, p.dffm);
 #pragma unroll
-            for (int c = 0; c < K; ++c) acc[c] = fmaf(x, seg[c], acc[c]);  // M:339
+              for (int c = 0; c < K; ++c) acc[c] = fmaf(x, seg[c], acc[c]);  // M:339
+            }
+            // field f complete: acc = S[f][lane]
+            if (lane < F && lane > f) {
+              float* u = U + pair_pos(f, lane, F) * K;
+#pragma unroll
+              for (int c = 0; c < K; c += 4)
+                *(float4*)(u + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            } else if (lane < f) {
+              const int pp = pair_pos(lane, f, F);
+              float pv = 0.f;
+              if (spres[f] && my_pres) {  // inactive pairs stay exactly 0 (M:346-351)
+                const float* u = U + pp * K;  // S[lane][f]
+#pragma unroll
+                for (int c = 0; c < K; c += 4) {
+                  const float4 a = *(const float4*)(u + c);
+                  pv = fmaf(a.x, acc[c], pv);
+                  pv = fmaf(a.y, acc[c + 1], pv);
+                  pv = fmaf(a.z, acc[c + 2], pv);
+                  pv = fmaf(a.w, acc[c + 3], pv);
+                }
+              }
+              X[(pp + 1) * XS + el] = pv;
+              s1 += (double)pv;
+              pbad |= !isfinite(pv);
+            }
           }
         }
-        while (cur_f < F) flush(cur_f++);
         __syncwarp();
         double lrs = 0.0;
 #pragma unroll
