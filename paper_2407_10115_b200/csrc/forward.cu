@@ -32,8 +32,8 @@ static int forward_family() {
   static int cached = -1;
   if (cached < 0) {
     const char* v = getenv("DFFM_FORWARD_KERNEL");
-    cached = FAM_ROWS;
-    if (v && strcmp(v, "ws") == 0) cached = FAM_WS;
+    cached = FAM_WS;  // measured fastest on cfg2 (see profiles/)
+    if (v && strcmp(v, "rows") == 0) cached = FAM_ROWS;
     if (v && strcmp(v, "v1") == 0) cached = FAM_V1;
     if (v && strcmp(v, "tma") == 0) cached = FAM_TMA;
   }
@@ -75,7 +75,7 @@ static bool try_rows_forward(const dffm_model* m, FwdParams& p, int smax, cudaSt
 }
 
 static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc) {
-  if (forward_family() != FAM_WS && forward_family() != FAM_ROWS) return false;
+  if (forward_family() != FAM_WS && forward_family() != FAM_ROWS) return false;  // rows falls back here
   for (int l = 1; l < p.n_layers; ++l)
     if (p.dims[l] % 4) return false;
   for (int TE = 32; TE >= 8; TE >>= 1) {
