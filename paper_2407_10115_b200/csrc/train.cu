@@ -1,13 +1,521 @@
-// K2: sequential Adagrad trainer -- placeholder until the persistent kernel lands.
+// K2: sequential Adagrad trainer (replaces training._train_lines T:172-185 =
+// forward M:321 -> predict_proba M:300 -> backward_update M:440-533, batch 1,
+// in the reference's exact example order).
+//
+// One persistent CTA (1024 threads) walks the whole stream; every example is
+// a dependent step, so the design goal is per-example latency.  All model
+// arithmetic is f64 over f32 storage like the reference (M:15-18), with the
+// roundings the reference performs:
+//   forward   S[f][g] = sum_m x_m * f64(w)       (M:339), pairs in f64 (M:351),
+//             MergeNorm (M:355-360), MLP in f64 with f32 weights (M:367-373)
+//   Adagrad   acc64 = f64(acc32) + g*g ; acc32 <- f32(acc64) ;
+//             w32 <- f32(f64(w32) - (lr*g) * (1/sqrt(acc64)))     (M:510-513, M:545-554)
+//             -- separate IEEE mul / add / sqrt / div, never FMA-contracted
+//   duplicate buckets across fields: gradients summed in occurrence order
+//             before one update (sort-and-segment, M:424-437)
+//   sparse    zero-gradient slots are skipped; byte-identical to dense (M:536-572)
+// The MLP weights/accumulators and the hashed tables stay in HBM (L2-hot);
+// per-example temporaries live in shared memory.
+#include <math.h>
+
 #include "common.cuh"
+
+namespace dffm {
+
+constexpr int TR_THREADS = 1024;
+constexpr int TR_WARPS = TR_THREADS / 32;
+
+struct TrainParams {
+  const int32_t* idx;
+  const float* val;
+  const uint8_t* labels;
+  double* prob_out;
+  uint64_t* status;
+  int64_t n;
+  int64_t n_buckets;
+  int F, M, k, P, D;
+  int n_layers;
+  int dims[DFFM_MAX_LAYERS + 1];
+  int hsum;  // sum of hidden sizes
+  int dmax;  // max layer width incl. D
+  float* lr;
+  float* ffm;
+  float* W[DFFM_MAX_LAYERS];
+  float* b[DFFM_MAX_LAYERS];
+  float* lr_acc;
+  float* ffm_acc;
+  float* W_acc[DFFM_MAX_LAYERS];
+  float* b_acc[DFFM_MAX_LAYERS];
+  double lr_ffm, lr_lr, lr_nn, power_t;
+  int sparse;
+};
+
+struct TrSmem {
+  int off_sidx, off_sval, off_pres, off_lrp, off_S, off_v, off_merged, off_pre, off_act, off_d0,
+      off_d1, off_dv, off_occf, off_lead, off_fact, off_red, off_misc, total;
+};
+
+__host__ __device__ inline int a8(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int hsum, int dmax) {
+  TrSmem s;
+  const int FM = F * M;
+  int o = 0;
+  s.off_sidx = o; o = a8(o + FM * 4);
+  s.off_sval = o; o = a8(o + FM * 8);
+  s.off_pres = o; o = a8(o + F * 4);
+  s.off_lrp = o; o = a8(o + F * 8);
+  s.off_S = o; o = a8(o + F * F * k * 8);
+  s.off_v = o; o = a8(o + D * 8);
+  s.off_merged = o; o = a8(o + D * 8);
+  s.off_pre = o; o = a8(o + (hsum + 1) * 8);
+  s.off_act = o; o = a8(o + (hsum + 1) * 8);
+  s.off_d0 = o; o = a8(o + dmax * 8);
+  s.off_d1 = o; o = a8(o + dmax * 8);
+  s.off_dv = o; o = a8(o + D * 8);
+  s.off_occf = o; o = a8(o + FM * 4);
+  s.off_lead = o; o = a8(o + FM * 4);
+  s.off_fact = o; o = a8(o + F * 4);
+  s.off_red = o; o = a8(o + 64 * 8);
+  s.off_misc = o; o = a8(o + 16 * 8);
+  s.total = o;
+  return s;
+}
+
+__device__ __forceinline__ double inv_pow(double acc, double pt) {
+  if (pt == 0.5) return __ddiv_rn(1.0, __dsqrt_rn(acc));  // M:400-404
+  return pow(acc, -pt);
+}
+
+// One Adagrad element step, reference rounding (M:510-513): returns new w.
+__device__ __forceinline__ void adagrad(float* w, float* acc, double g, double lr, double pt) {
+  const double a64 = __dadd_rn((double)*acc, __dmul_rn(g, g));
+  *acc = __double2float_rn(a64);
+  const double step = __dmul_rn(__dmul_rn(lr, g), inv_pow(a64, pt));
+  *w = __double2float_rn(__dsub_rn((double)*w, step));
+}
+
+// Block-wide f64 sum (all threads must call); result broadcast to all.
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < TR_WARPS ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__device__ __forceinline__ int tr_pair_pos(int a, int b, int F) {
+  return a * F - a * (a + 1) / 2 + (b - a - 1);
+}
+
+__device__ __forceinline__ double sigmoid_raw(double logit) {  // M:293-297
+  if (logit >= 0.0) return 1.0 / (1.0 + exp(-fmin(logit, 60.0)));
+  const double e = exp(fmax(logit, -60.0));
+  return e / (1.0 + e);
+}
+
+__global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int F = p.F, M = p.M, k = p.k, P = p.P, D = p.D, FM = F * M, Fk = F * k;
+  const TrSmem L = tr_smem_layout(F, M, k, D, p.hsum, p.dmax);
+  int* sidx = (int*)(smem + L.off_sidx);
+  double* sval = (double*)(smem + L.off_sval);
+  int* pres = (int*)(smem + L.off_pres);
+  double* lrp = (double*)(smem + L.off_lrp);
+  double* S = (double*)(smem + L.off_S);
+  double* v = (double*)(smem + L.off_v);
+  double* merged = (double*)(smem + L.off_merged);
+  double* pre = (double*)(smem + L.off_pre);
+  double* act = (double*)(smem + L.off_act);
+  double* d0 = (double*)(smem + L.off_d0);
+  double* d1 = (double*)(smem + L.off_d1);
+  double* dv = (double*)(smem + L.off_dv);
+  int* occf = (int*)(smem + L.off_occf);
+  int* lead = (int*)(smem + L.off_lead);
+  int* fact = (int*)(smem + L.off_fact);
+  double* red = (double*)(smem + L.off_red);
+  double* misc = (double*)(smem + L.off_misc);
+  const int tid = threadIdx.x;
+  const int NL = p.n_layers;
+  const double pt = p.power_t;
+
+  for (int64_t e = 0; e < p.n; ++e) {
+    // ---------------------------------------------------------- stage example
+    const int label = p.labels[e];
+    if (label > 1) {  // M:453-454 ContractError, before touching anything
+      if (tid == 0)
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(e, DFFM_BLOCK_NONE, DFFM_CONTRACT));
+      return;
+    }
+    int bad = 0;
+    for (int s = tid; s < FM; s += TR_THREADS) {
+      int j = p.idx[e * FM + s];
+      if (j >= p.n_buckets || j < -1) {
+        bad = 1;
+        j = -1;
+      }
+      sidx[s] = j;
+      sval[s] = (double)p.val[e * FM + s];
+    }
+    if (__syncthreads_or(bad)) {
+      if (tid == 0)
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(e, DFFM_BLOCK_NONE, DFFM_CONTRACT));
+      return;
+    }
+    for (int f = tid; f < F; f += TR_THREADS) {
+      int pr = 0;
+      double lp = 0.0;
+      for (int m = 0; m < M; ++m) {
+        const int j = sidx[f * M + m];
+        if (j >= 0) {
+          pr = 1;
+          lp += (double)p.lr[j] * sval[f * M + m];  // M:338 np.dot(lr[idx], x)
+        }
+      }
+      pres[f] = pr;
+      lrp[f] = lp;
+    }
+    // S[f][g][c] = sum_m x_m * ffm[j_m][g][c]  (M:339)
+    for (int t = tid; t < F * Fk; t += TR_THREADS) {
+      const int f = t / Fk, gk = t - f * Fk;
+      double s = 0.0;
+      for (int m = 0; m < M; ++m) {
+        const int j = sidx[f * M + m];
+        if (j >= 0) s += sval[f * M + m] * (double)p.ffm[(int64_t)j * Fk + gk];
+      }
+      S[t] = s;
+    }
+    __syncthreads();
+    // ---------------------------------------------------------- pairs, MergeNorm
+    double psum_part = 0.0;
+    int ffm_bad = 0;
+    for (int pp = tid; pp < P; pp += TR_THREADS) {
+      // decode pair pp -> (f1, f2)
+      int f1 = 0, rem = pp;
+      while (rem >= F - 1 - f1) { rem -= F - 1 - f1; ++f1; }
+      const int f2 = f1 + 1 + rem;
+      double pv = 0.0;
+      if (pres[f1] && pres[f2]) {  // M:346-351
+        const double* a = S + (f1 * F + f2) * k;
+        const double* b = S + (f2 * F + f1) * k;
+        for (int c = 0; c < k; ++c) pv += a[c] * b[c];
+      }
+      v[1 + pp] = pv;
+      psum_part += pv;
+      ffm_bad |= !isfinite(pv);
+    }
+    if (tid == 0) {
+      double lo = (double)p.lr[p.n_buckets];  // bias, M:327
+      for (int f = 0; f < F; ++f)
+        if (pres[f]) lo += lrp[f];
+      v[0] = lo;
+    }
+    const double psum = block_sum(psum_part, red);
+    ffm_bad = __syncthreads_or(ffm_bad);
+    const double lr_out = v[0];
+    const double mu = (psum + lr_out) / D;
+    double sq_part = 0.0;
+    for (int i = tid; i < D; i += TR_THREADS) {
+      const double c = v[i] - mu;
+      sq_part += c * c;
+    }
+    const double sd = sqrt(block_sum(sq_part, red) / D);  // np.std (population)
+    const double denom = sd + 1e-6;
+    int merge_bad = 0;
+    for (int i = tid; i < D; i += TR_THREADS) {
+      merged[i] = (v[i] - mu) / denom;
+      merge_bad |= !isfinite(merged[i]);
+    }
+    merge_bad = __syncthreads_or(merge_bad);
+    // ---------------------------------------------------------- MLP forward (f64)
+    double nn_out = 0.0;
+    int nn_bad = 0;
+    if (NL > 0) {
+      const double* a = merged;
+      int hoff = 0;
+      for (int l = 0; l + 1 < NL; ++l) {
+        const int I = p.dims[l], O = p.dims[l + 1];
+        const float* W = p.W[l];
+        // each output o by a group of G threads (k-split), reduced by shuffles
+        const int G = O >= TR_THREADS ? 1 : (O >= 512 ? 2 : (O >= 256 ? 4 : (O >= 128 ? 8 : (O >= 64 ? 16 : 32))));
+        for (int base = 0; base < O * G; base += TR_THREADS) {
+          const int t = base + tid;
+          const int o = t / G, part = t % G;
+          double s = 0.0;
+          if (o < O)
+            for (int i = part; i < I; i += G) s += a[i] * (double)W[(int64_t)i * O + o];
+          for (int off = G >> 1; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, G);
+          if (o < O && part == 0) {
+            const double z = s + (double)p.b[l][o];  // M:368
+            pre[hoff + o] = z;
+            act[hoff + o] = (z != z) ? z : fmax(z, 0.0);  // np.maximum (M:370)
+            nn_bad |= !isfinite(z);
+          }
+        }
+        __syncthreads();
+        a = act + hoff;
+        hoff += O;
+      }
+      const int I = p.dims[NL - 1];
+      double s = 0.0;
+      for (int i = tid; i < I; i += TR_THREADS) s += a[i] * (double)p.W[NL - 1][i];
+      nn_out = block_sum(s, red) + (double)p.b[NL - 1][0];  // M:372-373
+      nn_bad = __syncthreads_or(nn_bad);
+    }
+    const double logit = nn_out + lr_out + psum;  // M:377
+    if (!isfinite(logit)) {  // M:392-396
+      if (tid == 0) {
+        const int blk = !isfinite(lr_out) ? DFFM_BLOCK_LR : ffm_bad ? DFFM_BLOCK_FFM
+                      : merge_bad ? DFFM_BLOCK_MERGE : nn_bad ? DFFM_BLOCK_NN : DFFM_BLOCK_LOGIT;
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(e, blk, DFFM_NUMERIC));
+      }
+      return;
+    }
+    const double p_raw = sigmoid_raw(logit);
+    const double g = p_raw - (double)label;  // M:456-457
+    if (tid == 0) p.prob_out[e] = fmin(fmax(p_raw, 1e-7), 1.0 - 1e-7);  // predict_proba
+    // ---------------------------------------------------------- MLP backward + update
+    double* dmerged = d1;
+    if (NL > 0) {
+      double* dcur = d0;
+      double* dnext = d1;
+      if (tid == 0) dcur[0] = g;
+      __syncthreads();
+      int hoff = p.hsum;
+      for (int l = NL - 1; l >= 0; --l) {
+        const int I = p.dims[l], O = p.dims[l + 1];
+        float* W = p.W[l];
+        float* Wa = p.W_acc[l];
+        const double* a_in = l == 0 ? merged : act + (hoff - I);
+        // upstream gradient from the PRE-update weights (M:473-475)
+        for (int r = tid; r < I; r += TR_THREADS) {
+          double s = 0.0;
+          for (int c = 0; c < O; ++c) s += (double)W[(int64_t)r * O + c] * dcur[c];
+          dnext[r] = s;
+        }
+        __syncthreads();
+        // W[r][c] -= ... with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554)
+        for (int t = tid; t < I * O; t += TR_THREADS) {
+          const int r = t / O, c = t - r * O;
+          const double gr = __dmul_rn(a_in[r], dcur[c]);
+          if (gr != 0.0 || !p.sparse) adagrad(&W[t], &Wa[t], gr, p.lr_nn, pt);
+        }
+        for (int c = tid; c < O; c += TR_THREADS) {  // M:557-572
+          const double gr = dcur[c];
+          if (gr != 0.0 || !p.sparse) adagrad(&p.b[l][c], &p.b_acc[l][c], gr, p.lr_nn, pt);
+        }
+        if (l > 0) {
+          hoff -= I;
+          for (int r = tid; r < I; r += TR_THREADS)
+            dnext[r] = pre[hoff + r] > 0.0 ? dnext[r] : 0.0;  // M:479 ReLU mask
+        }
+        __syncthreads();
+        double* tmp = dcur; dcur = dnext; dnext = tmp;
+      }
+      dmerged = dcur;
+    }
+    // ---------------------------------------------------------- MergeNorm backward (M:413-421)
+    double d_lr;
+    if (NL > 0) {
+      double s_d = 0.0, s_dc = 0.0;
+      for (int i = tid; i < D; i += TR_THREADS) {
+        s_d += dmerged[i];
+        s_dc += dmerged[i] * (v[i] - mu);
+      }
+      const double mean_d = block_sum(s_d, red) / D;
+      const double dot_dc = block_sum(s_dc, red);
+      for (int i = tid; i < D; i += TR_THREADS) {
+        double x = (dmerged[i] - mean_d) / denom;
+        if (sd > 0.0) x = x - (v[i] - mu) * (dot_dc / (D * sd * denom * denom));
+        dv[i] = x;
+      }
+      __syncthreads();
+      d_lr = g + dv[0];  // M:483
+    } else {
+      d_lr = g;
+      for (int i = tid; i < D; i += TR_THREADS) dv[i] = 0.0;
+      __syncthreads();
+    }
+    // d_pairs[p] = g + dv[1+p]  (M:484); dp is symmetric (M:492-495)
+    // ---------------------------------------------------------- FFM update (M:490-513)
+    // t[g][:] = dp[f][g] * S[g][f][:]; fields whose t is all zero are skipped (M:502)
+    for (int f = tid; f < F; f += TR_THREADS) {
+      int any = 0;
+      if (pres[f]) {
+        for (int gg = 0; gg < F && !any; ++gg) {
+          if (gg == f) continue;
+          const int pp = gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F);
+          const double dpv = g + dv[1 + pp];
+          const double* sgf = S + (gg * F + f) * k;
+          for (int c = 0; c < k; ++c) any |= (dpv * sgf[c]) != 0.0;
+        }
+      }
+      fact[f] = any;
+    }
+    // Sort-and-segment (M:424-437): occurrence order = field order, then slot
+    // order.  lead[s] = first slot holding the same bucket; occf[s] = next slot
+    // of the same bucket (chain), so each unique bucket's gradient is summed in
+    // occurrence order before its single Adagrad step.
+    for (int s = tid; s < FM; s += TR_THREADS) {
+      const int j = sidx[s];
+      int ld = -1, nx = -1;
+      if (j >= 0) {
+        ld = s;
+        for (int s2 = 0; s2 < s; ++s2)
+          if (sidx[s2] == j) { ld = s2; break; }
+        for (int s2 = s + 1; s2 < FM; ++s2)
+          if (sidx[s2] == j) { nx = s2; break; }
+      }
+      lead[s] = ld;
+      occf[s] = nx;
+    }
+    __syncthreads();
+    // one thread per (leader slot, latent element): merged gradient in occurrence order
+    for (int t = tid; t < FM * Fk; t += TR_THREADS) {
+      const int s = t / Fk, gk = t - s * Fk;
+      if (lead[s] != s) continue;
+      const int gg = gk / k, c = gk - gg * k;
+      const int j = sidx[s];
+      double ug = 0.0;
+      bool touched = false;
+      for (int s2 = s; s2 >= 0; s2 = occf[s2]) {
+        const int f = s2 / M;
+        if (!fact[f]) continue;
+        double dpv = 0.0;
+        if (gg != f) {
+          const int pp = gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F);
+          dpv = g + dv[1 + pp];
+        }
+        const double tv = dpv * S[(gg * F + f) * k + c];  // t[g][c] (M:501)
+        ug += sval[s2] * tv;                              // x * t (M:505), add.at order
+        touched = true;
+      }
+      if (!touched) continue;
+      if (ug != 0.0 || !p.sparse) {
+        const int64_t wi = (int64_t)j * Fk + gk;
+        adagrad(&p.ffm[wi], &p.ffm_acc[wi], ug, p.lr_ffm, pt);  // M:509-513
+      }
+    }
+    // ---------------------------------------------------------- LR + bias (M:516-530)
+    for (int s = tid; s < FM; s += TR_THREADS) {
+      if (lead[s] != s) continue;
+      const int j = sidx[s];
+      double ug = 0.0;
+      for (int s2 = s; s2 >= 0; s2 = occf[s2]) ug += d_lr * sval[s2];
+      adagrad(&p.lr[j], &p.lr_acc[j], ug, p.lr_lr, pt);
+    }
+    if (tid == 0) adagrad(&p.lr[p.n_buckets], &p.lr_acc[p.n_buckets], d_lr, p.lr_lr, pt);
+    (void)misc;
+    __syncthreads();
+  }
+}
+
+int fill_model_params(const dffm_model* m, struct FwdParams& p);
+
+}  // namespace dffm
 
 using namespace dffm;
 
+static int tr_validate(const dffm_model* m, int32_t M, TrainParams& p, int* smem_out) {
+  if (!m) { set_error("null model"); return DFFM_CONTRACT; }
+  if (m->wdtype != DFFM_W_F32) { set_error("training needs f32 tables"); return DFFM_CONTRACT; }
+  if (m->n_fields < 1 || m->k < 1 || M < 1) { set_error("bad shape"); return DFFM_CONTRACT; }
+  if (m->n_layers < 0 || m->n_layers > DFFM_MAX_LAYERS || m->n_layers == 1) {
+    set_error("n_layers=%d invalid", m->n_layers);
+    return DFFM_CONTRACT;
+  }
+  p.F = m->n_fields;
+  p.k = m->k;
+  p.M = M;
+  p.P = p.F * (p.F - 1) / 2;
+  p.D = 1 + p.P;
+  p.n_buckets = (int64_t)1 << m->hash_bits;
+  p.n_layers = m->n_layers;
+  p.hsum = 0;
+  p.dmax = p.D;
+  for (int l = 0; l <= DFFM_MAX_LAYERS; ++l) p.dims[l] = m->dims[l];
+  if (p.n_layers) {
+    if (m->dims[0] != p.D || m->dims[p.n_layers] != 1) {
+      set_error("MLP dims do not match 1+F(F-1)/2 -> ... -> 1");
+      return DFFM_CONTRACT;
+    }
+    for (int l = 1; l < p.n_layers; ++l) {
+      p.hsum += m->dims[l];
+      if (m->dims[l] > p.dmax) p.dmax = m->dims[l];
+    }
+  }
+  p.lr = (float*)m->lr;
+  p.ffm = (float*)m->ffm;
+  for (int l = 0; l < p.n_layers; ++l) {
+    p.W[l] = (float*)m->W[l];
+    p.b[l] = (float*)m->b[l];
+  }
+  const TrSmem L = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax);
+  if (L.total > max_smem_optin_current()) {
+    set_error("trainer needs %d B of shared memory per example state (> %d)", L.total,
+              max_smem_optin_current());
+    return DFFM_SIZING;
+  }
+  *smem_out = L.total;
+  return DFFM_OK;
+}
+
 extern "C" int64_t dffm_train_scratch_bytes(const dffm_model*, int32_t) { return 0; }
 
-extern "C" int dffm_train_sequential(const dffm_model*, const dffm_train_state*, const int32_t*,
-                                     const float*, const uint8_t*, int32_t, int64_t, double*,
-                                     void*, uint64_t*, void*) {
-  set_error("dffm_train_sequential: not built in this revision");
-  return DFFM_SIZING;
+extern "C" int dffm_train_sequential(const dffm_model* model, const dffm_train_state* state,
+                                     const int32_t* idx, const float* val, const uint8_t* labels,
+                                     int32_t max_per_field, int64_t n, double* prob_out,
+                                     void* scratch, uint64_t* status, void* stream) {
+  (void)scratch;
+  TrainParams p{};
+  int smem = 0;
+  int rc = tr_validate(model, max_per_field, p, &smem);
+  if (rc) return rc;
+  if (!state || !state->lr_acc || !state->ffm_acc) {
+    set_error("null optimizer state");
+    return DFFM_CONTRACT;
+  }
+  if (n < 0) { set_error("negative n"); return DFFM_CONTRACT; }
+  if (n == 0) return DFFM_OK;
+  if (!idx || !val || !labels || !prob_out || !status) {
+    set_error("null buffer");
+    return DFFM_CONTRACT;
+  }
+  for (int l = 0; l < p.n_layers; ++l) {
+    if (!state->W_acc[l] || !state->b_acc[l]) { set_error("null MLP acc"); return DFFM_CONTRACT; }
+    p.W_acc[l] = state->W_acc[l];
+    p.b_acc[l] = state->b_acc[l];
+  }
+  p.lr_acc = state->lr_acc;
+  p.ffm_acc = state->ffm_acc;
+  p.lr_ffm = state->lr_ffm;
+  p.lr_lr = state->lr_lr;
+  p.lr_nn = state->lr_nn;
+  p.power_t = state->power_t;
+  p.sparse = state->sparse;
+  p.idx = idx;
+  p.val = val;
+  p.labels = labels;
+  p.prob_out = prob_out;
+  p.status = status;
+  p.n = n;
+  int occ = 0;
+  rc = kernel_occupancy((const void*)train_kernel, TR_THREADS, smem, &occ);
+  if (rc) return rc;
+  train_kernel<<<1, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(train)");
+  return DFFM_OK;
 }

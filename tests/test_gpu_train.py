@@ -1,0 +1,114 @@
+"""K2 sequential Adagrad trainer parity (GPU).
+
+Bar (BASELINE north star): progressive predictions and updated weights within
+1e-5 relative, with an absolute floor for near-zero weights:
+|w_gpu - w_ref| <= 1e-5 * max(|w_ref|, 1e-3).  The kernel
+computes in f64 with f32 storage and the reference's rounding points, so in
+practice most slots are bit-identical; the test also reports that fraction."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fieldwise_oracle as fo
+from paper_2407_10115_b200 import configs, synth
+from paper_2407_10115_b200.errors import ContractError
+from paper_2407_10115_b200.model import ModelConfig, WeightStore
+from paper_2407_10115_b200.training import TrainOptions, train_sequential
+from tests.golden_io import load, seeded_flat
+from tests.remap import compact_oracle
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+def close_weights(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    tol = 1e-5 * np.maximum(np.abs(ref), 1e-3)
+    bad = np.abs(got - ref) > tol
+    return int(bad.sum()), float(np.mean(got == ref))
+
+
+@pytest.mark.parametrize("name", ["salted", "unsalted", "pt025_dense", "ffm_lr"])
+def test_train_matches_reference_golden(name):
+    g = load(f"train_{name}")
+    F, k, bits = int(g["F"]), int(g["k"]), int(g["bits"])
+    hidden = tuple(int(h) for h in g["hidden"])
+    lr, pt = float(g["lr"]), float(g["power_t"])
+    cfg = ModelConfig(n_fields=F, k=k, hidden_sizes=hidden, hash_bits=bits, lr_ffm=lr,
+                      lr_lr=lr, lr_nn=lr, power_t=pt)
+    flat = seeded_flat(F, k, hidden, bits, g["w_seed"], 0.05)
+    st = WeightStore.from_flat(cfg, flat, DEV)
+    rep = train_sequential(g["idx"], g["val"], g["labels"], st,
+                           TrainOptions(sparse_updates=bool(g["sparse"])))
+    assert np.max(np.abs(rep.probs - g["probs"]) / g["probs"]) < 1e-5
+    assert rep.progressive_logloss == pytest.approx(float(g["logloss"]), rel=1e-6)
+    nbad, same = close_weights(st.weight_values(True), g["final"])
+    assert nbad == 0, f"{nbad} slots outside tolerance ({same:.4%} bit-identical)"
+    assert st.version == g["idx"].shape[0]
+
+
+def test_train_matches_oracle_cfg3_shape_with_duplicates():
+    """cfg3 schema (F=24, k=8, M=3, 277->64->32->1), unsalted ranks -> many
+    cross-field duplicate buckets (sort-and-segment path)."""
+    wl = configs.CFG3
+    bits = 12
+    idx, val = synth.make_examples(wl, 1500, seed=77, hash_bits=bits, salted=False)
+    labels = (np.random.default_rng(3).random(1500) < 0.4).astype(np.uint8)
+    ost = fo.random_store(24, 8, (64, 32), bits, seed=9)
+    cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=bits, lr_ffm=0.1,
+                      lr_lr=0.1, lr_nn=0.1, power_t=0.5)
+    st = WeightStore.from_flat(cfg, ost.flat(True), DEV)
+    rep = train_sequential(idx, val, labels, st, TrainOptions(chunk=700))  # crosses a chunk edge
+    probs, _ = fo.train_sequential(idx.numpy(), val.numpy(), labels, ost, .1, .1, .1, .5)
+    assert np.max(np.abs(rep.probs - probs) / probs) < 1e-5
+    nbad, same = close_weights(st.weight_values(True), ost.flat(True))
+    assert nbad == 0, f"{nbad} slots outside tolerance ({same:.4%} bit-identical)"
+
+
+def test_train_full_size_table_prefix():
+    """BASELINE cfg3 at full size (2^24 buckets): a 2,000-example prefix on the
+    GPU vs the oracle on the remapped touched rows."""
+    wl = configs.CFG3
+    cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=24, lr_ffm=0.1,
+                      lr_lr=0.1, lr_nn=0.1, power_t=0.5)
+    st = WeightStore(cfg, DEV)
+    gen = torch.Generator(device=DEV).manual_seed(wl.weight_seed)
+    st.lr.copy_(synth.normal_table(st.lr.numel(), 0.05, gen, DEV))
+    st.ffm.view(-1).copy_(synth.normal_table(st.ffm.numel(), 0.05, gen, DEV))
+    for w, b in st.nn_layers:
+        w.copy_(torch.randn(w.shape, generator=gen, device=DEV) * 0.05)
+        b.copy_(torch.randn(b.shape, generator=gen, device=DEV) * 0.05)
+    n = 2000
+    idx, val = synth.make_examples(wl, n, device=DEV)
+    labels = synth.make_labels(n, 0.3, 5, device=DEV)
+    ih, vh, lh = idx.cpu().numpy(), val.cpu().numpy(), labels.cpu().numpy()
+    ost, ridx, u = compact_oracle(st, ih)  # snapshot BEFORE training
+    rep = train_sequential(idx, val, labels, st)
+    probs, _ = fo.train_sequential(ridx, vh, lh, ost, .1, .1, .1, .5)
+    assert np.max(np.abs(rep.probs - probs) / probs) < 1e-5
+    ut = torch.as_tensor(u, device=DEV)
+    got = np.concatenate([st.ffm[ut].cpu().numpy().ravel(), st.ffm_acc[ut].cpu().numpy().ravel(),
+                          st.lr[ut].cpu().numpy(), st.lr_acc[ut].cpu().numpy()])
+    ref = np.concatenate([ost.ffm[:len(u)].ravel(), ost.ffm_acc[:len(u)].ravel(),
+                          ost.lr[:len(u)], ost.lr_acc[:len(u)]])
+    nbad, same = close_weights(got, ref)
+    assert nbad == 0, f"{nbad} touched slots outside tolerance ({same:.4%} bit-identical)"
+
+
+def test_train_bad_label_is_contract_error_and_stops():
+    ost = fo.random_store(4, 4, (8,), 8, seed=1)
+    cfg = ModelConfig(n_fields=4, k=4, hidden_sizes=(8,), hash_bits=8)
+    st = WeightStore.from_flat(cfg, ost.flat(True), DEV)
+    idx = np.random.default_rng(0).integers(0, 256, (10, 4, 1)).astype(np.int32)
+    val = np.ones_like(idx, dtype=np.float32)
+    labels = np.array([0, 1, 0, 2, 1, 0, 0, 1, 1, 0], np.uint8)
+    before = st.weight_values(True)
+    with pytest.raises(ContractError):
+        train_sequential(idx, val, labels, st)
+    # the first three examples were applied (reference semantics), the rest not
+    o2 = fo.OracleStore.from_flat(4, 4, (8,), 8, before)
+    fo.train_sequential(idx[:3], val[:3], labels[:3], o2, cfg.lr_ffm, cfg.lr_lr, cfg.lr_nn, .5)
+    nbad, _ = close_weights(st.weight_values(True), o2.flat(True))
+    assert nbad == 0
