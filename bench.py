@@ -391,11 +391,67 @@ def run_ours(args, wl):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(st, idx, val, prob, wl)
+    if args.train_examples > 0:
+        del st, idx, val, prob, hp, idx_h, val_h, out_h
+        torch.cuda.empty_cache()
+        line["adagrad"] = bench_adagrad(args, dev, clk_index=local)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_adagrad(args, dev, clk_index=0):
+    """K2 on a prefix of the cfg3 stream: examples/s of the exact sequential
+    schedule (T:172-185), inputs resident, labels from a planted teacher."""
+    import torch
+
+    from paper_2407_10115_b200 import configs, synth
+    from paper_2407_10115_b200.model import ModelConfig, WeightStore, predict_batch
+    from paper_2407_10115_b200.training import TrainOptions, train_sequential
+    wl = configs.CFG3
+    n = args.train_examples
+    cfg = ModelConfig(n_fields=wl.n_fields, k=wl.k, hidden_sizes=wl.hidden,
+                      hash_bits=wl.hash_bits, lr_ffm=wl.lr, lr_lr=wl.lr, lr_nn=wl.lr,
+                      power_t=wl.power_t)
+    idx, val = build_inputs(wl, n, dev, 0)
+    teacher = WeightStore(cfg, dev, with_optimizer=False)
+    gen = torch.Generator(device=dev).manual_seed(3003)
+    for t in [teacher.lr, teacher.ffm] + [x for wb in teacher.nn_layers for x in wb]:
+        flat = t.view(-1)
+        for c0 in range(0, flat.numel(), 1 << 28):
+            c1 = min(flat.numel(), c0 + (1 << 28))
+            flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=dev) * 0.1)
+    p = predict_batch(idx, val, teacher)
+    labels = (torch.rand(n, generator=gen, device=dev) < p).to(torch.uint8)
+    del teacher, p
+    torch.cuda.empty_cache()
+    st = WeightStore(cfg, dev)
+    gen.manual_seed(wl.weight_seed)
+    for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
+        flat = t.view(-1)
+        for c0 in range(0, flat.numel(), 1 << 28):
+            c1 = min(flat.numel(), c0 + (1 << 28))
+            flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=dev) * wl.weight_scale)
+    warm = min(2000, n // 10)
+    train_sequential(idx[:warm], val[:warm], labels[:warm], st, TrainOptions())
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(clk_index) as clk:
+        s.record()
+        rep = train_sequential(idx[warm:], val[warm:], labels[warm:], st,
+                               TrainOptions(chunk=1 << 22))
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    done = n - warm
+    return {"value": done / (ms / 1e3), "unit": "examples/s", "examples": done,
+            "us_per_example": 1e3 * ms / done, "progressive_logloss": rep.progressive_logloss,
+            "workload": f"{wl.name} prefix ({done} of {wl.n_examples} examples, exact "
+                        "sequential schedule, batch size 1)",
+            "dtype": "f64 arithmetic, f32 storage", "gpu_launches": -(-done // (1 << 22)),
+            "clocks": clk.summary()}
 
 
 def cpu_baseline(st, idx, val, prob, wl, budget_s=12.0):
@@ -429,6 +485,8 @@ def main():
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--examples", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--train-examples", type=int, default=200_000,
+                    help="cfg3 Adagrad prefix timed after the forward (0 = skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

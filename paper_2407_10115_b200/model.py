@@ -243,7 +243,9 @@ class WeightStore:
 
     @classmethod
     def from_flat(cls, config, flat, device=None, wdtype="f32", with_optimizer=True):
-        return cls(config, device, wdtype, with_optimizer).load_flat(flat)
+        st = cls(config, device, wdtype, with_optimizer).load_flat(flat)
+        st.version = 0  # a freshly built store, like WeightStore(config) (M:180)
+        return st
 
     def copy(self) -> "WeightStore":
         dup = WeightStore(self.config, self.device, self.wdtype, _alloc=False)
