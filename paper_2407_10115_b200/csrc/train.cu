@@ -3,9 +3,16 @@
 // in the reference's exact example order).
 //
 // One persistent CTA (1024 threads) walks the whole stream; every example is
-// a dependent step, so the design goal is per-example latency.  All model
-// arithmetic is f64 over f32 storage like the reference (M:15-18), with the
-// roundings the reference performs:
+// a dependent step, so the design goal is per-example latency:
+//   * the MLP weights and their accumulators are staged into shared memory
+//     for the whole launch (159 KB at cfg3) and written back at the end, so
+//     every GEMV and every MLP Adagrad step runs at shared-memory latency;
+//   * GEMVs use conflict-free mappings with deterministic split-K
+//     reductions (fixed order: results do not depend on scheduling);
+//   * the hashed lr / ffm rows stay in HBM (L2-hot) and are read-modified-
+//     written in place, coalesced along the row.
+// All model arithmetic is f64 over f32 storage like the reference
+// (M:15-18), with the roundings it performs:
 //   forward   S[f][g] = sum_m x_m * f64(w)       (M:339), pairs in f64 (M:351),
 //             MergeNorm (M:355-360), MLP in f64 with f32 weights (M:367-373)
 //   Adagrad   acc64 = f64(acc32) + g*g ; acc32 <- f32(acc64) ;
@@ -14,8 +21,6 @@
 //   duplicate buckets across fields: gradients summed in occurrence order
 //             before one update (sort-and-segment, M:424-437)
 //   sparse    zero-gradient slots are skipped; byte-identical to dense (M:536-572)
-// The MLP weights/accumulators and the hashed tables stay in HBM (L2-hot);
-// per-example temporaries live in shared memory.
 #include <math.h>
 
 #include "common.cuh"
@@ -36,8 +41,10 @@ struct TrainParams {
   int F, M, k, P, D;
   int n_layers;
   int dims[DFFM_MAX_LAYERS + 1];
-  int hsum;  // sum of hidden sizes
-  int dmax;  // max layer width incl. D
+  int hsum;      // sum of hidden sizes
+  int dmax;      // max layer width incl. D
+  int mlp_size;  // floats in W+b over all layers
+  int mlp_smem;  // 1: MLP weights + accumulators resident in shared memory
   float* lr;
   float* ffm;
   float* W[DFFM_MAX_LAYERS];
@@ -52,32 +59,34 @@ struct TrainParams {
 
 struct TrSmem {
   int off_sidx, off_sval, off_pres, off_lrp, off_S, off_v, off_merged, off_pre, off_act, off_d0,
-      off_d1, off_dv, off_occf, off_lead, off_fact, off_red, off_misc, total;
+      off_d1, off_dv, off_nxt, off_lead, off_fact, off_red, off_part, off_mlp, total;
 };
 
-__host__ __device__ inline int a8(int x) { return (x + 15) & ~15; }
+__host__ __device__ inline int a16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int hsum, int dmax) {
+__host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int hsum, int dmax,
+                                                 int mlp_floats) {
   TrSmem s;
   const int FM = F * M;
   int o = 0;
-  s.off_sidx = o; o = a8(o + FM * 4);
-  s.off_sval = o; o = a8(o + FM * 8);
-  s.off_pres = o; o = a8(o + F * 4);
-  s.off_lrp = o; o = a8(o + F * 8);
-  s.off_S = o; o = a8(o + F * F * k * 8);
-  s.off_v = o; o = a8(o + D * 8);
-  s.off_merged = o; o = a8(o + D * 8);
-  s.off_pre = o; o = a8(o + (hsum + 1) * 8);
-  s.off_act = o; o = a8(o + (hsum + 1) * 8);
-  s.off_d0 = o; o = a8(o + dmax * 8);
-  s.off_d1 = o; o = a8(o + dmax * 8);
-  s.off_dv = o; o = a8(o + D * 8);
-  s.off_occf = o; o = a8(o + FM * 4);
-  s.off_lead = o; o = a8(o + FM * 4);
-  s.off_fact = o; o = a8(o + F * 4);
-  s.off_red = o; o = a8(o + 64 * 8);
-  s.off_misc = o; o = a8(o + 16 * 8);
+  s.off_sidx = o; o = a16(o + FM * 4);
+  s.off_sval = o; o = a16(o + FM * 8);
+  s.off_pres = o; o = a16(o + F * 4);
+  s.off_lrp = o; o = a16(o + F * 8);
+  s.off_S = o; o = a16(o + F * F * k * 8);
+  s.off_v = o; o = a16(o + D * 8);
+  s.off_merged = o; o = a16(o + D * 8);
+  s.off_pre = o; o = a16(o + (hsum + 1) * 8);
+  s.off_act = o; o = a16(o + (hsum + 1) * 8);
+  s.off_d0 = o; o = a16(o + dmax * 8);
+  s.off_d1 = o; o = a16(o + dmax * 8);
+  s.off_dv = o; o = a16(o + D * 8);
+  s.off_nxt = o; o = a16(o + FM * 4);
+  s.off_lead = o; o = a16(o + FM * 4);
+  s.off_fact = o; o = a16(o + F * 4);
+  s.off_red = o; o = a16(o + 64 * 8);
+  s.off_part = o; o = a16(o + TR_THREADS * 8);
+  s.off_mlp = o; o = a16(o + mlp_floats * 4);
   s.total = o;
   return s;
 }
@@ -87,7 +96,7 @@ __device__ __forceinline__ double inv_pow(double acc, double pt) {
   return pow(acc, -pt);
 }
 
-// One Adagrad element step, reference rounding (M:510-513): returns new w.
+// One Adagrad element step with the reference's rounding (M:510-513).
 __device__ __forceinline__ void adagrad(float* w, float* acc, double g, double lr, double pt) {
   const double a64 = __dadd_rn((double)*acc, __dmul_rn(g, g));
   *acc = __double2float_rn(a64);
@@ -95,7 +104,7 @@ __device__ __forceinline__ void adagrad(float* w, float* acc, double g, double l
   *w = __double2float_rn(__dsub_rn((double)*w, step));
 }
 
-// Block-wide f64 sum (all threads must call); result broadcast to all.
+// Block-wide f64 sum (all threads call); result broadcast to all.
 __device__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -103,9 +112,8 @@ __device__ double block_sum(double v, double* red) {
   __syncthreads();
   if (lane == 0) red[warp] = v;
   __syncthreads();
-  double t = 0.0;
   if (threadIdx.x < 32) {
-    t = threadIdx.x < TR_WARPS ? red[threadIdx.x] : 0.0;
+    double t = threadIdx.x < TR_WARPS ? red[threadIdx.x] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     if (threadIdx.x == 0) red[32] = t;
@@ -127,7 +135,8 @@ __device__ __forceinline__ double sigmoid_raw(double logit) {  // M:293-297
 __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int F = p.F, M = p.M, k = p.k, P = p.P, D = p.D, FM = F * M, Fk = F * k;
-  const TrSmem L = tr_smem_layout(F, M, k, D, p.hsum, p.dmax);
+  const TrSmem L =
+      tr_smem_layout(F, M, k, D, p.hsum, p.dmax, p.mlp_smem ? 2 * p.mlp_size : 0);
   int* sidx = (int*)(smem + L.off_sidx);
   double* sval = (double*)(smem + L.off_sval);
   int* pres = (int*)(smem + L.off_pres);
@@ -140,14 +149,38 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   double* d0 = (double*)(smem + L.off_d0);
   double* d1 = (double*)(smem + L.off_d1);
   double* dv = (double*)(smem + L.off_dv);
-  int* occf = (int*)(smem + L.off_occf);
+  int* nxt = (int*)(smem + L.off_nxt);
   int* lead = (int*)(smem + L.off_lead);
   int* fact = (int*)(smem + L.off_fact);
   double* red = (double*)(smem + L.off_red);
-  double* misc = (double*)(smem + L.off_misc);
-  const int tid = threadIdx.x;
+  double* part = (double*)(smem + L.off_part);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NL = p.n_layers;
   const double pt = p.power_t;
+
+  // ---- MLP working copies: shared memory for the whole launch when they fit
+  float* Wl[DFFM_MAX_LAYERS];
+  float* bl[DFFM_MAX_LAYERS];
+  float* Wal[DFFM_MAX_LAYERS];
+  float* bal[DFFM_MAX_LAYERS];
+  {
+    float* mw = (float*)(smem + L.off_mlp);
+    float* ma = mw + p.mlp_size;
+    int off = 0;
+    for (int l = 0; l < NL; ++l) {
+      const int IO = p.dims[l] * p.dims[l + 1], O = p.dims[l + 1];
+      if (p.mlp_smem) {
+        Wl[l] = mw + off; bl[l] = mw + off + IO;
+        Wal[l] = ma + off; bal[l] = ma + off + IO;
+        for (int t = tid; t < IO; t += TR_THREADS) { Wl[l][t] = p.W[l][t]; Wal[l][t] = p.W_acc[l][t]; }
+        for (int t = tid; t < O; t += TR_THREADS) { bl[l][t] = p.b[l][t]; bal[l][t] = p.b_acc[l][t]; }
+      } else {
+        Wl[l] = p.W[l]; bl[l] = p.b[l]; Wal[l] = p.W_acc[l]; bal[l] = p.b_acc[l];
+      }
+      off += IO + O;
+    }
+  }
+  __syncthreads();
 
   for (int64_t e = 0; e < p.n; ++e) {
     // ---------------------------------------------------------- stage example
@@ -156,23 +189,21 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       if (tid == 0)
         atomicMin((unsigned long long*)p.status,
                   (unsigned long long)status_key(e, DFFM_BLOCK_NONE, DFFM_CONTRACT));
-      return;
+      break;
     }
     int bad = 0;
     for (int s = tid; s < FM; s += TR_THREADS) {
       int j = p.idx[e * FM + s];
-      if (j >= p.n_buckets || j < -1) {
-        bad = 1;
-        j = -1;
-      }
+      if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
       sidx[s] = j;
       sval[s] = (double)p.val[e * FM + s];
     }
+    if (tid < F) fact[tid] = 0;
     if (__syncthreads_or(bad)) {
       if (tid == 0)
         atomicMin((unsigned long long*)p.status,
                   (unsigned long long)status_key(e, DFFM_BLOCK_NONE, DFFM_CONTRACT));
-      return;
+      break;
     }
     for (int f = tid; f < F; f += TR_THREADS) {
       int pr = 0;
@@ -187,7 +218,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       pres[f] = pr;
       lrp[f] = lp;
     }
-    // S[f][g][c] = sum_m x_m * ffm[j_m][g][c]  (M:339)
+    // S[f][g][c] = sum_m x_m * ffm[j_m][g][c]  (M:339); row-coalesced reads
     for (int t = tid; t < F * Fk; t += TR_THREADS) {
       const int f = t / Fk, gk = t - f * Fk;
       double s = 0.0;
@@ -197,12 +228,26 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       }
       S[t] = s;
     }
+    // sort-and-segment bookkeeping for the update (M:424-437): lead = first
+    // slot holding the bucket, nxt = next slot of the same bucket
+    for (int s = tid; s < FM; s += TR_THREADS) {
+      const int j = sidx[s];
+      int ld = -1, nx = -1;
+      if (j >= 0) {
+        ld = s;
+        for (int s2 = 0; s2 < s; ++s2)
+          if (sidx[s2] == j) { ld = s2; break; }
+        for (int s2 = s + 1; s2 < FM; ++s2)
+          if (sidx[s2] == j) { nx = s2; break; }
+      }
+      lead[s] = ld;
+      nxt[s] = nx;
+    }
     __syncthreads();
     // ---------------------------------------------------------- pairs, MergeNorm
     double psum_part = 0.0;
     int ffm_bad = 0;
     for (int pp = tid; pp < P; pp += TR_THREADS) {
-      // decode pair pp -> (f1, f2)
       int f1 = 0, rem = pp;
       while (rem >= F - 1 - f1) { rem -= F - 1 - f1; ++f1; }
       const int f2 = f1 + 1 + rem;
@@ -247,22 +292,30 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       int hoff = 0;
       for (int l = 0; l + 1 < NL; ++l) {
         const int I = p.dims[l], O = p.dims[l + 1];
-        const float* W = p.W[l];
-        // each output o by a group of G threads (k-split), reduced by shuffles
-        const int G = O >= TR_THREADS ? 1 : (O >= 512 ? 2 : (O >= 256 ? 4 : (O >= 128 ? 8 : (O >= 64 ? 16 : 32))));
-        for (int base = 0; base < O * G; base += TR_THREADS) {
-          const int t = base + tid;
-          const int o = t / G, part = t % G;
-          double s = 0.0;
-          if (o < O)
-            for (int i = part; i < I; i += G) s += a[i] * (double)W[(int64_t)i * O + o];
-          for (int off = G >> 1; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, G);
-          if (o < O && part == 0) {
-            const double z = s + (double)p.b[l][o];  // M:368
-            pre[hoff + o] = z;
-            act[hoff + o] = (z != z) ? z : fmax(z, 0.0);  // np.maximum (M:370)
-            nn_bad |= !isfinite(z);
+        const float* W = Wl[l];
+        // split-K: thread (part, o), o fastest -> conflict-free W reads;
+        // partials reduced in fixed part order (deterministic)
+        const int G = O <= TR_THREADS ? TR_THREADS / O : 1;
+        if (G > 1) {
+          const int o = tid % O, pa = tid / O;
+          if (pa < G) {
+            double s = 0.0;
+            for (int i = pa; i < I; i += G) s += a[i] * (double)W[(int64_t)i * O + o];
+            part[pa * O + o] = s;
           }
+          __syncthreads();
+        }
+        for (int o = tid; o < O; o += TR_THREADS) {
+          double z = 0.0;
+          if (G > 1) {
+            for (int q = 0; q < G; ++q) z += part[q * O + o];
+          } else {
+            for (int i = 0; i < I; ++i) z += a[i] * (double)W[(int64_t)i * O + o];
+          }
+          z += (double)bl[l][o];  // M:368
+          pre[hoff + o] = z;
+          act[hoff + o] = (z != z) ? z : fmax(z, 0.0);  // np.maximum (M:370)
+          nn_bad |= !isfinite(z);
         }
         __syncthreads();
         a = act + hoff;
@@ -270,19 +323,19 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       }
       const int I = p.dims[NL - 1];
       double s = 0.0;
-      for (int i = tid; i < I; i += TR_THREADS) s += a[i] * (double)p.W[NL - 1][i];
-      nn_out = block_sum(s, red) + (double)p.b[NL - 1][0];  // M:372-373
+      for (int i = tid; i < I; i += TR_THREADS) s += a[i] * (double)Wl[NL - 1][i];
+      nn_out = block_sum(s, red) + (double)bl[NL - 1][0];  // M:372-373
       nn_bad = __syncthreads_or(nn_bad);
     }
     const double logit = nn_out + lr_out + psum;  // M:377
-    if (!isfinite(logit)) {  // M:392-396
+    if (!isfinite(logit)) {  // M:392-396 (uniform across the block)
       if (tid == 0) {
         const int blk = !isfinite(lr_out) ? DFFM_BLOCK_LR : ffm_bad ? DFFM_BLOCK_FFM
                       : merge_bad ? DFFM_BLOCK_MERGE : nn_bad ? DFFM_BLOCK_NN : DFFM_BLOCK_LOGIT;
         atomicMin((unsigned long long*)p.status,
                   (unsigned long long)status_key(e, blk, DFFM_NUMERIC));
       }
-      return;
+      break;
     }
     const double p_raw = sigmoid_raw(logit);
     const double g = p_raw - (double)label;  // M:456-457
@@ -297,17 +350,19 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       int hoff = p.hsum;
       for (int l = NL - 1; l >= 0; --l) {
         const int I = p.dims[l], O = p.dims[l + 1];
-        float* W = p.W[l];
-        float* Wa = p.W_acc[l];
+        float* W = Wl[l];
+        float* Wa = Wal[l];
         const double* a_in = l == 0 ? merged : act + (hoff - I);
-        // upstream gradient from the PRE-update weights (M:473-475)
-        for (int r = tid; r < I; r += TR_THREADS) {
+        // upstream gradient from the PRE-update weights (M:473-475): warp per row
+        for (int r = warp; r < I; r += TR_WARPS) {
           double s = 0.0;
-          for (int c = 0; c < O; ++c) s += (double)W[(int64_t)r * O + c] * dcur[c];
-          dnext[r] = s;
+          for (int c = lane; c < O; c += 32) s += (double)W[(int64_t)r * O + c] * dcur[c];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) dnext[r] = s;
         }
         __syncthreads();
-        // W[r][c] -= ... with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554)
+        // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554)
         for (int t = tid; t < I * O; t += TR_THREADS) {
           const int r = t / O, c = t - r * O;
           const double gr = __dmul_rn(a_in[r], dcur[c]);
@@ -315,7 +370,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         }
         for (int c = tid; c < O; c += TR_THREADS) {  // M:557-572
           const double gr = dcur[c];
-          if (gr != 0.0 || !p.sparse) adagrad(&p.b[l][c], &p.b_acc[l][c], gr, p.lr_nn, pt);
+          if (gr != 0.0 || !p.sparse) adagrad(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt);
         }
         if (l > 0) {
           hoff -= I;
@@ -349,40 +404,20 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       for (int i = tid; i < D; i += TR_THREADS) dv[i] = 0.0;
       __syncthreads();
     }
-    // d_pairs[p] = g + dv[1+p]  (M:484); dp is symmetric (M:492-495)
-    // ---------------------------------------------------------- FFM update (M:490-513)
+    // d_pairs[p] = g + dv[1+p] (M:484); dp symmetric (M:492-495).
     // t[g][:] = dp[f][g] * S[g][f][:]; fields whose t is all zero are skipped (M:502)
-    for (int f = tid; f < F; f += TR_THREADS) {
+    for (int t = tid; t < F * F; t += TR_THREADS) {
+      const int f = t / F, gg = t - f * F;
+      if (gg == f || !pres[f]) continue;
+      const int pp = gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F);
+      const double dpv = g + dv[1 + pp];
+      const double* sgf = S + (gg * F + f) * k;
       int any = 0;
-      if (pres[f]) {
-        for (int gg = 0; gg < F && !any; ++gg) {
-          if (gg == f) continue;
-          const int pp = gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F);
-          const double dpv = g + dv[1 + pp];
-          const double* sgf = S + (gg * F + f) * k;
-          for (int c = 0; c < k; ++c) any |= (dpv * sgf[c]) != 0.0;
-        }
-      }
-      fact[f] = any;
-    }
-    // Sort-and-segment (M:424-437): occurrence order = field order, then slot
-    // order.  lead[s] = first slot holding the same bucket; occf[s] = next slot
-    // of the same bucket (chain), so each unique bucket's gradient is summed in
-    // occurrence order before its single Adagrad step.
-    for (int s = tid; s < FM; s += TR_THREADS) {
-      const int j = sidx[s];
-      int ld = -1, nx = -1;
-      if (j >= 0) {
-        ld = s;
-        for (int s2 = 0; s2 < s; ++s2)
-          if (sidx[s2] == j) { ld = s2; break; }
-        for (int s2 = s + 1; s2 < FM; ++s2)
-          if (sidx[s2] == j) { nx = s2; break; }
-      }
-      lead[s] = ld;
-      occf[s] = nx;
+      for (int c = 0; c < k; ++c) any |= (dpv * sgf[c]) != 0.0;
+      if (any) atomicOr(&fact[f], 1);
     }
     __syncthreads();
+    // ---------------------------------------------------------- FFM update (M:490-513)
     // one thread per (leader slot, latent element): merged gradient in occurrence order
     for (int t = tid; t < FM * Fk; t += TR_THREADS) {
       const int s = t / Fk, gk = t - s * Fk;
@@ -391,7 +426,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       const int j = sidx[s];
       double ug = 0.0;
       bool touched = false;
-      for (int s2 = s; s2 >= 0; s2 = occf[s2]) {
+      for (int s2 = s; s2 >= 0; s2 = nxt[s2]) {
         const int f = s2 / M;
         if (!fact[f]) continue;
         double dpv = 0.0;
@@ -414,16 +449,24 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       if (lead[s] != s) continue;
       const int j = sidx[s];
       double ug = 0.0;
-      for (int s2 = s; s2 >= 0; s2 = occf[s2]) ug += d_lr * sval[s2];
+      for (int s2 = s; s2 >= 0; s2 = nxt[s2]) ug += d_lr * sval[s2];
       adagrad(&p.lr[j], &p.lr_acc[j], ug, p.lr_lr, pt);
     }
     if (tid == 0) adagrad(&p.lr[p.n_buckets], &p.lr_acc[p.n_buckets], d_lr, p.lr_lr, pt);
-    (void)misc;
     __syncthreads();
   }
-}
 
-int fill_model_params(const dffm_model* m, struct FwdParams& p);
+  // ---- write the MLP working copies back (also after an error: the reference
+  // keeps every update applied before the failing example)
+  __syncthreads();
+  if (p.mlp_smem) {
+    for (int l = 0; l < NL; ++l) {
+      const int IO = p.dims[l] * p.dims[l + 1], O = p.dims[l + 1];
+      for (int t = tid; t < IO; t += TR_THREADS) { p.W[l][t] = Wl[l][t]; p.W_acc[l][t] = Wal[l][t]; }
+      for (int t = tid; t < O; t += TR_THREADS) { p.b[l][t] = bl[l][t]; p.b_acc[l][t] = bal[l][t]; }
+    }
+  }
+}
 
 }  // namespace dffm
 
@@ -446,6 +489,7 @@ static int tr_validate(const dffm_model* m, int32_t M, TrainParams& p, int* smem
   p.n_layers = m->n_layers;
   p.hsum = 0;
   p.dmax = p.D;
+  p.mlp_size = 0;
   for (int l = 0; l <= DFFM_MAX_LAYERS; ++l) p.dims[l] = m->dims[l];
   if (p.n_layers) {
     if (m->dims[0] != p.D || m->dims[p.n_layers] != 1) {
@@ -456,6 +500,7 @@ static int tr_validate(const dffm_model* m, int32_t M, TrainParams& p, int* smem
       p.hsum += m->dims[l];
       if (m->dims[l] > p.dmax) p.dmax = m->dims[l];
     }
+    for (int l = 0; l < p.n_layers; ++l) p.mlp_size += m->dims[l] * m->dims[l + 1] + m->dims[l + 1];
   }
   p.lr = (float*)m->lr;
   p.ffm = (float*)m->ffm;
@@ -463,10 +508,12 @@ static int tr_validate(const dffm_model* m, int32_t M, TrainParams& p, int* smem
     p.W[l] = (float*)m->W[l];
     p.b[l] = (float*)m->b[l];
   }
-  const TrSmem L = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax);
-  if (L.total > max_smem_optin_current()) {
-    set_error("trainer needs %d B of shared memory per example state (> %d)", L.total,
-              max_smem_optin_current());
+  const int smax = max_smem_optin_current();
+  TrSmem L = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 2 * p.mlp_size);
+  p.mlp_smem = L.total <= smax;
+  if (!p.mlp_smem) L = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 0);
+  if (L.total > smax) {
+    set_error("trainer needs %d B of shared memory per example state (> %d)", L.total, smax);
     return DFFM_SIZING;
   }
   *smem_out = L.total;
