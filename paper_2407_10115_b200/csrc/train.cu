@@ -59,7 +59,8 @@ struct TrainParams {
 
 struct TrSmem {
   int off_sidx, off_sval, off_pres, off_lrp, off_S, off_v, off_merged, off_pre, off_act, off_d0,
-      off_d1, off_dv, off_nxt, off_lead, off_fact, off_red, off_part, off_mlp, total;
+      off_d1, off_dv, off_nxt, off_lead, off_fact, off_red, off_part, off_dpm, off_ptab, off_ulist,
+      off_gkg, off_sfield, off_mlp, total;
 };
 
 __host__ __device__ inline int a16(int x) { return (x + 15) & ~15; }
@@ -86,6 +87,11 @@ __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int
   s.off_fact = o; o = a16(o + F * 4);
   s.off_red = o; o = a16(o + 64 * 8);
   s.off_part = o; o = a16(o + TR_THREADS * 8);
+  s.off_dpm = o; o = a16(o + F * F * 8);
+  s.off_ptab = o; o = a16(o + (F * (F - 1) / 2) * 2);
+  s.off_ulist = o; o = a16(o + FM * 4 + 16);
+  s.off_gkg = o; o = a16(o + F * k);
+  s.off_sfield = o; o = a16(o + FM);
   s.off_mlp = o; o = a16(o + mlp_floats * 4);
   s.total = o;
   return s;
@@ -154,9 +160,24 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   int* fact = (int*)(smem + L.off_fact);
   double* red = (double*)(smem + L.off_red);
   double* part = (double*)(smem + L.off_part);
+  double* dpm = (double*)(smem + L.off_dpm);
+  uint16_t* ptab = (uint16_t*)(smem + L.off_ptab);
+  int* ulist = (int*)(smem + L.off_ulist);
+  int* nuniq = ulist + FM;
+  unsigned char* gkg = smem + L.off_gkg;
+  unsigned char* sfield = smem + L.off_sfield;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NL = p.n_layers;
   const double pt = p.power_t;
+
+  // constant tables: pair order (M:113-117), latent column -> target field,
+  // slot -> field
+  for (int f1 = tid; f1 < F; f1 += TR_THREADS) {
+    const int base = f1 * F - f1 * (f1 + 1) / 2;
+    for (int f2 = f1 + 1; f2 < F; ++f2) ptab[base + f2 - f1 - 1] = (uint16_t)(f1 | (f2 << 8));
+  }
+  for (int t = tid; t < Fk; t += TR_THREADS) gkg[t] = (unsigned char)(t / k);
+  for (int t = tid; t < FM; t += TR_THREADS) sfield[t] = (unsigned char)(t / M);
 
   // ---- MLP working copies: shared memory for the whole launch when they fit
   float* Wl[DFFM_MAX_LAYERS];
@@ -218,18 +239,22 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       pres[f] = pr;
       lrp[f] = lp;
     }
-    // S[f][g][c] = sum_m x_m * ffm[j_m][g][c]  (M:339); row-coalesced reads
-    for (int t = tid; t < F * Fk; t += TR_THREADS) {
-      const int f = t / Fk, gk = t - f * Fk;
-      double s = 0.0;
-      for (int m = 0; m < M; ++m) {
-        const int j = sidx[f * M + m];
-        if (j >= 0) s += sval[f * M + m] * (double)p.ffm[(int64_t)j * Fk + gk];
+    // S[f][g][c] = sum_m x_m * ffm[j_m][g][c]  (M:339): warp per field,
+    // lanes along the row (coalesced)
+    for (int f = warp; f < F; f += TR_WARPS) {
+      for (int gk = lane; gk < Fk; gk += 32) {
+        double s = 0.0;
+        for (int m = 0; m < M; ++m) {
+          const int j = sidx[f * M + m];
+          if (j >= 0) s += sval[f * M + m] * (double)p.ffm[(int64_t)j * Fk + gk];
+        }
+        S[f * Fk + gk] = s;
       }
-      S[t] = s;
     }
     // sort-and-segment bookkeeping for the update (M:424-437): lead = first
-    // slot holding the bucket, nxt = next slot of the same bucket
+    // slot holding the bucket, nxt = next slot of the same bucket; the
+    // leaders (one per unique bucket, occurrence order) are compacted into
+    // ulist by warp 0
     for (int s = tid; s < FM; s += TR_THREADS) {
       const int j = sidx[s];
       int ld = -1, nx = -1;
@@ -244,13 +269,23 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       nxt[s] = nx;
     }
     __syncthreads();
+    if (warp == 0) {
+      int cnt = 0;
+      for (int s0 = 0; s0 < FM; s0 += 32) {
+        const int s = s0 + lane;
+        const bool isl = s < FM && lead[s] == s;
+        const unsigned bm = __ballot_sync(0xffffffffu, isl);
+        if (isl) ulist[cnt + __popc(bm & ((1u << lane) - 1u))] = s;
+        cnt += __popc(bm);
+      }
+      if (lane == 0) *nuniq = cnt;
+    }
+    __syncthreads();
     // ---------------------------------------------------------- pairs, MergeNorm
     double psum_part = 0.0;
     int ffm_bad = 0;
     for (int pp = tid; pp < P; pp += TR_THREADS) {
-      int f1 = 0, rem = pp;
-      while (rem >= F - 1 - f1) { rem -= F - 1 - f1; ++f1; }
-      const int f2 = f1 + 1 + rem;
+      const int f1 = ptab[pp] & 0xFF, f2 = ptab[pp] >> 8;
       double pv = 0.0;
       if (pres[f1] && pres[f2]) {  // M:346-351
         const double* a = S + (f1 * F + f2) * k;
@@ -362,11 +397,17 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           if (lane == 0) dnext[r] = s;
         }
         __syncthreads();
-        // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554)
-        for (int t = tid; t < I * O; t += TR_THREADS) {
-          const int r = t / O, c = t - r * O;
-          const double gr = __dmul_rn(a_in[r], dcur[c]);
-          if (gr != 0.0 || !p.sparse) adagrad(&W[t], &Wa[t], gr, p.lr_nn, pt);
+        // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554):
+        // warp per row (dead-ReLU rows skipped warp-uniformly), lanes along c
+        for (int r = warp; r < I; r += TR_WARPS) {
+          const double ar = a_in[r];
+          if (ar == 0.0 && p.sparse) continue;
+          float* wr = W + (int64_t)r * O;
+          float* war = Wa + (int64_t)r * O;
+          for (int c = lane; c < O; c += 32) {
+            const double gr = __dmul_rn(ar, dcur[c]);
+            if (gr != 0.0 || !p.sparse) adagrad(&wr[c], &war[c], gr, p.lr_nn, pt);
+          }
         }
         for (int c = tid; c < O; c += TR_THREADS) {  // M:557-572
           const double gr = dcur[c];
@@ -419,29 +460,34 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
     __syncthreads();
     // ---------------------------------------------------------- FFM update (M:490-513)
     // one thread per (leader slot, latent element): merged gradient in occurrence order
-    for (int t = tid; t < FM * Fk; t += TR_THREADS) {
-      const int s = t / Fk, gk = t - s * Fk;
-      if (lead[s] != s) continue;
-      const int gg = gk / k, c = gk - gg * k;
+    // warp per unique bucket, lanes along its row; dp[f][g] precomputed per
+    // (field, target) into dpm (f64) to keep the inner loop division-free
+    for (int t = tid; t < F * F; t += TR_THREADS) {
+      const int f = t / F, gg = t - f * F;  // once per example (F*F = 576)
+      double dpv = 0.0;
+      if (gg != f) dpv = g + dv[1 + (gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F))];
+      dpm[t] = dpv;
+    }
+    __syncthreads();
+    const int nu = *nuniq;
+    for (int u = warp; u < nu; u += TR_WARPS) {
+      const int s = ulist[u];
       const int j = sidx[s];
-      double ug = 0.0;
-      bool touched = false;
-      for (int s2 = s; s2 >= 0; s2 = nxt[s2]) {
-        const int f = s2 / M;
-        if (!fact[f]) continue;
-        double dpv = 0.0;
-        if (gg != f) {
-          const int pp = gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F);
-          dpv = g + dv[1 + pp];
+      float* wrow = p.ffm + (int64_t)j * Fk;
+      float* arow = p.ffm_acc + (int64_t)j * Fk;
+      for (int gk = lane; gk < Fk; gk += 32) {
+        const int gg = gkg[gk], c = gk - gg * k;
+        double ug = 0.0;
+        bool touched = false;
+        for (int s2 = s; s2 >= 0; s2 = nxt[s2]) {
+          const int f = sfield[s2];
+          if (!fact[f]) continue;
+          const double tv = dpm[f * F + gg] * S[(gg * F + f) * k + c];  // t[g][c] (M:501)
+          ug += sval[s2] * tv;  // x * t (M:505), add.at order
+          touched = true;
         }
-        const double tv = dpv * S[(gg * F + f) * k + c];  // t[g][c] (M:501)
-        ug += sval[s2] * tv;                              // x * t (M:505), add.at order
-        touched = true;
-      }
-      if (!touched) continue;
-      if (ug != 0.0 || !p.sparse) {
-        const int64_t wi = (int64_t)j * Fk + gk;
-        adagrad(&p.ffm[wi], &p.ffm_acc[wi], ug, p.lr_ffm, pt);  // M:509-513
+        if (touched && (ug != 0.0 || !p.sparse))
+          adagrad(&wrow[gk], &arow[gk], ug, p.lr_ffm, pt);  // M:509-513
       }
     }
     // ---------------------------------------------------------- LR + bias (M:516-530)
