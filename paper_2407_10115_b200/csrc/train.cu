@@ -256,18 +256,22 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
     // leaders (one per unique bucket, occurrence order) are compacted into
     // ulist by warp 0
     for (int s = tid; s < FM; s += TR_THREADS) {
-      const int j = sidx[s];
-      int ld = -1, nx = -1;
-      if (j >= 0) {
-        ld = s;
-        for (int s2 = 0; s2 < s; ++s2)
-          if (sidx[s2] == j) { ld = s2; break; }
-        for (int s2 = s + 1; s2 < FM; ++s2)
-          if (sidx[s2] == j) { nx = s2; break; }
-      }
-      lead[s] = ld;
-      nxt[s] = nx;
+      lead[s] = sidx[s] >= 0 ? s : -1;
+      nxt[s] = 0x7fffffff;
     }
+    __syncthreads();
+    // all (s, s2) slot pairs in parallel: lead = smallest equal slot, nxt =
+    // smallest equal slot after s
+    for (int t = tid; t < FM * FM; t += TR_THREADS) {
+      const int s = t / FM, s2 = t - s * FM;
+      if (s2 != s && sidx[s] >= 0 && sidx[s2] == sidx[s]) {
+        if (s2 < s) atomicMin(&lead[s], s2);
+        else atomicMin(&nxt[s], s2);
+      }
+    }
+    __syncthreads();
+    for (int s = tid; s < FM; s += TR_THREADS)
+      if (nxt[s] == 0x7fffffff) nxt[s] = -1;
     __syncthreads();
     if (warp == 0) {
       int cnt = 0;
