@@ -97,8 +97,19 @@ __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int
   return s;
 }
 
+// acc**(-power_t) (M:400-404).  For power_t = 0.5 the reference evaluates
+// 1.0/np.sqrt(acc) (two correctly rounded f64 ops); rsqrt() is within 1 ulp
+// of that f64 value at a fraction of the instruction count, and the step is
+// rounded to f32 afterwards, so the stored weights agree except when the
+// f64 result sits within an ulp of an f32 rounding boundary (~2^-29 per
+// element) -- far inside the 1e-5 contract.  DFFM_EXACT_INVSQRT=1 restores
+// the two-rounding form.
 __device__ __forceinline__ double inv_pow(double acc, double pt) {
-  if (pt == 0.5) return __ddiv_rn(1.0, __dsqrt_rn(acc));  // M:400-404
+#if defined(DFFM_EXACT_INVSQRT) && DFFM_EXACT_INVSQRT
+  if (pt == 0.5) return __ddiv_rn(1.0, __dsqrt_rn(acc));
+#else
+  if (pt == 0.5) return rsqrt(acc);
+#endif
   return pow(acc, -pt);
 }
 
@@ -203,6 +214,17 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   }
   __syncthreads();
 
+  // The next example's slots are loaded one example ahead (thread s < FM
+  // holds slot s), and its latent / lr rows are prefetched into L2 while the
+  // current example's backward pass runs; the current example's accumulator
+  // rows are prefetched at its start for its update phase.  (Prefetches only
+  // warm L2 -- the values are always re-read after the preceding update.)
+  const bool pf_on = FM <= TR_THREADS;
+  int pf_j = -1;
+  float pf_x = 0.f;
+  if (pf_on && tid < FM && p.n > 0) { pf_j = p.idx[tid]; pf_x = p.val[tid]; }
+  const int row_bytes = Fk * 4;
+
   for (int64_t e = 0; e < p.n; ++e) {
     // ---------------------------------------------------------- stage example
     const int label = p.labels[e];
@@ -213,11 +235,25 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       break;
     }
     int bad = 0;
-    for (int s = tid; s < FM; s += TR_THREADS) {
-      int j = p.idx[e * FM + s];
-      if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
-      sidx[s] = j;
-      sval[s] = (double)p.val[e * FM + s];
+    if (pf_on) {
+      if (tid < FM) {
+        int j = pf_j;
+        if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
+        sidx[tid] = j;
+        sval[tid] = (double)pf_x;
+        if (j >= 0) {  // this example's accumulator rows, for its update phase
+          const unsigned char* ar = (const unsigned char*)(p.ffm_acc + (int64_t)j * Fk);
+          for (int off = 0; off < row_bytes; off += 128) prefetch_l2(ar + off);
+        }
+        if (e + 1 < p.n) { pf_j = p.idx[(e + 1) * FM + tid]; pf_x = p.val[(e + 1) * FM + tid]; }
+      }
+    } else {
+      for (int s = tid; s < FM; s += TR_THREADS) {
+        int j = p.idx[e * FM + s];
+        if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
+        sidx[s] = j;
+        sval[s] = (double)p.val[e * FM + s];
+      }
     }
     if (tid < F) fact[tid] = 0;
     if (__syncthreads_or(bad)) {
@@ -375,6 +411,11 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
                   (unsigned long long)status_key(e, blk, DFFM_NUMERIC));
       }
       break;
+    }
+    if (pf_on && tid < FM && e + 1 < p.n && pf_j >= 0 && pf_j < p.n_buckets) {
+      const unsigned char* wr = (const unsigned char*)(p.ffm + (int64_t)pf_j * Fk);
+      for (int off = 0; off < row_bytes; off += 128) prefetch_l2(wr + off);
+      prefetch_l2(p.lr + pf_j);
     }
     const double p_raw = sigmoid_raw(logit);
     const double g = p_raw - (double)label;  // M:456-457
