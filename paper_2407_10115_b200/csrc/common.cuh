@@ -71,6 +71,9 @@ __device__ __forceinline__ uint4 ldg_stream16_pred(const void* p, int pred) {
       : "l"(p), "r"(pred));
   return r;
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ uint2 ldg_stream8(const void* p) {
   uint2 r;
   asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
