@@ -10,6 +10,9 @@
 #include "forward_tma.cuh"
 #include "forward_ws.cuh"
 #include "forward_rows.cuh"
+#include "forward_g4.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace dffm {
 
@@ -27,13 +30,18 @@ int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_
 template <typename T>
 int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s);
 
-enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3 };
+template <typename T>
+int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int smem,
+                        cudaStream_t s);
+
+enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3, FAM_G4 = 4 };
 static int forward_family() {
   static int cached = -1;
   if (cached < 0) {
     const char* v = getenv("DFFM_FORWARD_KERNEL");
     cached = FAM_WS;  // measured fastest on cfg2 (see profiles/)
     if (v && strcmp(v, "rows") == 0) cached = FAM_ROWS;
+    if (v && strcmp(v, "g4") == 0) cached = FAM_G4;
     if (v && strcmp(v, "v1") == 0) cached = FAM_V1;
     if (v && strcmp(v, "tma") == 0) cached = FAM_TMA;
   }
@@ -42,6 +50,102 @@ static int forward_family() {
 static bool tma_forward_enabled() { return forward_family() == FAM_TMA; }
 
 int pick_k_template(int k, int wdtype);
+
+// ---- 2-D tensor map over the ffm table (rows = buckets, box = one whole row),
+// encoded through the driver entry point (no -lcuda), cached per table.
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) ==
+            cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+  }
+  return fn;
+}
+
+static int row_tensor_map(const void* base, int wdtype, int64_t rows, int row_elems,
+                          CUtensorMap* out) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, CUtensorMap> cache;
+  const uint64_t key = ((uint64_t)(uintptr_t)base) ^ ((uint64_t)rows << 1) ^
+                       ((uint64_t)row_elems << 40) ^ ((uint64_t)wdtype << 60);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) { *out = it->second; return DFFM_OK; }
+  auto fn = encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return DFFM_CUDA; }
+  const int esz = wdtype == DFFM_W_F32 ? 4 : 2;
+  const CUtensorMapDataType dt = wdtype == DFFM_W_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : wdtype == DFFM_W_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                         : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+  cuuint64_t dims[2] = {(cuuint64_t)row_elems, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_elems * esz};
+  cuuint32_t box[2] = {(cuuint32_t)row_elems, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap tm;
+  CUresult r = fn(&tm, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return DFFM_CUDA;
+  }
+  cache[key] = tm;
+  *out = tm;
+  return DFFM_OK;
+}
+
+// K1 v5: TMA gather4 ring (whole rows per TMA op)
+static bool try_g4_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc) {
+  if (forward_family() != FAM_G4) return false;
+  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
+  const int k = p.k;
+  const int row_elems = p.F * k;
+  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
+  if (row_elems > 256 || (row_elems * esz) % 16 != 0) return false;
+  if (p.F * p.M > 128 || (p.F * p.M) % 4) return false;
+  if (((uintptr_t)p.idx & 15) || ((uintptr_t)p.val & 15) || ((uintptr_t)p.ffm & 15)) return false;
+  for (int l = 1; l < p.n_layers; ++l)
+    if (p.dims[l] % 4) return false;
+  static int te_env = -1, smem_cap = -1;
+  if (te_env < 0) {
+    const char* v = getenv("DFFM_G4_TE");
+    te_env = v ? atoi(v) : 16;
+    if (te_env < 4 || te_env > 64 || (te_env & 3)) te_env = 16;
+    const char* c = getenv("DFFM_G4_SMEM_KB");  // leave the rest of the SM's 256 KB to L1
+    smem_cap = c ? atoi(c) * 1024 : 160 * 1024;
+  }
+  G4Params q{};
+  q.row_bytes = row_elems * esz;
+  q.quad_bytes = 4 * q.row_bytes;
+  const int cap = smem_cap < smax ? smem_cap : smax;
+  for (int TE = te_env; TE >= 4; TE >>= 1) {
+    p.TE = TE;
+    p.XS = TE + 4;
+    const G4Smem L0 = g4_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.quad_bytes, 0);
+    const int quads = (cap - L0.total - 128) / q.quad_bytes;
+    const int need = (p.F * p.M + 3) / 4;
+    if (quads < 2 * need || quads * 4 > 32767) continue;
+    q.ring_quads = quads;
+    q.f = p;
+    const G4Smem L = g4_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.quad_bytes, quads);
+    CUtensorMap tm;
+    int r = row_tensor_map(p.ffm, m->wdtype, p.n_buckets, row_elems, &tm);
+    if (r) { *rc = r; return true; }
+    switch (m->wdtype) {
+      case DFFM_W_F32: *rc = launch_forward_g4_t<float>(tm, q, k, L.total, s); break;
+      case DFFM_W_BF16: *rc = launch_forward_g4_t<__nv_bfloat16>(tm, q, k, L.total, s); break;
+      default: *rc = launch_forward_g4_t<uint16_t>(tm, q, k, L.total, s); break;
+    }
+    return true;
+  }
+  return false;
+}
 
 // K1 v4: row-coalesced gather (F <= 32, 16/32/64-byte segments)
 static bool try_rows_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
@@ -225,6 +329,7 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   p.status_base = status_base;
   p.M = max_per_field;
   const int smax = max_smem_optin_current();
+  if (try_g4_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_rows_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_ws_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_tma_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;

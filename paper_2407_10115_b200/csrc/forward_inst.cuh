@@ -9,6 +9,7 @@
 #include "forward_tma.cuh"
 #include "forward_ws.cuh"
 #include "forward_rows.cuh"
+#include "forward_g4.cuh"
 
 namespace dffm {
 
@@ -149,5 +150,36 @@ int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s) {
 }
 
 template int launch_forward_rows_t<DFFM_INST_T>(const FwdParams&, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------- K1 v5 (TMA gather4)
+using G4Kernel = void (*)(const CUtensorMap, G4Params);
+
+template <typename T>
+static G4Kernel select_g4(int K) {
+  if constexpr (sizeof(T) == 4) {
+    if (K == 4) return fwd_g4_kernel<4, T>;
+  }
+  if (K == 8) return fwd_g4_kernel<8, T>;
+  if (K == 16) return fwd_g4_kernel<16, T>;
+  return nullptr;
+}
+
+template <typename T>
+int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int smem,
+                        cudaStream_t s) {
+  G4Kernel kern = select_g4<T>(K);
+  if (!kern) { set_error("no gather4 kernel for k=%d", K); return DFFM_SIZING; }
+  int occ = 0;
+  int rc = kernel_occupancy((const void*)kern, G4_THREADS, smem, &occ);
+  if (rc) return rc;
+  const int64_t ntiles = (q.f.n + q.f.TE - 1) / q.f.TE;
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current());
+  kern<<<(unsigned)grid, G4_THREADS, smem, s>>>(tm, q);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_g4)");
+  return DFFM_OK;
+}
+
+template int launch_forward_g4_t<DFFM_INST_T>(const CUtensorMap&, const G4Params&, int, int,
+                                              cudaStream_t);
 
 }  // namespace dffm

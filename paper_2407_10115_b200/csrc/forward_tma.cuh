@@ -210,7 +210,7 @@ fwd_tma_kernel(TmaParams q) {
         if (lane >= o) incl += v;
       }
       const int total = __shfl_sync(0xffffffffu, incl, 31);
-      while (head + total - tail > RR) {
+      while (ole + TMA_NS <= le || head + total - tail > RR) {
         mbar_wait(&empty[ole % TMA_NS], (uint32_t)((ole / TMA_NS) & 1));
         tail = slot_end[ole % TMA_NS];
         ++ole;
