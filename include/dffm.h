@@ -96,6 +96,15 @@ int dffm_forward(const dffm_model* model, const int32_t* idx, const float* val,
                  int64_t status_base, uint64_t* status, void* stream);
 
 /*
+ * K1 kernel family (all compute identical results within the 1e-5 contract;
+ * shapes a family cannot take fall back to family 2):
+ *   0 row-coalesced, 1 warp-specialised (default), 2 CTA-synchronous,
+ *   3 TMA 1-D ring, 4 TMA gather4 ring, -1 = from DFFM_FORWARD_KERNEL.
+ * Process-wide; for A/B measurements and tests.
+ */
+int dffm_set_forward_family(int32_t family);
+
+/*
  * K3 context-cached scorer (no reference code).  Request r
  * has ctx fields [0, n_ctx_fields) in ctx_idx[r][n_ctx_fields][ctx_m] and
  * n_cand candidates with fields [n_ctx_fields, F) in

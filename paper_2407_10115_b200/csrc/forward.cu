@@ -35,17 +35,18 @@ int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int sme
                         cudaStream_t s);
 
 enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3, FAM_G4 = 4 };
+static int g_family = -1;  // set by env (first call) or dffm_set_forward_family()
 static int forward_family() {
-  static int cached = -1;
-  if (cached < 0) {
+  if (g_family < 0) {
     const char* v = getenv("DFFM_FORWARD_KERNEL");
-    cached = FAM_WS;  // measured fastest on cfg2 (see profiles/)
-    if (v && strcmp(v, "rows") == 0) cached = FAM_ROWS;
-    if (v && strcmp(v, "g4") == 0) cached = FAM_G4;
-    if (v && strcmp(v, "v1") == 0) cached = FAM_V1;
-    if (v && strcmp(v, "tma") == 0) cached = FAM_TMA;
+    int f = FAM_WS;  // measured fastest on cfg2 (see profiles/)
+    if (v && strcmp(v, "rows") == 0) f = FAM_ROWS;
+    if (v && strcmp(v, "g4") == 0) f = FAM_G4;
+    if (v && strcmp(v, "v1") == 0) f = FAM_V1;
+    if (v && strcmp(v, "tma") == 0) f = FAM_TMA;
+    g_family = f;
   }
-  return cached;
+  return g_family;
 }
 static bool tma_forward_enabled() { return forward_family() == FAM_TMA; }
 
@@ -307,6 +308,12 @@ int pick_k_template(int k, int wdtype) {
 }  // namespace dffm
 
 using namespace dffm;
+
+extern "C" int dffm_set_forward_family(int32_t family) {
+  if (family < -1 || family > FAM_G4) { set_error("bad forward family %d", family); return DFFM_CONTRACT; }
+  g_family = family;  // -1: re-read DFFM_FORWARD_KERNEL on the next call
+  return DFFM_OK;
+}
 
 extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const float* val,
                             int32_t max_per_field, int64_t n, float* prob, float* logit_opt,

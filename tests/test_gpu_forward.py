@@ -73,6 +73,32 @@ def test_forward_matches_oracle(F, k, hidden, M, bits, n):
     assert rel_err(p, ref).max() < RTOL
 
 
+@pytest.mark.parametrize("family", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("wdtype", ["f32", "bf16", "u16"])
+def test_every_forward_family_matches_oracle(family, wdtype):
+    """All five K1 kernel families (row-coalesced, warp-specialised,
+    CTA-synchronous, TMA-ring, TMA-gather4) on cfg2-shaped inputs and every
+    table storage type."""
+    from paper_2407_10115_b200 import _lib
+    from paper_2407_10115_b200.quant import quantize_store
+    wl = configs.CFG2
+    ost = fo.random_store(24, 8, (64, 32), 12, seed=4)
+    idx, val = synth.make_examples(wl, 1537, seed=8, hash_bits=12)
+    st = store_from_oracle(ost)
+    if wdtype == "bf16":
+        st = WeightStore.from_flat(st.config, ost.flat(False), DEV, "bf16", False)
+    elif wdtype == "u16":
+        st, _ = quantize_store(st)
+    _lib.check(_lib.lib().dffm_set_forward_family(family))
+    try:
+        p = predict_batch(idx, val, st).double().cpu().numpy()
+    finally:
+        _lib.lib().dffm_set_forward_family(-1)
+    cst, ridx, _ = compact_oracle(st, idx.numpy())
+    _, ref = fo.forward_batch(ridx, val.numpy(), cst)
+    assert rel_err(p, ref).max() < RTOL
+
+
 def test_forward_bf16_and_u16_tables_match_widened_oracle():
     from paper_2407_10115_b200.quant import quantize_store
     wl = configs.CFG2
