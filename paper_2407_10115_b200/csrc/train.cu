@@ -21,7 +21,9 @@
 //   duplicate buckets across fields: gradients summed in occurrence order
 //             before one update (sort-and-segment, M:424-437)
 //   sparse    zero-gradient slots are skipped; byte-identical to dense (M:536-572)
+#include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -29,6 +31,7 @@ namespace dffm {
 
 constexpr int TR_THREADS = 1024;
 constexpr int TR_WARPS = TR_THREADS / 32;
+constexpr int TR_CLUSTER = 8;  // CTAs per cluster for the split trainer
 
 struct TrainParams {
   const int32_t* idx;
@@ -60,7 +63,7 @@ struct TrainParams {
 struct TrSmem {
   int off_sidx, off_sval, off_pres, off_lrp, off_S, off_v, off_merged, off_pre, off_act, off_d0,
       off_d1, off_dv, off_nxt, off_lead, off_fact, off_red, off_part, off_dpm, off_ptab, off_ulist,
-      off_gkg, off_sfield, off_mlp, total;
+      off_gkg, off_sfield, off_zbuf, off_dpart, off_mlp, total;
 };
 
 __host__ __device__ inline int a16(int x) { return (x + 15) & ~15; }
@@ -92,6 +95,8 @@ __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int
   s.off_ulist = o; o = a16(o + FM * 4 + 16);
   s.off_gkg = o; o = a16(o + F * k);
   s.off_sfield = o; o = a16(o + FM);
+  s.off_zbuf = o; o = a16(o + dmax * 8);
+  s.off_dpart = o; o = a16(o + D * 8);
   s.off_mlp = o; o = a16(o + mlp_floats * 4);
   s.total = o;
   return s;
@@ -116,6 +121,15 @@ __device__ __forceinline__ void adagrad(float* w, float* acc, double g, double l
   *acc = __double2float_rn(a64);
   const double step = __dmul_rn(__dmul_rn(lr, g), inv_pow(a64, pt));
   *w = __double2float_rn(__dsub_rn((double)*w, step));
+}
+
+// Same step on a global-memory slot shared across the cluster's SMs: L2-only
+// accesses so no CTA can read a stale L1 line of another SM's update.
+__device__ __forceinline__ void adagrad_g(float* w, float* acc, double g, double lr, double pt) {
+  const double a64 = __dadd_rn((double)__ldcg(acc), __dmul_rn(g, g));
+  __stcg(acc, __double2float_rn(a64));
+  const double step = __dmul_rn(__dmul_rn(lr, g), inv_pow(a64, pt));
+  __stcg(w, __double2float_rn(__dsub_rn((double)__ldcg(w), step)));
 }
 
 // Block-wide f64 sum (all threads call); result broadcast to all.
@@ -146,6 +160,7 @@ __device__ __forceinline__ double sigmoid_raw(double logit) {  // M:293-297
   return e / (1.0 + e);
 }
 
+template <int C>
 __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int F = p.F, M = p.M, k = p.k, P = p.P, D = p.D, FM = F * M, Fk = F * k;
@@ -187,29 +202,48 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   for (int t = tid; t < Fk; t += TR_THREADS) gkg[t] = (unsigned char)(t / k);
   for (int t = tid; t < FM; t += TR_THREADS) sfield[t] = (unsigned char)(t / M);
 
-  // ---- MLP working copies: shared memory for the whole launch when they fit
+  // ---- cluster split (C > 1): CTA `rank` owns layer-0 columns [c0, c0+W0)
+  // (weights, accumulators, GEMV partials, updates), every other layer and the
+  // forward chain are replicated (identical deterministic updates in every CTA)
+  const int rank = C > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int W0 = (C > 1 && NL > 1) ? p.dims[1] / C : (NL > 0 ? p.dims[1] : 0);
+  const int c0 = (C > 1 && NL > 1) ? rank * W0 : 0;
+  double* zbuf = (double*)(smem + L.off_zbuf);
+  double* dpart = (double*)(smem + L.off_dpart);
+
+  // ---- MLP working copies: shared memory for the whole launch when they fit.
+  // Layer 0 is stored as its [I][W0] column slice (W0 = O when C == 1).
   float* Wl[DFFM_MAX_LAYERS];
   float* bl[DFFM_MAX_LAYERS];
   float* Wal[DFFM_MAX_LAYERS];
   float* bal[DFFM_MAX_LAYERS];
+  int ldw[DFFM_MAX_LAYERS];  // row stride of the working copy
   {
     float* mw = (float*)(smem + L.off_mlp);
     float* ma = mw + p.mlp_size;
     int off = 0;
     for (int l = 0; l < NL; ++l) {
-      const int IO = p.dims[l] * p.dims[l + 1], O = p.dims[l + 1];
+      const int I = p.dims[l], O = p.dims[l + 1];
+      const bool split = (C > 1 && l == 0 && NL > 1);
+      const int Ow = split ? W0 : O, cb = split ? c0 : 0;
+      ldw[l] = p.mlp_smem ? Ow : O;
       if (p.mlp_smem) {
-        Wl[l] = mw + off; bl[l] = mw + off + IO;
-        Wal[l] = ma + off; bal[l] = ma + off + IO;
-        for (int t = tid; t < IO; t += TR_THREADS) { Wl[l][t] = p.W[l][t]; Wal[l][t] = p.W_acc[l][t]; }
-        for (int t = tid; t < O; t += TR_THREADS) { bl[l][t] = p.b[l][t]; bal[l][t] = p.b_acc[l][t]; }
+        Wl[l] = mw + off; bl[l] = mw + off + I * Ow;
+        Wal[l] = ma + off; bal[l] = ma + off + I * Ow;
+        for (int t = tid; t < I * Ow; t += TR_THREADS) {
+          const int i = t / Ow, c = t - i * Ow;
+          Wl[l][t] = p.W[l][(int64_t)i * O + cb + c];
+          Wal[l][t] = p.W_acc[l][(int64_t)i * O + cb + c];
+        }
+        for (int t = tid; t < Ow; t += TR_THREADS) { bl[l][t] = p.b[l][cb + t]; bal[l][t] = p.b_acc[l][cb + t]; }
+        off += I * Ow + Ow;
       } else {
-        Wl[l] = p.W[l]; bl[l] = p.b[l]; Wal[l] = p.W_acc[l]; bal[l] = p.b_acc[l];
+        Wl[l] = p.W[l] + cb; bl[l] = p.b[l] + cb; Wal[l] = p.W_acc[l] + cb; bal[l] = p.b_acc[l] + cb;
       }
-      off += IO + O;
     }
   }
-  __syncthreads();
+  if (C > 1) cooperative_groups::this_cluster().sync();  // every CTA resident before DSMEM use
+  else __syncthreads();
 
   // The next example's slots are loaded one example ahead (thread s < FM
   // holds slot s), and its latent / lr rows are prefetched into L2 while the
@@ -266,7 +300,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         const int j = sidx[f * M + m];
         if (j >= 0) {
           pr = 1;
-          lp += (double)p.lr[j] * sval[f * M + m];  // M:338 np.dot(lr[idx], x)
+          lp += (double)__ldcg(p.lr + j) * sval[f * M + m];  // M:338 np.dot(lr[idx], x)
         }
       }
       pres[f] = pr;
@@ -279,7 +313,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         double s = 0.0;
         for (int m = 0; m < M; ++m) {
           const int j = sidx[f * M + m];
-          if (j >= 0) s += sval[f * M + m] * (double)p.ffm[(int64_t)j * Fk + gk];
+          if (j >= 0) s += sval[f * M + m] * (double)__ldcg(p.ffm + (int64_t)j * Fk + gk);
         }
         S[f * Fk + gk] = s;
       }
@@ -334,7 +368,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       ffm_bad |= !isfinite(pv);
     }
     if (tid == 0) {
-      double lo = (double)p.lr[p.n_buckets];  // bias, M:327
+      double lo = (double)__ldcg(p.lr + p.n_buckets);  // bias, M:327
       for (int f = 0; f < F; ++f)
         if (pres[f]) lo += lrp[f];
       v[0] = lo;
@@ -364,30 +398,47 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       int hoff = 0;
       for (int l = 0; l + 1 < NL; ++l) {
         const int I = p.dims[l], O = p.dims[l + 1];
+        const bool split = (C > 1 && l == 0);
+        const int Ow = split ? W0 : O, ld = ldw[l];
         const float* W = Wl[l];
         // split-K: thread (part, o), o fastest -> conflict-free W reads;
         // partials reduced in fixed part order (deterministic)
-        const int G = O <= TR_THREADS ? TR_THREADS / O : 1;
+        const int G = Ow <= TR_THREADS ? TR_THREADS / Ow : 1;
         if (G > 1) {
-          const int o = tid % O, pa = tid / O;
+          const int o = tid % Ow, pa = tid / Ow;
           if (pa < G) {
             double s = 0.0;
-            for (int i = pa; i < I; i += G) s += a[i] * (double)W[(int64_t)i * O + o];
-            part[pa * O + o] = s;
+            for (int i = pa; i < I; i += G) s += a[i] * (double)W[(int64_t)i * ld + o];
+            part[pa * Ow + o] = s;
           }
           __syncthreads();
         }
-        for (int o = tid; o < O; o += TR_THREADS) {
+        for (int o = tid; o < Ow; o += TR_THREADS) {
           double z = 0.0;
           if (G > 1) {
-            for (int q = 0; q < G; ++q) z += part[q * O + o];
+            for (int q = 0; q < G; ++q) z += part[q * Ow + o];
           } else {
-            for (int i = 0; i < I; ++i) z += a[i] * (double)W[(int64_t)i * O + o];
+            for (int i = 0; i < I; ++i) z += a[i] * (double)W[(int64_t)i * ld + o];
           }
           z += (double)bl[l][o];  // M:368
-          pre[hoff + o] = z;
-          act[hoff + o] = (z != z) ? z : fmax(z, 0.0);  // np.maximum (M:370)
-          nn_bad |= !isfinite(z);
+          if (split) {
+            // owner broadcasts its columns' pre-activations to every CTA (DSMEM)
+            for (int rk = 0; rk < C; ++rk)
+              cooperative_groups::this_cluster().map_shared_rank(zbuf, rk)[c0 + o] = z;
+          } else {
+            pre[hoff + o] = z;
+            act[hoff + o] = (z != z) ? z : fmax(z, 0.0);  // np.maximum (M:370)
+            nn_bad |= !isfinite(z);
+          }
+        }
+        if (split) {
+          cooperative_groups::this_cluster().sync();
+          for (int o = tid; o < O; o += TR_THREADS) {
+            const double z = zbuf[o];
+            pre[hoff + o] = z;
+            act[hoff + o] = (z != z) ? z : fmax(z, 0.0);
+            nn_bad |= !isfinite(z);
+          }
         }
         __syncthreads();
         a = act + hoff;
@@ -400,8 +451,8 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       nn_bad = __syncthreads_or(nn_bad);
     }
     const double logit = nn_out + lr_out + psum;  // M:377
-    if (!isfinite(logit)) {  // M:392-396 (uniform across the block)
-      if (tid == 0) {
+    if (!isfinite(logit)) {  // M:392-396 (uniform across the block and the cluster)
+      if (tid == 0 && rank == 0) {
         const int blk = !isfinite(lr_out) ? DFFM_BLOCK_LR : ffm_bad ? DFFM_BLOCK_FFM
                       : merge_bad ? DFFM_BLOCK_MERGE : nn_bad ? DFFM_BLOCK_NN : DFFM_BLOCK_LOGIT;
         atomicMin((unsigned long long*)p.status,
@@ -409,14 +460,14 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       }
       break;
     }
-    if (pf_on && tid < FM && e + 1 < p.n && pf_j >= 0 && pf_j < p.n_buckets) {
+    if (pf_on && rank == 0 && tid < FM && e + 1 < p.n && pf_j >= 0 && pf_j < p.n_buckets) {
       const unsigned char* wr = (const unsigned char*)(p.ffm + (int64_t)pf_j * Fk);
       for (int off = 0; off < row_bytes; off += 128) prefetch_l2(wr + off);
       prefetch_l2(p.lr + pf_j);
     }
     const double p_raw = sigmoid_raw(logit);
     const double g = p_raw - (double)label;  // M:456-457
-    if (tid == 0) p.prob_out[e] = fmin(fmax(p_raw, 1e-7), 1.0 - 1e-7);  // predict_proba
+    if (tid == 0 && rank == 0) p.prob_out[e] = fmin(fmax(p_raw, 1e-7), 1.0 - 1e-7);
     // ---------------------------------------------------------- MLP backward + update
     double* dmerged = d1;
     if (NL > 0) {
@@ -427,16 +478,28 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       int hoff = p.hsum;
       for (int l = NL - 1; l >= 0; --l) {
         const int I = p.dims[l], O = p.dims[l + 1];
+        const bool split = (C > 1 && l == 0);
+        const int Ow = split ? W0 : O, cb = split ? c0 : 0, ld = ldw[l];
         float* W = Wl[l];
         float* Wa = Wal[l];
         const double* a_in = l == 0 ? merged : act + (hoff - I);
         // upstream gradient from the PRE-update weights (M:473-475): warp per row
+        // (split layer: partial over this CTA's columns, reduced across the cluster)
         for (int r = warp; r < I; r += TR_WARPS) {
           double s = 0.0;
-          for (int c = lane; c < O; c += 32) s += (double)W[(int64_t)r * O + c] * dcur[c];
+          for (int c = lane; c < Ow; c += 32) s += (double)W[(int64_t)r * ld + c] * dcur[cb + c];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) dnext[r] = s;
+          if (lane == 0) (split ? dpart : dnext)[r] = s;
+        }
+        if (split) {
+          cooperative_groups::this_cluster().sync();
+          for (int r = tid; r < I; r += TR_THREADS) {
+            double s = 0.0;
+            for (int rk = 0; rk < C; ++rk)
+              s += cooperative_groups::this_cluster().map_shared_rank(dpart, rk)[r];
+            dnext[r] = s;
+          }
         }
         __syncthreads();
         // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554):
@@ -444,15 +507,15 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         for (int r = warp; r < I; r += TR_WARPS) {
           const double ar = a_in[r];
           if (ar == 0.0 && p.sparse) continue;
-          float* wr = W + (int64_t)r * O;
-          float* war = Wa + (int64_t)r * O;
-          for (int c = lane; c < O; c += 32) {
-            const double gr = __dmul_rn(ar, dcur[c]);
+          float* wr = W + (int64_t)r * ld;
+          float* war = Wa + (int64_t)r * ld;
+          for (int c = lane; c < Ow; c += 32) {
+            const double gr = __dmul_rn(ar, dcur[cb + c]);
             if (gr != 0.0 || !p.sparse) adagrad(&wr[c], &war[c], gr, p.lr_nn, pt);
           }
         }
-        for (int c = tid; c < O; c += TR_THREADS) {  // M:557-572
-          const double gr = dcur[c];
+        for (int c = tid; c < Ow; c += TR_THREADS) {  // M:557-572
+          const double gr = dcur[cb + c];
           if (gr != 0.0 || !p.sparse) adagrad(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt);
         }
         if (l > 0) {
@@ -512,7 +575,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
     }
     __syncthreads();
     const int nu = *nuniq;
-    for (int u = warp; u < nu; u += TR_WARPS) {
+    for (int u = rank * TR_WARPS + warp; u < nu; u += C * TR_WARPS) {  // rows split over the cluster
       const int s = ulist[u];
       const int j = sidx[s];
       float* wrow = p.ffm + (int64_t)j * Fk;
@@ -529,19 +592,24 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           touched = true;
         }
         if (touched && (ug != 0.0 || !p.sparse))
-          adagrad(&wrow[gk], &arow[gk], ug, p.lr_ffm, pt);  // M:509-513
+          adagrad_g(&wrow[gk], &arow[gk], ug, p.lr_ffm, pt);  // M:509-513
       }
     }
     // ---------------------------------------------------------- LR + bias (M:516-530)
-    for (int s = tid; s < FM; s += TR_THREADS) {
-      if (lead[s] != s) continue;
-      const int j = sidx[s];
-      double ug = 0.0;
-      for (int s2 = s; s2 >= 0; s2 = nxt[s2]) ug += d_lr * sval[s2];
-      adagrad(&p.lr[j], &p.lr_acc[j], ug, p.lr_lr, pt);
+    if (rank == C - 1) {  // the last CTA has the fewest FFM rows
+      for (int s = tid; s < FM; s += TR_THREADS) {
+        if (lead[s] != s) continue;
+        const int j = sidx[s];
+        double ug = 0.0;
+        for (int s2 = s; s2 >= 0; s2 = nxt[s2]) ug += d_lr * sval[s2];
+        adagrad_g(&p.lr[j], &p.lr_acc[j], ug, p.lr_lr, pt);
+      }
+      if (tid == 0) adagrad_g(&p.lr[p.n_buckets], &p.lr_acc[p.n_buckets], d_lr, p.lr_lr, pt);
     }
-    if (tid == 0) adagrad(&p.lr[p.n_buckets], &p.lr_acc[p.n_buckets], d_lr, p.lr_lr, pt);
-    __syncthreads();
+    // every table write of this example is visible cluster-wide before the
+    // next example reads (release/acquire at cluster scope; table reads are L2-only)
+    if (C > 1) cooperative_groups::this_cluster().sync();
+    else __syncthreads();
   }
 
   // ---- write the MLP working copies back (also after an error: the reference
@@ -549,18 +617,26 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   __syncthreads();
   if (p.mlp_smem) {
     for (int l = 0; l < NL; ++l) {
-      const int IO = p.dims[l] * p.dims[l + 1], O = p.dims[l + 1];
-      for (int t = tid; t < IO; t += TR_THREADS) { p.W[l][t] = Wl[l][t]; p.W_acc[l][t] = Wal[l][t]; }
-      for (int t = tid; t < O; t += TR_THREADS) { p.b[l][t] = bl[l][t]; p.b_acc[l][t] = bal[l][t]; }
+      const int I = p.dims[l], O = p.dims[l + 1];
+      const bool split = (C > 1 && l == 0 && NL > 1);
+      if (!split && rank != 0) continue;  // replicated layers: one writer
+      const int Ow = split ? W0 : O, cb = split ? c0 : 0;
+      for (int t = tid; t < I * Ow; t += TR_THREADS) {
+        const int i = t / Ow, c = t - i * Ow;
+        p.W[l][(int64_t)i * O + cb + c] = Wl[l][t];
+        p.W_acc[l][(int64_t)i * O + cb + c] = Wal[l][t];
+      }
+      for (int t = tid; t < Ow; t += TR_THREADS) { p.b[l][cb + t] = bl[l][t]; p.b_acc[l][cb + t] = bal[l][t]; }
     }
   }
+  if (C > 1) cooperative_groups::this_cluster().sync();  // no CTA exits while DSMEM is in use
 }
 
 }  // namespace dffm
 
 using namespace dffm;
 
-static int tr_validate(const dffm_model* m, int32_t M, TrainParams& p, int* smem_out) {
+static int tr_validate(const dffm_model* m, int32_t M, int C, TrainParams& p, int* smem_out) {
   if (!m) { set_error("null model"); return DFFM_CONTRACT; }
   if (m->wdtype != DFFM_W_F32) { set_error("training needs f32 tables"); return DFFM_CONTRACT; }
   if (m->n_fields < 1 || m->k < 1 || M < 1) { set_error("bad shape"); return DFFM_CONTRACT; }
@@ -588,7 +664,10 @@ static int tr_validate(const dffm_model* m, int32_t M, TrainParams& p, int* smem
       p.hsum += m->dims[l];
       if (m->dims[l] > p.dmax) p.dmax = m->dims[l];
     }
-    for (int l = 0; l < p.n_layers; ++l) p.mlp_size += m->dims[l] * m->dims[l + 1] + m->dims[l + 1];
+    for (int l = 0; l < p.n_layers; ++l) {
+      const int Ow = (C > 1 && l == 0) ? m->dims[1] / C : m->dims[l + 1];  // layer-0 slice
+      p.mlp_size += m->dims[l] * Ow + Ow;
+    }
   }
   p.lr = (float*)m->lr;
   p.ffm = (float*)m->ffm;
@@ -617,7 +696,22 @@ extern "C" int dffm_train_sequential(const dffm_model* model, const dffm_train_s
   (void)scratch;
   TrainParams p{};
   int smem = 0;
-  int rc = tr_validate(model, max_per_field, p, &smem);
+  // cluster split when layer 0 divides evenly (DFFM_TRAIN_CLUSTER=1 forces one CTA)
+  int C = 1;
+  {
+    static int env = -1;
+    if (env < 0) {
+      const char* v = getenv("DFFM_TRAIN_CLUSTER");
+      env = v ? atoi(v) : TR_CLUSTER;
+    }
+    if (env == TR_CLUSTER && model && model->n_layers >= 2 && model->dims[1] % TR_CLUSTER == 0)
+      C = TR_CLUSTER;
+  }
+  int rc = tr_validate(model, max_per_field, C, p, &smem);
+  if (rc == DFFM_SIZING && C > 1) {
+    C = 1;
+    rc = tr_validate(model, max_per_field, C, p, &smem);
+  }
   if (rc) return rc;
   if (!state || !state->lr_acc || !state->ffm_acc) {
     set_error("null optimizer state");
@@ -648,9 +742,28 @@ extern "C" int dffm_train_sequential(const dffm_model* model, const dffm_train_s
   p.status = status;
   p.n = n;
   int occ = 0;
-  rc = kernel_occupancy((const void*)train_kernel, TR_THREADS, smem, &occ);
-  if (rc) return rc;
-  train_kernel<<<1, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
+  if (C == 1) {
+    rc = kernel_occupancy((const void*)train_kernel<1>, TR_THREADS, smem, &occ);
+    if (rc) return rc;
+    train_kernel<1><<<1, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
+  } else {
+    // one thread-block cluster of C CTAs on C SMs (DSMEM exchange per example)
+    rc = kernel_occupancy((const void*)train_kernel<TR_CLUSTER>, TR_THREADS, smem, &occ);
+    if (rc) return rc;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(TR_CLUSTER);
+    cfg.blockDim = dim3(TR_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = TR_CLUSTER;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DFFM_CUDA_TRY(cudaLaunchKernelEx(&cfg, train_kernel<TR_CLUSTER>, p), "launch(train cluster)");
+  }
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(train)");
   return DFFM_OK;
 }
