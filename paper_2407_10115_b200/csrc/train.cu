@@ -29,7 +29,10 @@
 
 namespace dffm {
 
-constexpr int TR_THREADS = 1024;
+#ifndef DFFM_TR_THREADS
+#define DFFM_TR_THREADS 1024
+#endif
+constexpr int TR_THREADS = DFFM_TR_THREADS;
 constexpr int TR_WARPS = TR_THREADS / 32;
 constexpr int TR_CLUSTER = 8;  // CTAs per cluster for the split trainer
 
@@ -88,7 +91,7 @@ __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int
   s.off_nxt = o; o = a16(o + FM * 4);
   s.off_lead = o; o = a16(o + FM * 4);
   s.off_fact = o; o = a16(o + F * 4);
-  s.off_red = o; o = a16(o + 64 * 8);
+  s.off_red = o; o = a16(o + 2 * TR_WARPS * 8);  // two ping-pong slots
   s.off_part = o; o = a16(o + TR_THREADS * 8);
   s.off_dpm = o; o = a16(o + F * F * 8);
   s.off_ptab = o; o = a16(o + (F * (F - 1) / 2) * 2);
@@ -132,22 +135,23 @@ __device__ __forceinline__ void adagrad_g(float* w, float* acc, double g, double
   __stcg(w, __double2float_rn(__dsub_rn((double)__ldcg(w), step)));
 }
 
-// Block-wide f64 sum (all threads call); result broadcast to all.
-__device__ double block_sum(double v, double* red) {
+// Block-wide f64 sum (all threads call); result broadcast to all.  One
+// barrier: warps publish partials into a ping-pong slot, then every thread
+// folds the TR_WARPS partials itself in a fixed order (deterministic).
+__device__ double block_sum(double v, double* red, int& ctr) {
+  // every thread calls block_sum the same number of times, so the per-thread
+  // call counter selects the same ping-pong slot block-wide; reusing a slot
+  // two calls later is ordered by the intervening call's barrier
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  double* slot = red + (++ctr & 1) * TR_WARPS;
+  if (lane == 0) slot[warp] = v;
   __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double t = threadIdx.x < TR_WARPS ? red[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (threadIdx.x == 0) red[32] = t;
-  }
-  __syncthreads();
-  return red[32];
+  double t = 0.0;
+#pragma unroll 8
+  for (int w = 0; w < TR_WARPS; ++w) t += slot[w];
+  return t;
 }
 
 __device__ __forceinline__ int tr_pair_pos(int a, int b, int F) {
@@ -192,6 +196,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NL = p.n_layers;
   const double pt = p.power_t;
+  int bsc = 0;  // block_sum call counter (same in every thread)
 
   // constant tables: pair order (M:113-117), latent column -> target field,
   // slot -> field
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         if (pres[f]) lo += lrp[f];
       v[0] = lo;
     }
-    const double psum = block_sum(psum_part, red);
+    const double psum = block_sum(psum_part, red, bsc);
     ffm_bad = __syncthreads_or(ffm_bad);
     const double lr_out = v[0];
     const double mu = (psum + lr_out) / D;
@@ -382,7 +387,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       const double c = v[i] - mu;
       sq_part += c * c;
     }
-    const double sd = sqrt(block_sum(sq_part, red) / D);  // np.std (population)
+    const double sd = sqrt(block_sum(sq_part, red, bsc) / D);  // np.std (population)
     const double denom = sd + 1e-6;
     int merge_bad = 0;
     for (int i = tid; i < D; i += TR_THREADS) {
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       const int I = p.dims[NL - 1];
       double s = 0.0;
       for (int i = tid; i < I; i += TR_THREADS) s += a[i] * (double)Wl[NL - 1][i];
-      nn_out = block_sum(s, red) + (double)bl[NL - 1][0];  // M:372-373
+      nn_out = block_sum(s, red, bsc) + (double)bl[NL - 1][0];  // M:372-373
       nn_bad = __syncthreads_or(nn_bad);
     }
     const double logit = nn_out + lr_out + psum;  // M:377
@@ -536,8 +541,8 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         s_d += dmerged[i];
         s_dc += dmerged[i] * (v[i] - mu);
       }
-      const double mean_d = block_sum(s_d, red) / D;
-      const double dot_dc = block_sum(s_dc, red);
+      const double mean_d = block_sum(s_d, red, bsc) / D;
+      const double dot_dc = block_sum(s_dc, red, bsc);
       for (int i = tid; i < D; i += TR_THREADS) {
         double x = (dmerged[i] - mean_d) / denom;
         if (sd > 0.0) x = x - (v[i] - mu) * (dot_dc / (D * sd * denom * denom));
