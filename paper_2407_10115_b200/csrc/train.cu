@@ -148,9 +148,9 @@ __device__ double block_sum(double v, double* red, int& ctr) {
   double* slot = red + (++ctr & 1) * TR_WARPS;
   if (lane == 0) slot[warp] = v;
   __syncthreads();
-  double t = 0.0;
-#pragma unroll 8
-  for (int w = 0; w < TR_WARPS; ++w) t += slot[w];
+  double t = lane < TR_WARPS ? slot[lane] : 0.0;  // fixed-order tree fold, every warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   return t;
 }
 
@@ -490,12 +490,20 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         const double* a_in = l == 0 ? merged : act + (hoff - I);
         // upstream gradient from the PRE-update weights (M:473-475): warp per row
         // (split layer: partial over this CTA's columns, reduced across the cluster)
-        for (int r = warp; r < I; r += TR_WARPS) {
-          double s = 0.0;
-          for (int c = lane; c < Ow; c += 32) s += (double)W[(int64_t)r * ld + c] * dcur[cb + c];
+        if (Ow <= 8) {  // narrow (cluster-split) slice: thread per row
+          for (int r = tid; r < I; r += TR_THREADS) {
+            double s = 0.0;
+            for (int c = 0; c < Ow; ++c) s += (double)W[(int64_t)r * ld + c] * dcur[cb + c];
+            (split ? dpart : dnext)[r] = s;
+          }
+        } else {
+          for (int r = warp; r < I; r += TR_WARPS) {
+            double s = 0.0;
+            for (int c = lane; c < Ow; c += 32) s += (double)W[(int64_t)r * ld + c] * dcur[cb + c];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) (split ? dpart : dnext)[r] = s;
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) (split ? dpart : dnext)[r] = s;
+          }
         }
         if (split) {
           cooperative_groups::this_cluster().sync();
@@ -509,14 +517,23 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         __syncthreads();
         // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554):
         // warp per row (dead-ReLU rows skipped warp-uniformly), lanes along c
-        for (int r = warp; r < I; r += TR_WARPS) {
-          const double ar = a_in[r];
-          if (ar == 0.0 && p.sparse) continue;
-          float* wr = W + (int64_t)r * ld;
-          float* war = Wa + (int64_t)r * ld;
-          for (int c = lane; c < Ow; c += 32) {
-            const double gr = __dmul_rn(ar, dcur[cb + c]);
-            if (gr != 0.0 || !p.sparse) adagrad(&wr[c], &war[c], gr, p.lr_nn, pt);
+        if (Ow <= 8) {  // narrow slice: flat (row, column) per thread
+          for (int t = tid; t < I * Ow; t += TR_THREADS) {
+            const int r = t / Ow, c = t - r * Ow;
+            const double gr = __dmul_rn(a_in[r], dcur[cb + c]);
+            if (gr != 0.0 || !p.sparse) adagrad(&W[(int64_t)r * ld + c], &Wa[(int64_t)r * ld + c],
+                                                gr, p.lr_nn, pt);
+          }
+        } else {
+          for (int r = warp; r < I; r += TR_WARPS) {
+            const double ar = a_in[r];
+            if (ar == 0.0 && p.sparse) continue;
+            float* wr = W + (int64_t)r * ld;
+            float* war = Wa + (int64_t)r * ld;
+            for (int c = lane; c < Ow; c += 32) {
+              const double gr = __dmul_rn(ar, dcur[cb + c]);
+              if (gr != 0.0 || !p.sparse) adagrad(&wr[c], &war[c], gr, p.lr_nn, pt);
+            }
           }
         }
         for (int c = tid; c < Ow; c += TR_THREADS) {  // M:557-572
@@ -557,11 +574,14 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
     }
     // d_pairs[p] = g + dv[1+p] (M:484); dp symmetric (M:492-495).
     // t[g][:] = dp[f][g] * S[g][f][:]; fields whose t is all zero are skipped (M:502)
+    // dp[f][g] precomputed per (field, target) into dpm (f64) so the update's
+    // inner loop is division-free; fact[f] = field f's t row is not all zero
     for (int t = tid; t < F * F; t += TR_THREADS) {
       const int f = t / F, gg = t - f * F;
+      double dpv = 0.0;
+      if (gg != f) dpv = g + dv[1 + (gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F))];
+      dpm[t] = dpv;
       if (gg == f || !pres[f]) continue;
-      const int pp = gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F);
-      const double dpv = g + dv[1 + pp];
       const double* sgf = S + (gg * F + f) * k;
       int any = 0;
       for (int c = 0; c < k; ++c) any |= (dpv * sgf[c]) != 0.0;
@@ -569,23 +589,20 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
     }
     __syncthreads();
     // ---------------------------------------------------------- FFM update (M:490-513)
-    // one thread per (leader slot, latent element): merged gradient in occurrence order
-    // warp per unique bucket, lanes along its row; dp[f][g] precomputed per
-    // (field, target) into dpm (f64) to keep the inner loop division-free
-    for (int t = tid; t < F * F; t += TR_THREADS) {
-      const int f = t / F, gg = t - f * F;  // once per example (F*F = 576)
-      double dpv = 0.0;
-      if (gg != f) dpv = g + dv[1 + (gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F))];
-      dpm[t] = dpv;
-    }
-    __syncthreads();
+    // merged gradient per (unique bucket, latent element) in occurrence order
     const int nu = *nuniq;
-    for (int u = rank * TR_WARPS + warp; u < nu; u += C * TR_WARPS) {  // rows split over the cluster
+    // work item = (unique row u, 32-element chunk); items dealt round-robin
+    // to the cluster's CTAs and then to warps, so every SM gets ~1/C of it
+    const int nchunk = (Fk + 31) >> 5;
+    for (int it = rank + C * warp; it < nu * nchunk; it += C * TR_WARPS) {
+      const int u = it / nchunk, ch = it - u * nchunk;
       const int s = ulist[u];
       const int j = sidx[s];
       float* wrow = p.ffm + (int64_t)j * Fk;
       float* arow = p.ffm_acc + (int64_t)j * Fk;
-      for (int gk = lane; gk < Fk; gk += 32) {
+      {
+        const int gk = ch * 32 + lane;
+        if (gk >= Fk) continue;
         const int gg = gkg[gk], c = gk - gg * k;
         double ug = 0.0;
         bool touched = false;
@@ -601,7 +618,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       }
     }
     // ---------------------------------------------------------- LR + bias (M:516-530)
-    if (rank == C - 1) {  // the last CTA has the fewest FFM rows
+    if (rank == C - 1) {  // the last CTA gets the fewest FFM work items
       for (int s = tid; s < FM; s += TR_THREADS) {
         if (lead[s] != s) continue;
         const int j = sidx[s];
