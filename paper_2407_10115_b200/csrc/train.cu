@@ -36,6 +36,20 @@ constexpr int TR_THREADS = DFFM_TR_THREADS;
 constexpr int TR_WARPS = TR_THREADS / 32;
 constexpr int TR_CLUSTER = 8;  // CTAs per cluster for the split trainer
 
+// Phase timestamps (debug builds only, -DDFFM_TR_TRACE): SM clock of thread 0
+// of rank 0 at each phase boundary, for examples [TR_T0, TR_T0 + TR_TN).
+#ifdef DFFM_TR_TRACE
+constexpr int TR_T0 = 16, TR_TN = 64, TR_NPH = 16;
+__device__ long long g_tr_trace[TR_TN * TR_NPH];
+#define TR_MARK(ph)                                                            \
+  do {                                                                         \
+    if (threadIdx.x == 0 && rank == 0 && e >= TR_T0 && e < TR_T0 + TR_TN)      \
+      g_tr_trace[(e - TR_T0) * TR_NPH + (ph)] = clock64();                     \
+  } while (0)
+#else
+#define TR_MARK(ph) do { } while (0)
+#endif
+
 struct TrainParams {
   const int32_t* idx;
   const float* val;
@@ -263,6 +277,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
 
   for (int64_t e = 0; e < p.n; ++e) {
     // ---------------------------------------------------------- stage example
+    TR_MARK(0);
     const int label = p.labels[e];
     if (label > 1) {  // M:453-454 ContractError, before touching anything
       if (tid == 0)
@@ -298,6 +313,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
                   (unsigned long long)status_key(e, DFFM_BLOCK_NONE, DFFM_CONTRACT));
       break;
     }
+    TR_MARK(1);
     for (int f = tid; f < F; f += TR_THREADS) {
       int pr = 0;
       double lp = 0.0;
@@ -332,6 +348,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       nxt[s] = 0x7fffffff;
     }
     __syncthreads();
+    TR_MARK(2);
     // all (s, s2) slot pairs in parallel: lead = smallest equal slot, nxt =
     // smallest equal slot after s
     for (int t = tid; t < FM * FM; t += TR_THREADS) {
@@ -357,6 +374,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       if (lane == 0) *nuniq = cnt;
     }
     __syncthreads();
+    TR_MARK(3);
     // ---------------------------------------------------------- pairs, MergeNorm
     double psum_part = 0.0;
     int ffm_bad = 0;
@@ -395,6 +413,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       merge_bad |= !isfinite(merged[i]);
     }
     merge_bad = __syncthreads_or(merge_bad);
+    TR_MARK(4);
     // ---------------------------------------------------------- MLP forward (f64)
     double nn_out = 0.0;
     int nn_bad = 0;
@@ -446,6 +465,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           }
         }
         __syncthreads();
+        TR_MARK(5 + (l > 0));
         a = act + hoff;
         hoff += O;
       }
@@ -455,6 +475,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       nn_out = block_sum(s, red, bsc) + (double)bl[NL - 1][0];  // M:372-373
       nn_bad = __syncthreads_or(nn_bad);
     }
+    TR_MARK(7);
     const double logit = nn_out + lr_out + psum;  // M:377
     if (!isfinite(logit)) {  // M:392-396 (uniform across the block and the cluster)
       if (tid == 0 && rank == 0) {
@@ -546,6 +567,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
             dnext[r] = pre[hoff + r] > 0.0 ? dnext[r] : 0.0;  // M:479 ReLU mask
         }
         __syncthreads();
+        TR_MARK(l == 0 ? 9 : 8);
         double* tmp = dcur; dcur = dnext; dnext = tmp;
       }
       dmerged = dcur;
@@ -566,6 +588,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         dv[i] = x;
       }
       __syncthreads();
+      TR_MARK(10);
       d_lr = g + dv[0];  // M:483
     } else {
       d_lr = g;
@@ -588,6 +611,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       if (any) atomicOr(&fact[f], 1);
     }
     __syncthreads();
+    TR_MARK(11);
     // ---------------------------------------------------------- FFM update (M:490-513)
     // merged gradient per (unique bucket, latent element) in occurrence order
     const int nu = *nuniq;
@@ -617,6 +641,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           adagrad_g(&wrow[gk], &arow[gk], ug, p.lr_ffm, pt);  // M:509-513
       }
     }
+    TR_MARK(12);
     // ---------------------------------------------------------- LR + bias (M:516-530)
     if (rank == C - 1) {  // the last CTA gets the fewest FFM work items
       for (int s = tid; s < FM; s += TR_THREADS) {
@@ -630,8 +655,10 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
     }
     // every table write of this example is visible cluster-wide before the
     // next example reads (release/acquire at cluster scope; table reads are L2-only)
+    TR_MARK(13);
     if (C > 1) cooperative_groups::this_cluster().sync();
     else __syncthreads();
+    TR_MARK(14);
   }
 
   // ---- write the MLP working copies back (also after an error: the reference
@@ -708,6 +735,12 @@ static int tr_validate(const dffm_model* m, int32_t M, int C, TrainParams& p, in
   *smem_out = L.total;
   return DFFM_OK;
 }
+
+#ifdef DFFM_TR_TRACE
+extern "C" int dffm_tr_trace_read(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_tr_trace, sizeof(g_tr_trace));
+}
+#endif
 
 extern "C" int64_t dffm_train_scratch_bytes(const dffm_model*, int32_t) { return 0; }
 

@@ -1,0 +1,26 @@
+"""Per-phase K2 latency breakdown from a -DDFFM_TR_TRACE build
+(tools/libdffm_trace.so): SM cycles between phase boundaries of thread 0,
+averaged over 64 examples of a cfg3-shaped stream."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+os.environ.setdefault("DFFM_LIB_PATH", "tools/libdffm_trace.so")
+sys.argv = [sys.argv[0], "400"] + sys.argv[1:]
+sys.path.insert(0, ".")
+exec(open("tools/train_profile.py").read())  # runs 200 warm-up + 400 examples
+from paper_2407_10115_b200 import _lib  # noqa: E402
+
+h = _lib.lib()
+buf = (ctypes.c_longlong * (64 * 16))()
+h.dffm_tr_trace_read(buf)
+t = np.array(buf, dtype=np.int64).reshape(64, 16)
+names = ["start", "staged", "S+lr loaded", "dup lists", "pairs+norm", "mlp l0 fwd", "mlp l1 fwd",
+         "mlp out", "bwd l>0", "bwd l0", "norm bwd", "dp/fact", "ffm upd", "lr upd", "cl.sync"]
+per = np.median(np.diff(t[:, :15], axis=1), axis=0)
+tot = np.median(t[1:, 0] - t[:-1, 0])
+for i, d in enumerate(per):
+    print(f"{names[i]:>12s} -> {names[i+1]:<12s} {d:8.0f} cyc")
+print(f"example period {tot:.0f} cycles")
