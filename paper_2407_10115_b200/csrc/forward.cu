@@ -11,6 +11,7 @@
 #include "forward_ws.cuh"
 #include "forward_rows.cuh"
 #include "forward_g4.cuh"
+#include "mlp_tc.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -34,16 +35,19 @@ template <typename T>
 int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int smem,
                         cudaStream_t s);
 
-enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3, FAM_G4 = 4 };
+enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3, FAM_G4 = 4, FAM_TC = 5 };
 static int g_family = -1;  // set by env (first call) or dffm_set_forward_family()
+static bool g_family_explicit = false;
 static int forward_family() {
   if (g_family < 0) {
     const char* v = getenv("DFFM_FORWARD_KERNEL");
     int f = FAM_WS;  // measured fastest on cfg2 (see profiles/)
+    g_family_explicit = v != nullptr;
     if (v && strcmp(v, "rows") == 0) f = FAM_ROWS;
     if (v && strcmp(v, "g4") == 0) f = FAM_G4;
     if (v && strcmp(v, "v1") == 0) f = FAM_V1;
     if (v && strcmp(v, "tma") == 0) f = FAM_TMA;
+    if (v && strcmp(v, "tc") == 0) f = FAM_TC;
     g_family = f;
   }
   return g_family;
@@ -239,6 +243,156 @@ static bool try_tma_forward(const dffm_model* m, FwdParams& p, int smax, cudaStr
   return false;
 }
 
+// ---- K1 v6: gather (ws family, staging mode) + tcgen05 MLP (mlp_tc.cu), per slice.
+// Chosen explicitly (family 5 / DFFM_FORWARD_KERNEL=tc) or, by default, when
+// the MLP is heavy enough that CUDA-core FMAs would bound the fused kernel.
+static bool tc_auto(const FwdParams& p) {
+  int64_t macs = 0;
+  for (int l = 0; l < p.n_layers; ++l) macs += (int64_t)p.dims[l] * p.dims[l + 1];
+  return macs >= 65536;  // cfg5 (781-256-128-1): 232,832; cfg2 (277-64-32-1): 19,808
+}
+
+// device workspace per (device, stream), grow-only: staged rows of one slice
+// and the blocked hi/lo MLP weights
+static int tc_workspace(cudaStream_t s, size_t bytes, unsigned char** out) {
+  struct Ws { void* ptr = nullptr; size_t bytes = 0; };
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, Ws> ws;
+  int dev = 0;
+  DFFM_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+  const uint64_t key = (uint64_t)(uintptr_t)s ^ ((uint64_t)dev << 56);
+  std::lock_guard<std::mutex> lk(mu);
+  Ws& w = ws[key];
+  if (w.bytes < bytes) {
+    if (w.ptr) DFFM_CUDA_TRY(cudaFree(w.ptr), "cudaFree(tc workspace)");
+    w.ptr = nullptr;
+    w.bytes = 0;
+    DFFM_CUDA_TRY(cudaMalloc(&w.ptr, bytes), "cudaMalloc(tc workspace)");
+    w.bytes = bytes;
+  }
+  *out = (unsigned char*)w.ptr;
+  return DFFM_OK;
+}
+
+static int rows_tensor_map_x(const float* X, int Kp, int64_t rows, CUtensorMap* tm) {
+  auto fn = encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return DFFM_CUDA; }
+  cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)Kp * 4};
+  cuuint32_t box[2] = {(cuuint32_t)TC_KC, (cuuint32_t)TC_M};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(staged rows) failed (%d)", (int)r);
+    return DFFM_CUDA;
+  }
+  return DFFM_OK;
+}
+
+static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
+                           int* rc) {
+  const int fam = forward_family();
+  if (fam != FAM_TC && !(fam == FAM_WS && !g_family_explicit && tc_auto(p))) return false;
+  const int NH = p.n_layers - 1;
+  if (NH < 1 || NH > TC_MAXH) return false;
+  int nmax = 0;
+  for (int l = 1; l <= NH; ++l) {
+    const int w = p.dims[l];
+    if (w < 16 || w > 256 || w % 16) return false;
+    nmax = std::max(nmax, w);
+  }
+  FwdParams pg = p;
+  int smem_g = 0;
+  for (int TE = 32; TE >= 8 && !smem_g; TE >>= 1) {
+    pg.TE = TE;
+    pg.XS = TE + 4;
+    const WsSmem L = ws_smem_layout(p.F, p.M, p.P, p.D, pg.TE, pg.XS, p.hmax);
+    if (L.total <= smax) smem_g = L.total;
+  }
+  if (!smem_g) return false;
+  MlpTcParams q{};
+  q.n_hidden = NH;
+  const int Kp = (p.D + 15) & ~15;
+  size_t wfloats = 0;
+  for (int l = 0; l < NH; ++l) {
+    q.kin[l] = l == 0 ? Kp : p.dims[l];
+    q.nout[l] = p.dims[l + 1];
+    wfloats += (size_t)q.kin[l] * q.nout[l] * 2;
+  }
+  q.stage_bytes = tc_stage_bytes(nmax);
+  q.stages = std::min(TC_MAX_STAGES, (smax - 1024 - 512) / q.stage_bytes);
+  if (q.stages < 2) return false;
+  int cols = 32;
+  while (cols < 2 * nmax) cols <<= 1;
+  q.tmem_cols = cols;
+  const int smem_tc = 1024 + q.stages * q.stage_bytes + (3 * q.stages + 2) * 8 + 16;
+  static int64_t slice_env = -1;
+  if (slice_env < 0) {
+    const char* v = getenv("DFFM_TC_SLICE");
+    slice_env = v ? atoll(v) : (int64_t)148 * TC_M;
+    slice_env = std::max<int64_t>(TC_M, slice_env / TC_M * TC_M);
+  }
+  const int64_t sl = std::min<int64_t>(slice_env, (p.n + TC_M - 1) / TC_M * TC_M);
+  auto a256 = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t b_w = a256(wfloats * 4), b_x = a256((size_t)sl * Kp * 4),
+               b_r = a256((size_t)sl * 8), b_f = a256((size_t)sl * 4);
+  unsigned char* ws = nullptr;
+  if ((*rc = tc_workspace(s, b_w + b_x + b_r + b_f, &ws))) return true;
+  float* wblk = (float*)ws;
+  float* X = (float*)(ws + b_w);
+  double* R = (double*)(ws + b_w + b_x);
+  int* Fl = (int*)(ws + b_w + b_x + b_r);
+  {
+    float* wl = wblk;
+    for (int l = 0; l < NH; ++l) {
+      const int kreal = l == 0 ? p.D : p.dims[l];
+      if ((*rc = launch_tc_prep_weights(p.W[l], kreal, q.nout[l], q.kin[l], wl, s))) return true;
+      q.wblk[l] = wl;
+      q.bias[l] = p.b[l];
+      wl += (size_t)q.kin[l] * q.nout[l] * 2;
+    }
+  }
+  q.w_out = p.W[NH];
+  q.b_out = p.b[NH];
+  q.resid = R;
+  q.flags = Fl;
+  q.status = p.status;
+  const int K = pick_k_template(p.k, m->wdtype);
+  const int MU = p.M <= 4 ? p.M : 0;
+  const int64_t FM = (int64_t)p.F * p.M;
+  for (int64_t s0 = 0; s0 < p.n; s0 += sl) {
+    const int64_t ns = std::min<int64_t>(sl, p.n - s0);
+    FwdParams a = pg;
+    a.idx = p.idx + s0 * FM;
+    a.val = p.val + s0 * FM;
+    a.n = ns;
+    a.status_base = p.status_base + s0;
+    a.prob = p.prob + s0;
+    a.logit = nullptr;
+    a.xout = X;
+    a.rout = R;
+    a.fout = Fl;
+    a.Kp = Kp;
+    switch (m->wdtype) {
+      case DFFM_W_F32: *rc = launch_forward_ws_t<float>(a, K, MU, smem_g, s); break;
+      case DFFM_W_BF16: *rc = launch_forward_ws_t<__nv_bfloat16>(a, K, MU, smem_g, s); break;
+      default: *rc = launch_forward_ws_t<uint16_t>(a, K, MU, smem_g, s); break;
+    }
+    if (*rc) return true;
+    CUtensorMap tm;
+    if ((*rc = rows_tensor_map_x(X, Kp, ns, &tm))) return true;
+    q.rows = ns;
+    q.status_base = p.status_base + s0;
+    q.prob = p.prob + s0;
+    q.logit = p.logit ? p.logit + s0 : nullptr;
+    if ((*rc = launch_mlp_tc(tm, q, smem_tc, s))) return true;
+  }
+  *rc = DFFM_OK;
+  return true;
+}
+
 // shared with ctx.cu: fills FwdParams' model part, validates
 int fill_model_params(const dffm_model* m, FwdParams& p) {
   if (!m) { set_error("null model"); return DFFM_CONTRACT; }
@@ -310,8 +464,9 @@ int pick_k_template(int k, int wdtype) {
 using namespace dffm;
 
 extern "C" int dffm_set_forward_family(int32_t family) {
-  if (family < -1 || family > FAM_G4) { set_error("bad forward family %d", family); return DFFM_CONTRACT; }
+  if (family < -1 || family > FAM_TC) { set_error("bad forward family %d", family); return DFFM_CONTRACT; }
   g_family = family;  // -1: re-read DFFM_FORWARD_KERNEL on the next call
+  g_family_explicit = family >= 0;
   return DFFM_OK;
 }
 
@@ -336,6 +491,7 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   p.status_base = status_base;
   p.M = max_per_field;
   const int smax = max_smem_optin_current();
+  if (try_tc_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_g4_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_rows_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
   if (try_ws_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;

@@ -51,6 +51,14 @@ struct FwdParams {
   const void* lr;
   const void* ffm;
   Deq dlr, dffm;
+  // staging mode (tensor-core MLP, mlp_tc.cu): when xout is set the MLP warps
+  // do not run the MLP; they write each example's MergeNorm row to
+  // xout[e][0..Kp) (zero padded), lr_out + sum(pairs) to rout[e] and the
+  // non-finite stage bits to fout[e]
+  float* xout;
+  double* rout;
+  int* fout;
+  int Kp;
 };
 
 struct FwdSmem {

@@ -59,6 +59,20 @@ __device__ __forceinline__ void mlp_warps_tile(const FwdParams& p, const float* 
                                                float* Hb, int64_t base, int mt) {
   const int TE = p.TE, XS = p.XS;
   const int lane = mt & 31, mw = mt >> 5;
+  if (p.xout) {  // staging mode: rows for the tensor-core MLP (mlp_tc.cu)
+    for (int el = mw; el < TE; el += NM) {
+      const int64_t e = base + el;
+      if (e >= p.n) continue;
+      float* row = p.xout + e * p.Kp;
+      for (int i = lane; i < p.Kp; i += 32) row[i] = i < p.D ? xin[i * XS + el] : 0.f;
+      if (lane == 0) {
+        p.rout[e] = exd[el] + exd[TE + el];
+        p.fout[e] = flag[el];
+      }
+    }
+    __syncwarp();
+    return;
+  }
   int I = p.D;
   float* outb = Ha;
   for (int l = 0; l + 1 < p.n_layers; ++l) {

@@ -1,0 +1,44 @@
+// K1 MLP stage on the 5th-generation tensor cores (tcgen05, kind::tf32, 3xTF32).
+// Shared between mlp_tc.cu (kernels) and forward.cu (slicing / dispatch).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace dffm {
+
+constexpr int TC_M = 128;       // examples per tile = UMMA M (one TMEM lane per example)
+constexpr int TC_KC = 16;       // K elements per pipeline stage (64 B per row)
+constexpr int TC_MAXH = 4;      // hidden layers (M:70-71)
+constexpr int TC_THREADS = 192; // warp 0 TMA, warp 1 MMA, warps 2-5 convert + epilogue
+constexpr int TC_MAX_STAGES = 8;
+
+struct MlpTcParams {
+  const double* resid;  // [rows] lr_out + sum(pairs)            (M:377 residual)
+  const int* flags;     // [rows] non-finite stage bits 1 lr, 2 ffm, 4 merge
+  float* prob;          // [rows]
+  float* logit;         // [rows] or null
+  uint64_t* status;
+  int64_t rows;
+  int64_t status_base;
+  int n_hidden;
+  int kin[TC_MAXH];     // layer l input width, padded to a multiple of 16
+  int nout[TC_MAXH];    // layer l output width (multiple of 16, <= 256)
+  const float* wblk[TC_MAXH];  // per layer, kin/16 chunks of [hi N x 16][lo N x 16] (core-matrix blocked)
+  const float* bias[TC_MAXH];
+  const float* w_out;   // [nout[n_hidden-1]] output layer column (M:372)
+  const float* b_out;   // [1]
+  int stages;
+  int stage_bytes;      // 16 KB (A hi + lo) + nmax * 128 B (W hi + lo), 1 KB aligned
+  int tmem_cols;        // power of two >= 2 * nmax: two accumulator regions
+};
+
+__host__ __device__ inline int tc_stage_bytes(int nmax) {
+  return (16384 + nmax * 128 + 1023) & ~1023;
+}
+
+int launch_mlp_tc(const CUtensorMap& tmx, const MlpTcParams& p, int smem, cudaStream_t s);
+int launch_tc_prep_weights(const float* W, int K, int N, int Kp, float* dst, cudaStream_t s);
+
+}  // namespace dffm

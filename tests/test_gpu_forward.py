@@ -73,12 +73,12 @@ def test_forward_matches_oracle(F, k, hidden, M, bits, n):
     assert rel_err(p, ref).max() < RTOL
 
 
-@pytest.mark.parametrize("family", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("family", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("wdtype", ["f32", "bf16", "u16"])
 def test_every_forward_family_matches_oracle(family, wdtype):
-    """All five K1 kernel families (row-coalesced, warp-specialised,
-    CTA-synchronous, TMA-ring, TMA-gather4) on cfg2-shaped inputs and every
-    table storage type."""
+    """All six K1 kernel families (row-coalesced, warp-specialised,
+    CTA-synchronous, TMA-ring, TMA-gather4, gather + tcgen05 3xTF32 MLP) on
+    cfg2-shaped inputs and every table storage type."""
     from paper_2407_10115_b200 import _lib
     from paper_2407_10115_b200.quant import quantize_store
     wl = configs.CFG2
@@ -97,6 +97,54 @@ def test_every_forward_family_matches_oracle(family, wdtype):
     cst, ridx, _ = compact_oracle(st, idx.numpy())
     _, ref = fo.forward_batch(ridx, val.numpy(), cst)
     assert rel_err(p, ref).max() < RTOL
+
+
+@pytest.mark.parametrize("family", [-1, 5, 1])
+@pytest.mark.parametrize("n", [1, 127, 300])
+def test_forward_cfg5_shape_tensor_core_mlp(family, n):
+    """cfg5 shape (F=40, k=16, bf16 tables, MLP 781-256-128-1): the default
+    dispatch picks the tcgen05 MLP; ragged tails (n % 128 != 0) included."""
+    from paper_2407_10115_b200 import _lib
+    wl = configs.CFG5
+    ost = fo.random_store(40, 16, (256, 128), 12, seed=5, scale=0.05)
+    idx, val = synth.make_examples(wl, n, seed=11, hash_bits=12)
+    st = WeightStore.from_flat(ModelConfig(n_fields=40, k=16, hidden_sizes=(256, 128),
+                                           hash_bits=12), ost.flat(False), DEV, "bf16", False)
+    _lib.check(_lib.lib().dffm_set_forward_family(family))
+    try:
+        lg = torch.empty(n, device=DEV)
+        p = predict_batch(idx, val, st, logits=lg).double().cpu().numpy()
+    finally:
+        _lib.lib().dffm_set_forward_family(-1)
+    cst, ridx, _ = compact_oracle(st, idx.numpy())
+    lref, ref = fo.forward_batch(ridx, val.numpy(), cst)
+    assert rel_err(p, ref).max() < RTOL
+    np.testing.assert_allclose(lg.double().cpu().numpy(), lref, rtol=1e-5, atol=1e-5)
+
+
+def test_forward_tc_slices_and_nonfinite_nn():
+    """Several staging slices (DFFM_TC_SLICE is 148*128 rows by default) and
+    a non-finite hidden unit reported as block "nn" at the first example."""
+    from paper_2407_10115_b200 import _lib
+    ost = fo.random_store(8, 4, (32, 16), 10, seed=3)
+    n = 148 * 128 * 2 + 77
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, 1 << 10, size=(n, 8, 1)).astype(np.int32)
+    val = np.ones_like(idx, dtype=np.float32)
+    st = store_from_oracle(ost)
+    _lib.check(_lib.lib().dffm_set_forward_family(5))
+    try:
+        p = predict_batch(idx, val, st).double().cpu().numpy()
+        sel = np.r_[0:64, n - 200:n]
+        _, ref = fo.forward_batch(idx[sel], val[sel], ost)
+        assert rel_err(p[sel], ref).max() < RTOL
+        o = ost.copy()
+        o.layers[1][0][:, 5] = np.inf
+        with pytest.raises(NumericError) as ei:
+            predict_batch(idx, val, store_from_oracle(o))
+        assert ei.value.example == 0 and ei.value.block == "nn"
+    finally:
+        _lib.lib().dffm_set_forward_family(-1)
 
 
 def test_forward_bf16_and_u16_tables_match_widened_oracle():
