@@ -12,6 +12,7 @@
 #include "forward_rows.cuh"
 #include "forward_g4.cuh"
 #include "mlp_tc.cuh"
+#include "forward_rowstage.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -34,6 +35,8 @@ int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s);
 template <typename T>
 int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int smem,
                         cudaStream_t s);
+template <typename T>
+int launch_forward_rowstage_t(const FwdParams& p, int K, int NB, int smem, cudaStream_t s);
 
 enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3, FAM_G4 = 4, FAM_TC = 5 };
 static int g_family = -1;  // set by env (first call) or dffm_set_forward_family()
@@ -106,8 +109,9 @@ static int row_tensor_map(const void* base, int wdtype, int64_t rows, int row_el
 }
 
 // K1 v5: TMA gather4 ring (whole rows per TMA op)
-static bool try_g4_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc) {
-  if (forward_family() != FAM_G4) return false;
+static bool try_g4_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc,
+                           bool force = false) {
+  if (!force && forward_family() != FAM_G4) return false;
   const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
   const int k = p.k;
   const int row_elems = p.F * k;
@@ -154,8 +158,8 @@ static bool try_g4_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
 
 // K1 v4: row-coalesced gather (F <= 32, 16/32/64-byte segments)
 static bool try_rows_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
-                             int* rc) {
-  if (forward_family() != FAM_ROWS) return false;
+                             int* rc, bool force = false) {
+  if (!force && forward_family() != FAM_ROWS) return false;
   const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
   const int k = p.k;
   if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
@@ -183,11 +187,13 @@ static bool try_rows_forward(const dffm_model* m, FwdParams& p, int smax, cudaSt
   return false;
 }
 
-static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc) {
-  if (forward_family() != FAM_WS && forward_family() != FAM_ROWS) return false;  // rows falls back here
+static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc,
+                           bool force = false) {
+  if (!force && forward_family() != FAM_WS && forward_family() != FAM_ROWS)
+    return false;  // rows falls back here
   for (int l = 1; l < p.n_layers; ++l)
     if (p.dims[l] % 4) return false;
-  for (int TE = 32; TE >= 8; TE >>= 1) {
+  for (int TE = p.xout ? 8 : 32; TE >= 8; TE >>= 1) {  // staging: small tile, big ring
     p.TE = TE;
     p.XS = TE + 4;
     const WsSmem L = ws_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax);
@@ -207,8 +213,8 @@ static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
 // Pick K1 v2 (TMA ring) when the shape allows it; returns false to fall
 // through to fwd_kernel.
 static bool try_tma_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
-                            int* rc) {
-  if (!tma_forward_enabled()) return false;
+                            int* rc, bool force = false) {
+  if (!force && !tma_forward_enabled()) return false;
   const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
   const int k = p.k;
   if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
@@ -223,7 +229,7 @@ static bool try_tma_forward(const dffm_model* m, FwdParams& p, int smax, cudaStr
   }
   q.row_bytes = p.F * k * esz;
   q.rs = q.row_bytes + 16;
-  for (int TE = 32; TE >= 8; TE >>= 1) {
+  for (int TE = p.xout ? 8 : 32; TE >= 8; TE >>= 1) {  // staging: small tile, big ring
     p.TE = TE;
     p.XS = TE + 4;
     const TmaSmem L0 = tma_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.rs, 0);
@@ -291,6 +297,33 @@ static int rows_tensor_map_x(const float* X, int Kp, int64_t rows, CUtensorMap* 
   return DFFM_OK;
 }
 
+// K1 v7 staging gather for single-slot fields (whole rows via cp.async ring)
+static bool try_rowstage_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
+                                 int* rc) {
+  if (!p.xout || p.M != 1 || p.F > RS_MAXF) return false;
+  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
+  const int k = p.k;
+  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
+  if (((uintptr_t)p.ffm & 15) || ((uintptr_t)p.lr & 3)) return false;
+  const int row_bytes = p.F * k * esz;
+  static int ctas = -1;  // CTAs per SM to aim for (each overlaps its own example chain)
+  if (ctas < 0) {
+    const char* v = getenv("DFFM_RS_CTAS");
+    ctas = v ? std::max(1, atoi(v)) : 2;
+  }
+  for (int nb = 4; nb >= 2; --nb) {
+    const RsSmem L = rs_smem_layout(p.F, p.P, row_bytes, nb);
+    if (L.total > smax || (nb > 2 && ctas * (L.total + 1024) > 228 * 1024)) continue;
+    switch (m->wdtype) {
+      case DFFM_W_F32: *rc = launch_forward_rowstage_t<float>(p, k, nb, L.total, s); break;
+      case DFFM_W_BF16: *rc = launch_forward_rowstage_t<__nv_bfloat16>(p, k, nb, L.total, s); break;
+      default: *rc = launch_forward_rowstage_t<uint16_t>(p, k, nb, L.total, s); break;
+    }
+    return true;
+  }
+  return false;
+}
+
 static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
                            int* rc) {
   const int fam = forward_family();
@@ -304,14 +337,18 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     nmax = std::max(nmax, w);
   }
   FwdParams pg = p;
-  int smem_g = 0;
-  for (int TE = 32; TE >= 8 && !smem_g; TE >>= 1) {
-    pg.TE = TE;
-    pg.XS = TE + 4;
-    const WsSmem L = ws_smem_layout(p.F, p.M, p.P, p.D, pg.TE, pg.XS, p.hmax);
-    if (L.total <= smax) smem_g = L.total;
+  pg.hmax = 0;  // staging mode: the gather kernels keep no hidden-layer buffers
+  {
+    const WsSmem L = ws_smem_layout(p.F, p.M, p.P, p.D, 8, 12, 0);
+    if (L.total > smax) return false;  // the ws gather (the fallback) must fit
   }
-  if (!smem_g) return false;
+  static int gather_env = -1;
+  if (gather_env < 0) {
+    const char* v = getenv("DFFM_TC_GATHER");
+    gather_env = (v && strcmp(v, "g4") == 0) ? FAM_G4 : (v && strcmp(v, "rows") == 0) ? FAM_ROWS
+                 : (v && strcmp(v, "tma") == 0) ? FAM_TMA : (v && strcmp(v, "ws") == 0) ? FAM_WS
+                 : -1;  // default: row staging when it applies, else ws
+  }
   MlpTcParams q{};
   q.n_hidden = NH;
   const int Kp = (p.D + 15) & ~15;
@@ -359,8 +396,6 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
   q.resid = R;
   q.flags = Fl;
   q.status = p.status;
-  const int K = pick_k_template(p.k, m->wdtype);
-  const int MU = p.M <= 4 ? p.M : 0;
   const int64_t FM = (int64_t)p.F * p.M;
   for (int64_t s0 = 0; s0 < p.n; s0 += sl) {
     const int64_t ns = std::min<int64_t>(sl, p.n - s0);
@@ -375,11 +410,13 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     a.rout = R;
     a.fout = Fl;
     a.Kp = Kp;
-    switch (m->wdtype) {
-      case DFFM_W_F32: *rc = launch_forward_ws_t<float>(a, K, MU, smem_g, s); break;
-      case DFFM_W_BF16: *rc = launch_forward_ws_t<__nv_bfloat16>(a, K, MU, smem_g, s); break;
-      default: *rc = launch_forward_ws_t<uint16_t>(a, K, MU, smem_g, s); break;
-    }
+    bool launched = false;
+    if (gather_env < 0) launched = try_rowstage_forward(m, a, smax, s, rc);
+    if (gather_env == FAM_G4) launched = try_g4_forward(m, a, smax, s, rc, true);
+    else if (gather_env == FAM_ROWS) launched = try_rows_forward(m, a, smax, s, rc, true);
+    else if (gather_env == FAM_TMA) launched = try_tma_forward(m, a, smax, s, rc, true);
+    if (!launched) launched = try_ws_forward(m, a, smax, s, rc, true);
+    if (!launched) { set_error("no gather kernel fits the staging slice"); *rc = DFFM_SIZING; }
     if (*rc) return true;
     CUtensorMap tm;
     if ((*rc = rows_tensor_map_x(X, Kp, ns, &tm))) return true;

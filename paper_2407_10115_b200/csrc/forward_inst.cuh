@@ -10,6 +10,7 @@
 #include "forward_ws.cuh"
 #include "forward_rows.cuh"
 #include "forward_g4.cuh"
+#include "forward_rowstage.cuh"
 
 namespace dffm {
 
@@ -181,5 +182,36 @@ int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int sme
 
 template int launch_forward_g4_t<DFFM_INST_T>(const CUtensorMap&, const G4Params&, int, int,
                                               cudaStream_t);
+
+// ---------------------------------------------------------------- K1 v7 (row staging, M == 1)
+template <typename T>
+static FwdKernel select_rowstage(int K, int NB) {
+#define DFFM_SEL(KK)                                          \
+  if (K == KK) {                                              \
+    if (NB == 2) return fwd_rowstage_kernel<KK, T, 2>;        \
+    if (NB == 3) return fwd_rowstage_kernel<KK, T, 3>;        \
+    if (NB == 4) return fwd_rowstage_kernel<KK, T, 4>;        \
+  }
+  if constexpr (sizeof(T) == 4) { DFFM_SEL(4) }
+  DFFM_SEL(8)
+  DFFM_SEL(16)
+#undef DFFM_SEL
+  return nullptr;
+}
+
+template <typename T>
+int launch_forward_rowstage_t(const FwdParams& p, int K, int NB, int smem, cudaStream_t s) {
+  FwdKernel kern = select_rowstage<T>(K, NB);
+  if (!kern) { set_error("no row-staging kernel for k=%d", K); return DFFM_SIZING; }
+  int occ = 0;
+  int rc = kernel_occupancy((const void*)kern, RS_THREADS, smem, &occ);
+  if (rc) return rc;
+  const int64_t grid = std::min<int64_t>(p.n, (int64_t)sm_count_current() * occ);
+  kern<<<(unsigned)grid, RS_THREADS, smem, s>>>(p);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rowstage)");
+  return DFFM_OK;
+}
+
+template int launch_forward_rowstage_t<DFFM_INST_T>(const FwdParams&, int, int, int, cudaStream_t);
 
 }  // namespace dffm

@@ -183,6 +183,45 @@ __device__ __forceinline__ float pair_dot_batched(const FwdParams& p, const int*
   return pv;
 }
 
+// Two pairs per lane with all four segment loads in flight before any math
+// (single-slot fields: cfg1/4/5): doubles the gather's memory-level
+// parallelism where each pair is only 2 x 32 B.  Pair b is skipped (returns 0)
+// when !act_b; pair a likewise.
+template <int K, typename T>
+__device__ __forceinline__ float2 pair_dot_x2(const FwdParams& p, const int* sidx,
+                                              const float* sval, bool act_a, int fa1, int fa2,
+                                              bool act_b, int fb1, int fb2) {
+  constexpr int SEGB = K * (int)sizeof(T);
+  constexpr int NU = SEGB / 16;
+  constexpr int PER = 16 / (int)sizeof(T);
+  const T* ffm = (const T*)p.ffm;
+  const int ja1 = act_a ? sidx[fa1] : -1, ja2 = act_a ? sidx[fa2] : -1;
+  const int jb1 = act_b ? sidx[fb1] : -1, jb2 = act_b ? sidx[fb2] : -1;
+  uint4 r[4][NU];
+  ldg_chunks_pred<NU>(ffm + ((int64_t)(ja1 > 0 ? ja1 : 0) * p.F + fa2) * K, ja1 >= 0, r[0]);
+  ldg_chunks_pred<NU>(ffm + ((int64_t)(ja2 > 0 ? ja2 : 0) * p.F + fa1) * K, ja2 >= 0, r[1]);
+  ldg_chunks_pred<NU>(ffm + ((int64_t)(jb1 > 0 ? jb1 : 0) * p.F + fb2) * K, jb1 >= 0, r[2]);
+  ldg_chunks_pred<NU>(ffm + ((int64_t)(jb2 > 0 ? jb2 : 0) * p.F + fb1) * K, jb2 >= 0, r[3]);
+  const float x[4] = {ja1 >= 0 ? sval[fa1] : 0.f, ja2 >= 0 ? sval[fa2] : 0.f,
+                      jb1 >= 0 ? sval[fb1] : 0.f, jb2 >= 0 ? sval[fb2] : 0.f};
+  float out[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    float sa[K], sb[K];
+#pragma unroll
+    for (int c = 0; c < NU; ++c) {
+      unpack16<T>(r[2 * q][c], sa + c * PER, p.dffm);
+      unpack16<T>(r[2 * q + 1][c], sb + c * PER, p.dffm);
+    }
+    float pv = 0.f;
+#pragma unroll
+    for (int c = 0; c < K; ++c)
+      pv = fmaf(x[2 * q] * sa[c], x[2 * q + 1] * sb[c], pv);
+    out[q] = pv;
+  }
+  return make_float2(out[0], out[1]);
+}
+
 // MergeNorm tail for one example held by one warp (M:355-360).  The raw pair
 // values are already in column `el` of X (rows 1..P); lane-partial sums of
 // the pairs in `s1`.  Writes the standardised vector back in place, row 0 =
@@ -422,6 +461,103 @@ fwd_kernel(FwdParams p) {
     const int nvalid = (p.n - base) < TE ? (int)(p.n - base) : TE;
     mlp_tile(p, X, Ha, Hb, exd, flag, base, nvalid);
   }
+}
+
+// MLP over one X tile by NM warps (thread index mt in [0, 32*NM)); named
+// barrier 1 synchronises the MLP warps between layers.
+template <int NM>
+__device__ __forceinline__ void mlp_warps_tile(const FwdParams& p, const float* xin,
+                                               const double* exd, int* flag, float* Ha,
+                                               float* Hb, int64_t base, int mt) {
+  const int TE = p.TE, XS = p.XS;
+  const int lane = mt & 31, mw = mt >> 5;
+  if (p.xout) {  // staging mode: rows for the tensor-core MLP (mlp_tc.cu)
+    for (int el = mw; el < TE; el += NM) {
+      const int64_t e = base + el;
+      if (e >= p.n) continue;
+      float* row = p.xout + e * p.Kp;
+      for (int i = lane; i < p.Kp; i += 32) row[i] = i < p.D ? xin[i * XS + el] : 0.f;
+      if (lane == 0) {
+        p.rout[e] = exd[el] + exd[TE + el];
+        p.fout[e] = flag[el];
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  int I = p.D;
+  float* outb = Ha;
+  for (int l = 0; l + 1 < p.n_layers; ++l) {
+    const int O = p.dims[l + 1];
+    const float* __restrict__ W = p.W[l];
+    const float* __restrict__ bl = p.b[l];
+    const int O4 = O >> 2;
+    const int units = O4 * (TE >> 2);
+    for (int u = mt; u < units; u += 32 * NM) {
+      const int o0 = (u % O4) * 4, e0 = (u / O4) * 4;
+      const float4 bv = __ldg((const float4*)(bl + o0));
+      float acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        acc[r][0] = bv.x; acc[r][1] = bv.y; acc[r][2] = bv.z; acc[r][3] = bv.w;
+      }
+#pragma unroll 8
+      for (int i = 0; i < I; ++i) {
+        const float4 x = *(const float4*)(xin + i * XS + e0);
+        const float4 w = __ldg((const float4*)(W + (int64_t)i * O + o0));
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          acc[r][0] = fmaf(xs[r], w.x, acc[r][0]);
+          acc[r][1] = fmaf(xs[r], w.y, acc[r][1]);
+          acc[r][2] = fmaf(xs[r], w.z, acc[r][2]);
+          acc[r][3] = fmaf(xs[r], w.w, acc[r][3]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float4 o;
+        o.x = relu_nan(acc[0][c]);  // M:370
+        o.y = relu_nan(acc[1][c]);
+        o.z = relu_nan(acc[2][c]);
+        o.w = relu_nan(acc[3][c]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (!isfinite(acc[r][c])) atomicOr(&flag[e0 + r], 8);
+        *(float4*)(outb + (o0 + c) * XS + e0) = o;
+      }
+    }
+    named_bar_sync(1, 32 * NM);
+    xin = outb;
+    I = O;
+    outb = (outb == Ha) ? Hb : Ha;
+  }
+  for (int el = mw; el < TE; el += NM) {
+    const int64_t e = base + el;
+    if (e >= p.n) continue;
+    double nn = 0.0;
+    if (p.n_layers > 0) {
+      const float* __restrict__ Wo = p.W[p.n_layers - 1];
+      float sacc = 0.f;
+      for (int i = lane; i < I; i += 32) sacc = fmaf(xin[i * XS + el], __ldg(Wo + i), sacc);
+      sacc = warp_sumf(sacc);
+      nn = (double)sacc + (double)__ldg(p.b[p.n_layers - 1]);  // M:372-373
+    }
+    if (lane == 0) {
+      const double logit = nn + exd[el] + exd[TE + el];  // M:377
+      p.prob[e] = (float)sigmoid_clamped(logit);
+      if (p.logit) p.logit[e] = (float)logit;
+      if (!isfinite(logit)) {
+        const int fl = flag[el];
+        const int blk = (fl & 1) ? DFFM_BLOCK_LR : (fl & 2) ? DFFM_BLOCK_FFM
+                      : (fl & 4) ? DFFM_BLOCK_MERGE : (fl & 8) ? DFFM_BLOCK_NN
+                      : DFFM_BLOCK_LOGIT;
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(p.status_base + e, blk, DFFM_NUMERIC));
+      }
+    }
+  }
+  named_bar_sync(1, 32 * NM);  // Ha/Hb and this X buffer are free again
 }
 
 }  // namespace dffm

@@ -355,88 +355,13 @@ fwd_tma_kernel(TmaParams q) {
   } else {
     // ======================================================== MLP warps
     const int mt = threadIdx.x - (1 + TMA_NC) * 32;  // 0 .. 32*NM-1
-    const int mw = mt >> 5;
     for (int64_t ti = 0; ti < my_tiles; ++ti) {
       const int b = (int)(ti & 1);
       mbar_wait(&xfull[b], (uint32_t)((ti >> 1) & 1));
-      const float* xin = X_all + b * D * XS;
-      double* exd = exd_all + b * 2 * TE;
-      int* flag = flag_all + b * TE;
-      int I = D;
-      float* outb = Ha;
-      for (int l = 0; l + 1 < p.n_layers; ++l) {
-        const int O = p.dims[l + 1];
-        const float* __restrict__ W = p.W[l];
-        const float* __restrict__ bl = p.b[l];
-        const int O4 = O >> 2;
-        const int units = O4 * (TE >> 2);
-        for (int u = mt; u < units; u += 32 * TMA_NM) {
-          const int o0 = (u % O4) * 4, e0 = (u / O4) * 4;
-          const float4 bv = __ldg((const float4*)(bl + o0));
-          float acc[4][4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            acc[r][0] = bv.x; acc[r][1] = bv.y; acc[r][2] = bv.z; acc[r][3] = bv.w;
-          }
-#pragma unroll 8
-          for (int i = 0; i < I; ++i) {
-            const float4 x = *(const float4*)(xin + i * XS + e0);
-            const float4 w = __ldg((const float4*)(W + (int64_t)i * O + o0));
-            const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              acc[r][0] = fmaf(xs[r], w.x, acc[r][0]);
-              acc[r][1] = fmaf(xs[r], w.y, acc[r][1]);
-              acc[r][2] = fmaf(xs[r], w.z, acc[r][2]);
-              acc[r][3] = fmaf(xs[r], w.w, acc[r][3]);
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float4 o;
-            o.x = relu_nan(acc[0][c]);
-            o.y = relu_nan(acc[1][c]);
-            o.z = relu_nan(acc[2][c]);
-            o.w = relu_nan(acc[3][c]);
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-              if (!isfinite(acc[r][c])) atomicOr(&flag[e0 + r], 8);
-            *(float4*)(outb + (o0 + c) * XS + e0) = o;
-          }
-        }
-        named_bar_sync(1, 32 * TMA_NM);
-        xin = outb;
-        I = O;
-        outb = (outb == Ha) ? Hb : Ha;
-      }
       const int64_t base = ((int64_t)blockIdx.x + ti * gridDim.x) * TE;
-      for (int el = mw; el < TE; el += TMA_NM) {
-        const int64_t e = base + el;
-        if (e >= p.n) continue;
-        double nn = 0.0;
-        if (p.n_layers > 0) {
-          const float* __restrict__ Wo = p.W[p.n_layers - 1];
-          float sacc = 0.f;
-          for (int i = lane; i < I; i += 32) sacc = fmaf(xin[i * XS + el], __ldg(Wo + i), sacc);
-          sacc = warp_sumf(sacc);
-          nn = (double)sacc + (double)__ldg(p.b[p.n_layers - 1]);  // M:372-373
-        }
-        if (lane == 0) {
-          const double logit = nn + exd[el] + exd[TE + el];  // M:377
-          p.prob[e] = (float)sigmoid_clamped(logit);
-          if (p.logit) p.logit[e] = (float)logit;
-          if (!isfinite(logit)) {
-            const int fl = flag[el];
-            const int blk = (fl & 1) ? DFFM_BLOCK_LR : (fl & 2) ? DFFM_BLOCK_FFM
-                          : (fl & 4) ? DFFM_BLOCK_MERGE : (fl & 8) ? DFFM_BLOCK_NN
-                          : DFFM_BLOCK_LOGIT;
-            atomicMin((unsigned long long*)p.status,
-                      (unsigned long long)status_key(p.status_base + e, blk, DFFM_NUMERIC));
-          }
-        }
-      }
-      named_bar_sync(1, 32 * TMA_NM);
-      if (lane == 0) mbar_arrive(&xempty[b]);
+      mlp_warps_tile<TMA_NM>(p, X_all + b * D * XS, exd_all + b * 2 * TE, flag_all + b * TE, Ha,
+                             Hb, base, mt);
+      if ((mt & 31) == 0) mbar_arrive(&xempty[b]);
     }
   }
 }

@@ -51,103 +51,6 @@ __host__ __device__ inline WsSmem ws_smem_layout(int F, int M, int P, int D, int
   return s;
 }
 
-// MLP over one X tile by NM warps (thread index mt in [0, 32*NM)); named
-// barrier 1 synchronises the MLP warps between layers.
-template <int NM>
-__device__ __forceinline__ void mlp_warps_tile(const FwdParams& p, const float* xin,
-                                               const double* exd, int* flag, float* Ha,
-                                               float* Hb, int64_t base, int mt) {
-  const int TE = p.TE, XS = p.XS;
-  const int lane = mt & 31, mw = mt >> 5;
-  if (p.xout) {  // staging mode: rows for the tensor-core MLP (mlp_tc.cu)
-    for (int el = mw; el < TE; el += NM) {
-      const int64_t e = base + el;
-      if (e >= p.n) continue;
-      float* row = p.xout + e * p.Kp;
-      for (int i = lane; i < p.Kp; i += 32) row[i] = i < p.D ? xin[i * XS + el] : 0.f;
-      if (lane == 0) {
-        p.rout[e] = exd[el] + exd[TE + el];
-        p.fout[e] = flag[el];
-      }
-    }
-    __syncwarp();
-    return;
-  }
-  int I = p.D;
-  float* outb = Ha;
-  for (int l = 0; l + 1 < p.n_layers; ++l) {
-    const int O = p.dims[l + 1];
-    const float* __restrict__ W = p.W[l];
-    const float* __restrict__ bl = p.b[l];
-    const int O4 = O >> 2;
-    const int units = O4 * (TE >> 2);
-    for (int u = mt; u < units; u += 32 * NM) {
-      const int o0 = (u % O4) * 4, e0 = (u / O4) * 4;
-      const float4 bv = __ldg((const float4*)(bl + o0));
-      float acc[4][4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        acc[r][0] = bv.x; acc[r][1] = bv.y; acc[r][2] = bv.z; acc[r][3] = bv.w;
-      }
-#pragma unroll 8
-      for (int i = 0; i < I; ++i) {
-        const float4 x = *(const float4*)(xin + i * XS + e0);
-        const float4 w = __ldg((const float4*)(W + (int64_t)i * O + o0));
-        const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          acc[r][0] = fmaf(xs[r], w.x, acc[r][0]);
-          acc[r][1] = fmaf(xs[r], w.y, acc[r][1]);
-          acc[r][2] = fmaf(xs[r], w.z, acc[r][2]);
-          acc[r][3] = fmaf(xs[r], w.w, acc[r][3]);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float4 o;
-        o.x = relu_nan(acc[0][c]);  // M:370
-        o.y = relu_nan(acc[1][c]);
-        o.z = relu_nan(acc[2][c]);
-        o.w = relu_nan(acc[3][c]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (!isfinite(acc[r][c])) atomicOr(&flag[e0 + r], 8);
-        *(float4*)(outb + (o0 + c) * XS + e0) = o;
-      }
-    }
-    named_bar_sync(1, 32 * NM);
-    xin = outb;
-    I = O;
-    outb = (outb == Ha) ? Hb : Ha;
-  }
-  for (int el = mw; el < TE; el += NM) {
-    const int64_t e = base + el;
-    if (e >= p.n) continue;
-    double nn = 0.0;
-    if (p.n_layers > 0) {
-      const float* __restrict__ Wo = p.W[p.n_layers - 1];
-      float sacc = 0.f;
-      for (int i = lane; i < I; i += 32) sacc = fmaf(xin[i * XS + el], __ldg(Wo + i), sacc);
-      sacc = warp_sumf(sacc);
-      nn = (double)sacc + (double)__ldg(p.b[p.n_layers - 1]);  // M:372-373
-    }
-    if (lane == 0) {
-      const double logit = nn + exd[el] + exd[TE + el];  // M:377
-      p.prob[e] = (float)sigmoid_clamped(logit);
-      if (p.logit) p.logit[e] = (float)logit;
-      if (!isfinite(logit)) {
-        const int fl = flag[el];
-        const int blk = (fl & 1) ? DFFM_BLOCK_LR : (fl & 2) ? DFFM_BLOCK_FFM
-                      : (fl & 4) ? DFFM_BLOCK_MERGE : (fl & 8) ? DFFM_BLOCK_NN
-                      : DFFM_BLOCK_LOGIT;
-        atomicMin((unsigned long long*)p.status,
-                  (unsigned long long)status_key(p.status_base + e, blk, DFFM_NUMERIC));
-      }
-    }
-  }
-  named_bar_sync(1, 32 * NM);  // Ha/Hb and this X buffer are free again
-}
-
 template <int K, int MU, typename T>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 fwd_ws_kernel(FwdParams p) {
@@ -253,6 +156,32 @@ fwd_ws_kernel(FwdParams p) {
         __syncwarp();
         double s1 = 0.0;
         int pbad = 0;
+        if constexpr (MU == 1 && K > 0 && (K * sizeof(T)) % 16 == 0) {
+          // single-slot fields: two pairs per lane, loads first (same sums, same order)
+          for (int pp = lane; pp < P; pp += 64) {
+            const int pq = pp + 32;
+            const uint32_t pr = pairtab[pp];
+            const int f1 = pr & 0xFF, f2 = pr >> 8;
+            int g1 = 0, g2 = 0;
+            bool actq = false;
+            if (pq < P) {
+              const uint32_t pr2 = pairtab[pq];
+              g1 = pr2 & 0xFF;
+              g2 = pr2 >> 8;
+              actq = spres[g1] & spres[g2];
+            }
+            const float2 v = pair_dot_x2<K, T>(p, sidx, sval, spres[f1] & spres[f2], f1, f2,
+                                               actq, g1, g2);
+            X[(pp + 1) * XS + el] = v.x;
+            s1 += (double)v.x;
+            pbad |= !isfinite(v.x);
+            if (pq < P) {
+              X[(pq + 1) * XS + el] = v.y;
+              s1 += (double)v.y;
+              pbad |= !isfinite(v.y);
+            }
+          }
+        } else
         for (int pp = lane; pp < P; pp += 32) {
           const uint32_t pr = pairtab[pp];
           const int f1 = pr & 0xFF, f2 = pr >> 8;
