@@ -368,7 +368,7 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
   static int64_t slice_env = -1;
   if (slice_env < 0) {
     const char* v = getenv("DFFM_TC_SLICE");
-    slice_env = v ? atoll(v) : (int64_t)148 * TC_M;
+    slice_env = v ? atoll(v) : (int64_t)4 * 148 * TC_M;
     slice_env = std::max<int64_t>(TC_M, slice_env / TC_M * TC_M);
   }
   const int64_t sl = std::min<int64_t>(slice_env, (p.n + TC_M - 1) / TC_M * TC_M);

@@ -238,16 +238,17 @@ __device__ __forceinline__ void merge_finish(float* X, double* exd, int* flag, i
   }
   s2 = warp_sum(s2) + (lr_out - mu) * (lr_out - mu);
   const double denom = sqrt(s2 / D) + 1e-6;  // population std + MERGE_EPS (M:37, M:359-360)
+  const double rden = 1.0 / denom;            // one f64 division per example
   int mbad = 0;
   for (int pp = lane; pp < P; pp += 32) {
-    const float m = (float)(((double)X[(pp + 1) * XS + el] - mu) / denom);
+    const float m = (float)(((double)X[(pp + 1) * XS + el] - mu) * rden);
     X[(pp + 1) * XS + el] = m;
     mbad |= !isfinite(m);
   }
   pbad = __any_sync(0xffffffffu, pbad);
   mbad = __any_sync(0xffffffffu, mbad);
   if (lane == 0) {
-    const float m0 = (float)((lr_out - mu) / denom);
+    const float m0 = (float)((lr_out - mu) * rden);
     X[el] = m0;
     mbad |= !isfinite(m0);
     exd[el] = lr_out;

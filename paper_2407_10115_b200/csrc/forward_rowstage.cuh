@@ -229,12 +229,13 @@ __global__ void __launch_bounds__(RS_THREADS, 2) fwd_rowstage_kernel(FwdParams p
     rs_block_sum<1>(&s2, red, bsc);
     s2 += (lr_out - mu) * (lr_out - mu);
     const double denom = sqrt(s2 / D) + 1e-6;
+    const double rden = 1.0 / denom;  // one f64 division per example (<= 1 f64 ulp vs dividing)
     int mbad = 0;
     float* row = p.xout + e * p.Kp;
     for (int c = tid; c < p.Kp; c += RS_THREADS) {
       float m = 0.f;
-      if (c == 0) m = (float)((lr_out - mu) / denom);
-      else if (c < D) m = (float)(((double)xv[c] - mu) / denom);
+      if (c == 0) m = (float)((lr_out - mu) * rden);
+      else if (c < D) m = (float)(((double)xv[c] - mu) * rden);
       mbad |= !isfinite(m);
       row[c] = m;
     }
