@@ -13,10 +13,13 @@
 //   copied from the cache.  MergeNorm and the MLP are not cached and
 //   run through the same phase-B tile code as K1.
 #include <algorithm>
+#include <stdlib.h>
+#include <string.h>
 #include <mutex>
 #include <unordered_map>
 
 #include "forward_kernel.cuh"
+#include "mlp_tc.cuh"
 
 namespace dffm {
 
@@ -100,7 +103,8 @@ ctx_kernel(CtxParams q) {
       if (lane == 0) *lrp = tot;
       if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicMin((unsigned long long*)p.status,
-                  (unsigned long long)status_key(r * q.C, DFFM_BLOCK_NONE, DFFM_CONTRACT));
+                  (unsigned long long)status_key(p.status_base + r * q.C, DFFM_BLOCK_NONE,
+                                                 DFFM_CONTRACT));
     }
     __syncthreads();
     for (int x = threadIdx.x; x < Fc; x += FWD_THREADS) {
@@ -149,7 +153,8 @@ ctx_kernel(CtxParams q) {
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0)
           atomicMin((unsigned long long*)p.status,
-                    (unsigned long long)status_key(e, DFFM_BLOCK_NONE, DFFM_CONTRACT));
+                    (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
+                                                   DFFM_CONTRACT));
         const double lr_out = lr_ctx + warp_sum(lrs);
         __syncwarp();
         double s1 = 0.0;
@@ -269,6 +274,13 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
   p.logit = nullptr;
   p.status = status;
   const int smax = max_smem_optin_current();
+  // DFFM_CTX_MLP=tc: MLP on the tensor cores (staged rows + mlp_tc, as K1 v6).
+  // Off by default: at cfg4 (277-64-32-1) K3's candidate gather, not its MLP,
+  // bounds the kernel, and staging costs more than it saves (measured
+  // 93M vs 153M candidates/s).  Read per call.
+  const char* ctx_mlp = getenv("DFFM_CTX_MLP");
+  const bool use_tc = ctx_mlp && strcmp(ctx_mlp, "tc") == 0 && tc_eligible(p, smax);
+  if (use_tc) p.hmax = 0;
   CtxSmem L;
   int TE = 32;
   for (;; TE >>= 1) {
@@ -290,5 +302,32 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
     default: kern = select_ctx<uint16_t>(K, MU); break;
   }
   if (!kern) { set_error("no context kernel for k=%d", p.k); return DFFM_SIZING; }
-  return launch_ctx(kern, q, L.total, (cudaStream_t)stream);
+  if (!use_tc) return launch_ctx(kern, q, L.total, (cudaStream_t)stream);
+  // requests in slices: K3 stages each candidate's MergeNorm row, mlp_tc scores them
+  const cudaStream_t s = (cudaStream_t)stream;
+  const int64_t req_per = std::max<int64_t>(1, tc_default_slice_rows() / n_cand);
+  const int64_t rows_max = std::min<int64_t>(req_per, n_requests) * n_cand;
+  TcPlan plan;
+  if ((rc = tc_plan(p, smax, (rows_max + TC_M - 1) / TC_M * TC_M, s, &plan))) return rc;
+  const int DM = q.Fd * q.Md;
+  for (int64_t r0 = 0; r0 < n_requests; r0 += req_per) {
+    const int64_t nr = std::min<int64_t>(req_per, n_requests - r0);
+    CtxParams a = q;
+    a.cidx = ctx_idx ? ctx_idx + r0 * q.Fc * q.Mc : nullptr;
+    a.cval = ctx_val ? ctx_val + r0 * q.Fc * q.Mc : nullptr;
+    a.didx = cand_idx ? cand_idx + r0 * n_cand * DM : nullptr;
+    a.dval = cand_val ? cand_val + r0 * n_cand * DM : nullptr;
+    a.R = nr;
+    a.f.n = nr * n_cand;
+    a.f.status_base = r0 * n_cand;
+    a.f.prob = prob + r0 * n_cand;
+    a.f.xout = plan.X;
+    a.f.rout = plan.resid;
+    a.f.fout = plan.flags;
+    a.f.Kp = plan.Kp;
+    if ((rc = launch_ctx(kern, a, L.total, s))) return rc;
+    if ((rc = tc_mlp_slice(plan, nr * n_cand, r0 * n_cand, prob + r0 * n_cand, nullptr, s)))
+      return rc;
+  }
+  return DFFM_OK;
 }

@@ -324,10 +324,7 @@ static bool try_rowstage_forward(const dffm_model* m, FwdParams& p, int smax, cu
   return false;
 }
 
-static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
-                           int* rc) {
-  const int fam = forward_family();
-  if (fam != FAM_TC && !(fam == FAM_WS && !g_family_explicit && tc_auto(p))) return false;
+bool tc_eligible(const FwdParams& p, int smax) {
   const int NH = p.n_layers - 1;
   if (NH < 1 || NH > TC_MAXH) return false;
   int nmax = 0;
@@ -336,20 +333,25 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     if (w < 16 || w > 256 || w % 16) return false;
     nmax = std::max(nmax, w);
   }
-  FwdParams pg = p;
-  pg.hmax = 0;  // staging mode: the gather kernels keep no hidden-layer buffers
-  {
-    const WsSmem L = ws_smem_layout(p.F, p.M, p.P, p.D, 8, 12, 0);
-    if (L.total > smax) return false;  // the ws gather (the fallback) must fit
+  return (smax - 1024 - 512) / tc_stage_bytes(nmax) >= 2;
+}
+
+int64_t tc_default_slice_rows() {
+  static int64_t slice_env = -1;
+  if (slice_env < 0) {
+    const char* v = getenv("DFFM_TC_SLICE");
+    slice_env = v ? atoll(v) : (int64_t)4 * 148 * TC_M;
+    slice_env = std::max<int64_t>(TC_M, slice_env / TC_M * TC_M);
   }
-  static int gather_env = -1;
-  if (gather_env < 0) {
-    const char* v = getenv("DFFM_TC_GATHER");
-    gather_env = (v && strcmp(v, "g4") == 0) ? FAM_G4 : (v && strcmp(v, "rows") == 0) ? FAM_ROWS
-                 : (v && strcmp(v, "tma") == 0) ? FAM_TMA : (v && strcmp(v, "ws") == 0) ? FAM_WS
-                 : -1;  // default: row staging when it applies, else ws
-  }
-  MlpTcParams q{};
+  return slice_env;
+}
+
+int tc_plan(const FwdParams& p, int smax, int64_t slice_rows, cudaStream_t s, TcPlan* plan) {
+  MlpTcParams& q = plan->q;
+  q = MlpTcParams{};
+  const int NH = p.n_layers - 1;
+  int nmax = 0;
+  for (int l = 1; l <= NH; ++l) nmax = std::max(nmax, p.dims[l]);
   q.n_hidden = NH;
   const int Kp = (p.D + 15) & ~15;
   size_t wfloats = 0;
@@ -360,42 +362,71 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
   }
   q.stage_bytes = tc_stage_bytes(nmax);
   q.stages = std::min(TC_MAX_STAGES, (smax - 1024 - 512) / q.stage_bytes);
-  if (q.stages < 2) return false;
   int cols = 32;
   while (cols < 2 * nmax) cols <<= 1;
   q.tmem_cols = cols;
-  const int smem_tc = 1024 + q.stages * q.stage_bytes + (3 * q.stages + 2) * 8 + 16;
-  static int64_t slice_env = -1;
-  if (slice_env < 0) {
-    const char* v = getenv("DFFM_TC_SLICE");
-    slice_env = v ? atoll(v) : (int64_t)4 * 148 * TC_M;
-    slice_env = std::max<int64_t>(TC_M, slice_env / TC_M * TC_M);
-  }
-  const int64_t sl = std::min<int64_t>(slice_env, (p.n + TC_M - 1) / TC_M * TC_M);
+  plan->smem = 1024 + q.stages * q.stage_bytes + (3 * q.stages + 2) * 8 + 16;
+  plan->Kp = Kp;
+  plan->slice_rows = slice_rows;
   auto a256 = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  const size_t b_w = a256(wfloats * 4), b_x = a256((size_t)sl * Kp * 4),
-               b_r = a256((size_t)sl * 8), b_f = a256((size_t)sl * 4);
+  const size_t b_w = a256(wfloats * 4), b_x = a256((size_t)slice_rows * Kp * 4),
+               b_r = a256((size_t)slice_rows * 8), b_f = a256((size_t)slice_rows * 4);
   unsigned char* ws = nullptr;
-  if ((*rc = tc_workspace(s, b_w + b_x + b_r + b_f, &ws))) return true;
+  int rc = tc_workspace(s, b_w + b_x + b_r + b_f, &ws);
+  if (rc) return rc;
   float* wblk = (float*)ws;
-  float* X = (float*)(ws + b_w);
-  double* R = (double*)(ws + b_w + b_x);
-  int* Fl = (int*)(ws + b_w + b_x + b_r);
-  {
-    float* wl = wblk;
-    for (int l = 0; l < NH; ++l) {
-      const int kreal = l == 0 ? p.D : p.dims[l];
-      if ((*rc = launch_tc_prep_weights(p.W[l], kreal, q.nout[l], q.kin[l], wl, s))) return true;
-      q.wblk[l] = wl;
-      q.bias[l] = p.b[l];
-      wl += (size_t)q.kin[l] * q.nout[l] * 2;
-    }
+  plan->X = (float*)(ws + b_w);
+  plan->resid = (double*)(ws + b_w + b_x);
+  plan->flags = (int*)(ws + b_w + b_x + b_r);
+  float* wl = wblk;
+  for (int l = 0; l < NH; ++l) {
+    const int kreal = l == 0 ? p.D : p.dims[l];
+    if ((rc = launch_tc_prep_weights(p.W[l], kreal, q.nout[l], q.kin[l], wl, s))) return rc;
+    q.wblk[l] = wl;
+    q.bias[l] = p.b[l];
+    wl += (size_t)q.kin[l] * q.nout[l] * 2;
   }
   q.w_out = p.W[NH];
   q.b_out = p.b[NH];
-  q.resid = R;
-  q.flags = Fl;
+  q.resid = plan->resid;
+  q.flags = plan->flags;
   q.status = p.status;
+  return DFFM_OK;
+}
+
+int tc_mlp_slice(TcPlan& plan, int64_t rows, int64_t status_base, float* prob, float* logit,
+                 cudaStream_t s) {
+  CUtensorMap tm;
+  int rc = rows_tensor_map_x(plan.X, plan.Kp, rows, &tm);
+  if (rc) return rc;
+  plan.q.rows = rows;
+  plan.q.status_base = status_base;
+  plan.q.prob = prob;
+  plan.q.logit = logit;
+  return launch_mlp_tc(tm, plan.q, plan.smem, s);
+}
+
+static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
+                           int* rc) {
+  const int fam = forward_family();
+  if (fam != FAM_TC && !(fam == FAM_WS && !g_family_explicit && tc_auto(p))) return false;
+  if (!tc_eligible(p, smax)) return false;
+  FwdParams pg = p;
+  pg.hmax = 0;  // staging mode: the gather kernels keep no hidden-layer buffers
+  {
+    const WsSmem L = ws_smem_layout(p.F, p.M, p.P, p.D, 8, 12, 0);
+    if (L.total > smax) return false;  // the ws gather (the fallback) must fit
+  }
+  static int gather_env = -2;
+  if (gather_env == -2) {
+    const char* v = getenv("DFFM_TC_GATHER");
+    gather_env = (v && strcmp(v, "g4") == 0) ? FAM_G4 : (v && strcmp(v, "rows") == 0) ? FAM_ROWS
+                 : (v && strcmp(v, "tma") == 0) ? FAM_TMA : (v && strcmp(v, "ws") == 0) ? FAM_WS
+                 : -1;  // default: row staging when it applies, else ws
+  }
+  const int64_t sl = std::min<int64_t>(tc_default_slice_rows(), (p.n + TC_M - 1) / TC_M * TC_M);
+  TcPlan plan;
+  if ((*rc = tc_plan(p, smax, sl, s, &plan))) return true;
   const int64_t FM = (int64_t)p.F * p.M;
   for (int64_t s0 = 0; s0 < p.n; s0 += sl) {
     const int64_t ns = std::min<int64_t>(sl, p.n - s0);
@@ -406,10 +437,10 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     a.status_base = p.status_base + s0;
     a.prob = p.prob + s0;
     a.logit = nullptr;
-    a.xout = X;
-    a.rout = R;
-    a.fout = Fl;
-    a.Kp = Kp;
+    a.xout = plan.X;
+    a.rout = plan.resid;
+    a.fout = plan.flags;
+    a.Kp = plan.Kp;
     bool launched = false;
     if (gather_env < 0) launched = try_rowstage_forward(m, a, smax, s, rc);
     if (gather_env == FAM_G4) launched = try_g4_forward(m, a, smax, s, rc, true);
@@ -418,13 +449,9 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     if (!launched) launched = try_ws_forward(m, a, smax, s, rc, true);
     if (!launched) { set_error("no gather kernel fits the staging slice"); *rc = DFFM_SIZING; }
     if (*rc) return true;
-    CUtensorMap tm;
-    if ((*rc = rows_tensor_map_x(X, Kp, ns, &tm))) return true;
-    q.rows = ns;
-    q.status_base = p.status_base + s0;
-    q.prob = p.prob + s0;
-    q.logit = p.logit ? p.logit + s0 : nullptr;
-    if ((*rc = launch_mlp_tc(tm, q, smem_tc, s))) return true;
+    if ((*rc = tc_mlp_slice(plan, ns, p.status_base + s0, p.prob + s0,
+                            p.logit ? p.logit + s0 : nullptr, s)))
+      return true;
   }
   *rc = DFFM_OK;
   return true;

@@ -270,6 +270,19 @@ __device__ __forceinline__ void mlp_tile(const FwdParams& p, float* X, float* Ha
                                          double* exd, int* flag, int64_t out_base, int nvalid) {
   const int TE = p.TE, XS = p.XS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.xout) {  // staging mode (mlp_tc.cu): rows, residuals, stage bits; row index = out_base + el
+    for (int el = warp; el < nvalid; el += FWD_WARPS) {
+      const int64_t e = out_base + el;
+      float* row = p.xout + e * p.Kp;
+      for (int i = lane; i < p.Kp; i += 32) row[i] = i < p.D ? X[i * XS + el] : 0.f;
+      if (lane == 0) {
+        p.rout[e] = exd[el] + exd[TE + el];
+        p.fout[e] = flag[el];
+      }
+    }
+    __syncthreads();
+    return;
+  }
   const float* xin = X;
   int I = p.D;
   float* outb = Ha;

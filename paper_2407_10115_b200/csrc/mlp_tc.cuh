@@ -39,6 +39,24 @@ __host__ __device__ inline int tc_stage_bytes(int nmax) {
 }
 
 int launch_mlp_tc(const CUtensorMap& tmx, const MlpTcParams& p, int smem, cudaStream_t s);
+
+// Host plan for "stage rows, then tensor-core MLP" over slices (forward.cu):
+// eligibility, per-stream workspace, blocked hi/lo weights.
+struct TcPlan {
+  MlpTcParams q;
+  int smem;
+  int Kp;
+  int64_t slice_rows;
+  float* X;       // [slice_rows][Kp] staged MergeNorm rows
+  double* resid;  // [slice_rows]
+  int* flags;     // [slice_rows]
+};
+struct FwdParams;
+bool tc_eligible(const FwdParams& p, int smax);
+int tc_plan(const FwdParams& p, int smax, int64_t slice_rows, cudaStream_t s, TcPlan* plan);
+int tc_mlp_slice(TcPlan& plan, int64_t rows, int64_t status_base, float* prob, float* logit,
+                 cudaStream_t s);
+int64_t tc_default_slice_rows();
 int launch_tc_prep_weights(const float* W, int K, int N, int Kp, float* dst, cudaStream_t s);
 
 }  // namespace dffm

@@ -111,7 +111,9 @@ def test_hash_synthetic_ranks_large_batch():
 # ------------------------------------------------------------------ K3
 
 
-def test_context_cache_matches_reference_merged_forward():
+@pytest.mark.parametrize("ctx_mlp", ["simt", "tc"])
+def test_context_cache_matches_reference_merged_forward(ctx_mlp, monkeypatch):
+    monkeypatch.setenv("DFFM_CTX_MLP", ctx_mlp)
     g = load("ctx")
     F, k, hidden, bits, flat = fixture_flat(g)
     cfg = ModelConfig(n_fields=F, k=k, hidden_sizes=hidden, hash_bits=bits)
@@ -127,7 +129,10 @@ def test_context_cache_matches_reference_merged_forward():
         inference.predict_batch(cache, g["cand_idx"][3], g["cand_val"][3], st)
 
 
-def test_context_cache_equals_uncached_forward_u16():
+@pytest.mark.parametrize("ctx_mlp", ["simt", "tc"])
+def test_context_cache_equals_uncached_forward_u16(ctx_mlp, monkeypatch):
+    """K3 (SIMT or staged tensor-core MLP) == K1 on the merged examples == oracle."""
+    monkeypatch.setenv("DFFM_CTX_MLP", ctx_mlp)
     wl = configs.CFG4
     bits = 14
     ost = fo.random_store(24, 8, (64, 32), bits, seed=44)
