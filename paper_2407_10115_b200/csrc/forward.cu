@@ -330,10 +330,10 @@ bool tc_eligible(const FwdParams& p, int smax) {
   int nmax = 0;
   for (int l = 1; l <= NH; ++l) {
     const int w = p.dims[l];
-    if (w < 16 || w > 256 || w % 16) return false;
+    if (w < TC_WIDTH_MULT || w > 256 || w % TC_WIDTH_MULT) return false;  // 16-col blocks per part
     nmax = std::max(nmax, w);
   }
-  return (smax - 1024 - 512) / tc_stage_bytes(nmax) >= 2;
+  return tc_smem_bytes(2, tc_stage_bytes(nmax)) <= smax;
 }
 
 int64_t tc_default_slice_rows() {
@@ -361,11 +361,12 @@ int tc_plan(const FwdParams& p, int smax, int64_t slice_rows, cudaStream_t s, Tc
     wfloats += (size_t)q.kin[l] * q.nout[l] * 2;
   }
   q.stage_bytes = tc_stage_bytes(nmax);
-  q.stages = std::min(TC_MAX_STAGES, (smax - 1024 - 512) / q.stage_bytes);
+  q.stages = TC_MAX_STAGES;
+  while (q.stages > 2 && tc_smem_bytes(q.stages, q.stage_bytes) > smax) --q.stages;
   int cols = 32;
   while (cols < 2 * nmax) cols <<= 1;
   q.tmem_cols = cols;
-  plan->smem = 1024 + q.stages * q.stage_bytes + (3 * q.stages + 2) * 8 + 16;
+  plan->smem = tc_smem_bytes(q.stages, q.stage_bytes);
   plan->Kp = Kp;
   plan->slice_rows = slice_rows;
   auto a256 = [](size_t b) { return (b + 255) & ~(size_t)255; };

@@ -12,13 +12,15 @@
 //              (3xTF32: ~fp32 accuracy from the TF32 tensor cores; the
 //              tensor core truncates f32 operands to tf32, so A_hi is the raw
 //              f32 and A_lo = x - trunc_tf32(x))
-//   warps 2-5  layer 0: A_lo for each landed X chunk; layers >= 1: the
-//              previous layer's TMEM accumulator -> +bias, ReLU (NaN kept,
-//              M:370) -> hi/lo A chunks; last: output column dot product,
-//              residual logit (M:377), clamped sigmoid (M:304-305), status.
-// Two TMEM regions alternate between layers, so layer l+1's MMAs overlap the
-// epilogue draining layer l.  All operand layouts are the canonical K-major
-// core-matrix layouts (validated by tools/tc_probe.cu).
+//   warps 2-9  (two per TMEM lane quadrant, each owning half of a layer's
+//              columns) layer 0: A_lo for each landed X chunk; every layer:
+//              drain each accumulation group from TMEM into f32 register sums
+//              (see below), then +bias, ReLU (NaN kept, M:370) -> the next
+//              layer's hi/lo A chunks straight from registers; last: output
+//              column dot product (halves meet in shared memory), residual
+//              logit (M:377), clamped sigmoid (M:304-305), status.
+// All operand layouts are the canonical K-major core-matrix layouts
+// (validated by tools/tc_probe.cu).
 #include "mlp_tc.cuh"
 
 namespace dffm {
@@ -90,6 +92,44 @@ __device__ __forceinline__ float tf32_lo(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
+// Accumulation precision: the tensor core's f32 accumulation is coarser than
+// IEEE round-to-nearest (tools/tc_accuracy.cu: one accumulator over K=784 at
+// cfg5 scale errs 2.5e-5 x rms vs 3.7e-6 for a sequential fp32 FMA chain), so
+// each layer's K-loop is cut into groups of TC_GROUP chunks: a group
+// accumulates in one TMEM region (regions alternate), and the epilogue drains
+// it into IEEE f32 register sums while the MMAs run the next group.
+
+// one thread's part of a row of accumulators, statically indexed (registers)
+struct HalfRow {
+  float v[TC_PART_MAX];
+};
+
+__device__ __forceinline__ void drain_group(HalfRow& acc, uint32_t taddr, int nblk, bool first) {
+#pragma unroll
+  for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
+    if (cb < nblk) {
+      float v[16];
+      tmem_ld16(taddr + (uint32_t)cb * 16, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc.v[cb * 16 + j] = first ? v[j] : acc.v[cb * 16 + j] + v[j];
+    }
+  }
+}
+
+// drain accumulation group #dg (region dg & 1) into this thread's half-row
+__device__ __forceinline__ void epi_drain(HalfRow& acc, uint64_t* accf, uint64_t* tempty,
+                                          uint32_t& dg, uint32_t lane_base, uint32_t RS,
+                                          int col0, int nblk, bool first, int lane) {
+  const uint32_t reg = dg & 1;
+  mbar_wait(&accf[reg], (dg >> 1) & 1);
+  tc_fence_after();
+  drain_group(acc, lane_base + reg * RS + (uint32_t)col0, nblk, first);
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&tempty[reg]);
+  ++dg;
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
 mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   extern __shared__ unsigned char smem_raw[];
@@ -98,18 +138,23 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   uint64_t* full = (uint64_t*)(smem + S * SB);
   uint64_t* aready = full + S;
   uint64_t* empty = aready + S;
-  uint64_t* accf = empty + S;  // [2] accumulator region complete
-  uint32_t* tmem_slot = (uint32_t*)(accf + 2);
+  uint64_t* accf = empty + S;    // [2] TMEM region holds a finished group
+  uint64_t* tempty = accf + 2;   // [2] TMEM region drained by the epilogue
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  float* xpart = (float*)(smem + S * SB + (3 * S + 4) * 8 + 16);  // [2][TC_PARTS][TC_M]
+  int* xbad = (int*)(xpart + 2 * TC_PARTS * TC_M);                 // [2][TC_PARTS][TC_M]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&aready[s], 4);
+      mbar_init(&aready[s], TC_EPI_WARPS);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&accf[0], 1);
-    mbar_init(&accf[1], 1);
+    for (int r = 0; r < 2; ++r) {
+      mbar_init(&accf[r], 1);
+      mbar_init(&tempty[r], TC_EPI_WARPS);
+    }
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -148,14 +193,20 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint32_t g = 0;
+      uint32_t g = 0, gg = 0;  // chunk counter, accumulation-group counter
+      uint32_t d = tmem;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int l = 0; l < NH; ++l) {
           const int nck = p.kin[l] >> 4, N = p.nout[l];
           const uint32_t id = idesc_tf32(TC_M, N);
-          const uint32_t d = tmem + (uint32_t)(l & 1) * RS;
           const uint32_t lboW = (uint32_t)(N >> 3) * 128u;
           for (int c = 0; c < nck; ++c, ++g) {
+            const int cg = c % TC_GROUP;
+            if (cg == 0) {  // a new group: its region must have been drained
+              const uint32_t reg = gg & 1;
+              if (gg >= 2) mbar_wait(&tempty[reg], ((gg >> 1) - 1) & 1);
+              d = tmem + reg * RS;
+            }
             const int s = (int)(g % S);
             const uint32_t u = g / S;
             mbar_wait(&aready[s], u & 1);
@@ -175,104 +226,117 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
               }
               const uint64_t bhi = umma_desc(whi + ks * 2 * lboW, lboW, 128, 0);
               const uint64_t blo = umma_desc(wlo + ks * 2 * lboW, lboW, 128, 0);
-              mma_tf32(d, ahi, bhi, id, (c | ks) != 0);
+              mma_tf32(d, ahi, bhi, id, (cg | ks) != 0);
               mma_tf32(d, ahi, blo, id, 1);
               mma_tf32(d, alo, bhi, id, 1);
             }
-            mma_commit(&empty[s]);                   // stage reusable once these MMAs finish
-            if (c == nck - 1) mma_commit(&accf[l & 1]);  // layer's accumulator complete
+            mma_commit(&empty[s]);  // stage reusable once these MMAs finish
+            if (cg == TC_GROUP - 1 || c == nck - 1) {
+              mma_commit(&accf[gg & 1]);  // group complete in its region
+              ++gg;
+            }
           }
         }
       }
     }
   } else {
-    // ------------------------------------------------------------ converter + epilogue
-    const int q = warp & 3;            // TMEM lane quadrant this warp may access
-    const int r = q * 32 + lane;       // tile row = example handled by this thread
-    const int ct = threadIdx.x - 64;   // 0..127
+    // ------------------------------------------------------------ epilogue warps
+    const int ew = warp - 2;               // 0 .. TC_EPI_WARPS-1
+    const int h = ew >> 2;                 // column part owned by this warp
+    const int q = warp & 3;                // TMEM lane quadrant this warp may access
+    const int r = q * 32 + lane;           // tile row = example of this thread
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    uint32_t g = 0, ause0 = 0, ause1 = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint32_t g = 0, dg = 0;                // chunk counter, drained-group counter
+    HalfRow acc;
+    int tl = 0;                            // local tile counter (exchange buffer parity)
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
       int nn_bad = 0;
       for (int l = 0; l < NH; ++l) {
-        const int nck = p.kin[l] >> 4;
-        if (l == 0) {
-          for (int c = 0; c < nck; ++c, ++g) {
+        const int nck = p.kin[l] >> 4, N = p.nout[l];
+        const int hc = N / TC_PARTS;       // columns per part (multiple of 16)
+        const int ngr = (nck + TC_GROUP - 1) / TC_GROUP;
+        const int hcp = l > 0 ? p.nout[l - 1] / TC_PARTS : 0;  // previous layer's part width
+        for (int gi = 0; gi < ngr; ++gi) {
+          const int cend = min(nck, (gi + 1) * TC_GROUP);
+          for (int c = gi * TC_GROUP; c < cend; ++c, ++g) {
             const int s = (int)(g % S);
             mbar_wait(&full[s], (g / S) & 1);
-            const float4* a = (const float4*)(smem + s * SB);
-            float4* lo = (float4*)(smem + s * SB + 8192);
-#pragma unroll
-            for (int i = ct; i < 512; i += 128) {
-              const float4 x = a[i];
-              lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
-            }
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&aready[s]);
-          }
-        } else {
-          const int reg = (l - 1) & 1;
-          mbar_wait(&accf[reg], (reg ? ause1 : ause0) & 1);
-          if (reg) ++ause1; else ++ause0;
-          tc_fence_after();
-          const float* __restrict__ bl = p.bias[l - 1];
-          for (int c = 0; c < nck; ++c, ++g) {
-            const int s = (int)(g % S);
-            mbar_wait(&full[s], (g / S) & 1);  // W landed => the stage's A area is free
-            float v[16];
-            tmem_ld16(lane_base + (uint32_t)reg * RS + (uint32_t)c * 16, v);
             unsigned char* st = smem + s * SB;
+            if (l == 0) {  // A_lo of the landed X chunk (same swizzled positions)
+              const float4* a = (const float4*)st;
+              float4* lo = (float4*)(st + 8192);
 #pragma unroll
-            for (int kq = 0; kq < 4; ++kq) {
-              const float4 b4 = __ldg((const float4*)(bl + c * 16 + kq * 4));
-              const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
-              float a4[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float z = v[kq * 4 + j] + bb[j];  // M:368
-                nn_bad |= !isfinite(z);
-                a4[j] = relu_nan(z);                    // M:370
+              for (int i = ew * 32 + lane; i < 512; i += 32 * TC_EPI_WARPS) {
+                const float4 x = a[i];
+                lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
               }
-              const int off = ((kq * 16 + (r >> 3)) * 128) + (r & 7) * 16;
-              *(float4*)(st + off) = make_float4(a4[0], a4[1], a4[2], a4[3]);
-              *(float4*)(st + 8192 + off) =
-                  make_float4(tf32_lo(a4[0]), tf32_lo(a4[1]), tf32_lo(a4[2]), tf32_lo(a4[3]));
+            } else if ((c * 16) / hcp == h) {  // this part holds the chunk's 16 columns
+              const int cbl = (c * 16 - h * hcp) >> 4;
+#pragma unroll
+              for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
+                if (cb == cbl) {
+#pragma unroll
+                  for (int kq = 0; kq < 4; ++kq) {
+                    const float* a4 = acc.v + cb * 16 + kq * 4;
+                    const int off = ((kq * 16 + (r >> 3)) * 128) + (r & 7) * 16;
+                    *(float4*)(st + off) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+                    *(float4*)(st + 8192 + off) =
+                        make_float4(tf32_lo(a4[0]), tf32_lo(a4[1]), tf32_lo(a4[2]), tf32_lo(a4[3]));
+                  }
+                }
+              }
             }
-            tc_fence_before();
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&aready[s]);
           }
+          if (gi > 0)  // one group behind the MMAs
+            epi_drain(acc, accf, tempty, dg, lane_base, RS, h * hc, hc >> 4, gi == 1, lane);
         }
-      }
-      // ---- output layer (M:372-373), residual logit (M:377), sigmoid (M:304-305)
-      const int reg = (NH - 1) & 1;
-      mbar_wait(&accf[reg], (reg ? ause1 : ause0) & 1);
-      if (reg) ++ause1; else ++ause0;
-      tc_fence_after();
-      const float* __restrict__ bl = p.bias[NH - 1];
-      float acc = 0.f;
-      const int NL = p.nout[NH - 1];
-      for (int c = 0; c < (NL >> 4); ++c) {
-        float v[16];
-        tmem_ld16(lane_base + (uint32_t)reg * RS + (uint32_t)c * 16, v);
+        epi_drain(acc, accf, tempty, dg, lane_base, RS, h * hc, hc >> 4, ngr == 1, lane);
+        // acc = this part's pre-activations of layer l: + bias, ReLU (M:368-370)
+        const float* __restrict__ bl = p.bias[l] + h * hc;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float z = v[j] + __ldg(bl + c * 16 + j);
-          nn_bad |= !isfinite(z);
-          acc = fmaf(relu_nan(z), __ldg(p.w_out + c * 16 + j), acc);
+        for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
+          if (cb < (hc >> 4)) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float z = acc.v[cb * 16 + j] + __ldg(bl + cb * 16 + j);
+              nn_bad |= !isfinite(z);
+              acc.v[cb * 16 + j] = relu_nan(z);
+            }
+          }
         }
       }
-      tc_fence_before();  // TMEM reads done before this thread's next aready arrival
+      // ---- output layer (M:372-373): the parts' partial dots meet in shared memory
+      const int hcl = p.nout[NH - 1] / TC_PARTS;
+      const float* __restrict__ wo = p.w_out + h * hcl;
+      float part = 0.f;
+#pragma unroll
+      for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
+        if (cb < (hcl >> 4)) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) part = fmaf(acc.v[cb * 16 + j], __ldg(wo + cb * 16 + j), part);
+        }
+      }
+      float* xp = xpart + (tl & 1) * TC_PARTS * TC_M;
+      int* xb = xbad + (tl & 1) * TC_PARTS * TC_M;
+      if (h > 0) { xp[h * TC_M + r] = part; xb[h * TC_M + r] = nn_bad; }
+      named_bar_sync(1, 32 * TC_EPI_WARPS);
       const int64_t e = t * TC_M + r;
-      if (e < p.rows) {
-        const double nn = (double)acc + (double)__ldg(p.b_out);
-        const double logit = nn + p.resid[e];
+      if (h == 0 && e < p.rows) {
+        float acc_nn = part;
+#pragma unroll
+        for (int k2 = 1; k2 < TC_PARTS; ++k2) {  // fixed order: deterministic
+          acc_nn += xp[k2 * TC_M + r];
+          nn_bad |= xb[k2 * TC_M + r];
+        }
+        const double nn = (double)acc_nn + (double)__ldg(p.b_out);
+        const double logit = nn + p.resid[e];  // M:377
         p.prob[e] = (float)sigmoid_clamped(logit);
         if (p.logit) p.logit[e] = (float)logit;
         if (!isfinite(logit)) {  // first non-finite stage, M:308-318
-          const int fl = p.flags[e] | (nn_bad || !isfinite(acc) ? 8 : 0);
+          const int fl = p.flags[e] | (nn_bad || !isfinite(acc_nn) ? 8 : 0);
           const int blk = (fl & 1) ? DFFM_BLOCK_LR : (fl & 2) ? DFFM_BLOCK_FFM
                         : (fl & 4) ? DFFM_BLOCK_MERGE : (fl & 8) ? DFFM_BLOCK_NN
                         : DFFM_BLOCK_LOGIT;

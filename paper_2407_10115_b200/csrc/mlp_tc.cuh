@@ -11,7 +11,18 @@ namespace dffm {
 constexpr int TC_M = 128;       // examples per tile = UMMA M (one TMEM lane per example)
 constexpr int TC_KC = 16;       // K elements per pipeline stage (64 B per row)
 constexpr int TC_MAXH = 4;      // hidden layers (M:70-71)
-constexpr int TC_THREADS = 192; // warp 0 TMA, warp 1 MMA, warps 2-5 convert + epilogue
+#ifndef DFFM_TC_PARTS
+#define DFFM_TC_PARTS 4
+#endif
+constexpr int TC_PARTS = DFFM_TC_PARTS;  // epilogue warps per TMEM lane quadrant (column parts)
+constexpr int TC_EPI_WARPS = 4 * TC_PARTS;
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, then epilogue
+constexpr int TC_PART_MAX = 256 / TC_PARTS;  // accumulator columns per epilogue thread
+constexpr int TC_WIDTH_MULT = 16 * TC_PARTS; // hidden widths: multiples of this, <= 256
+#ifndef DFFM_TC_GROUP
+#define DFFM_TC_GROUP 8
+#endif
+constexpr int TC_GROUP = DFFM_TC_GROUP;  // K chunks per TMEM accumulation group
 constexpr int TC_MAX_STAGES = 8;
 
 struct MlpTcParams {
@@ -36,6 +47,12 @@ struct MlpTcParams {
 
 __host__ __device__ inline int tc_stage_bytes(int nmax) {
   return (16384 + nmax * 128 + 1023) & ~1023;
+}
+// dynamic shared memory: 1 KB alignment slack, stages, barriers
+// (full/aready/empty per stage, accf/tempty per TMEM region), TMEM slot, and
+// the two halves' row exchange (double-buffered by tile)
+__host__ __device__ inline int tc_smem_bytes(int stages, int stage_bytes) {
+  return 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16 + 2 * TC_PARTS * TC_M * 8;
 }
 
 int launch_mlp_tc(const CUtensorMap& tmx, const MlpTcParams& p, int smem, cudaStream_t s);

@@ -21,6 +21,7 @@
 //   duplicate buckets across fields: gradients summed in occurrence order
 //             before one update (sort-and-segment, M:424-437)
 //   sparse    zero-gradient slots are skipped; byte-identical to dense (M:536-572)
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <math.h>
 #include <stdlib.h>
@@ -65,6 +66,7 @@ struct TrainParams {
   int dmax;      // max layer width incl. D
   int mlp_size;  // floats in W+b over all layers
   int mlp_smem;  // 1: MLP weights + accumulators resident in shared memory
+  int hogwild;   // K6: each CTA is an independent worker over examples blockIdx.x + i*gridDim.x
   float* lr;
   float* ffm;
   float* W[DFFM_MAX_LAYERS];
@@ -140,6 +142,13 @@ __device__ __forceinline__ void adagrad(float* w, float* acc, double g, double l
   *w = __double2float_rn(__dsub_rn((double)*w, step));
 }
 
+// MLP element of the working copy: shared memory, or global (L2-only reads so
+// no SM keeps a stale L1 line of a weight another SM -- Hogwild worker or
+// cluster peer -- updated)
+__device__ __forceinline__ double ldm(const float* q, bool glob) {
+  return (double)(glob ? __ldcg(q) : *q);
+}
+
 // Same step on a global-memory slot shared across the cluster's SMs: L2-only
 // accesses so no CTA can read a stale L1 line of another SM's update.
 __device__ __forceinline__ void adagrad_g(float* w, float* acc, double g, double lr, double pt) {
@@ -147,6 +156,12 @@ __device__ __forceinline__ void adagrad_g(float* w, float* acc, double g, double
   __stcg(acc, __double2float_rn(a64));
   const double step = __dmul_rn(__dmul_rn(lr, g), inv_pow(a64, pt));
   __stcg(w, __double2float_rn(__dsub_rn((double)__ldcg(w), step)));
+}
+
+__device__ __forceinline__ void adagrad_m(float* w, float* acc, double g, double lr, double pt,
+                                          bool glob) {
+  if (glob) adagrad_g(w, acc, g, lr, pt);
+  else adagrad(w, acc, g, lr, pt);
 }
 
 // Block-wide f64 sum (all threads call); result broadcast to all.  One
@@ -272,10 +287,16 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
   const bool pf_on = FM <= TR_THREADS;
   int pf_j = -1;
   float pf_x = 0.f;
-  if (pf_on && tid < FM && p.n > 0) { pf_j = p.idx[tid]; pf_x = p.val[tid]; }
+  const bool mg = !p.mlp_smem;  // MLP working copy in global memory
+  const int64_t e0 = p.hogwild ? blockIdx.x : 0, estep = p.hogwild ? gridDim.x : 1;
+  if (pf_on && tid < FM && e0 < p.n) { pf_j = p.idx[e0 * FM + tid]; pf_x = p.val[e0 * FM + tid]; }
   const int row_bytes = Fk * 4;
 
-  for (int64_t e = 0; e < p.n; ++e) {
+  for (int64_t e = e0; e < p.n; e += estep) {
+    if (p.hogwild) {  // a worker that hit an error stops the pool (T:253-256)
+      if (__syncthreads_or(tid == 0 && __ldcg((const unsigned long long*)p.status) != ~0ull))
+        break;
+    }
     // ---------------------------------------------------------- stage example
     TR_MARK(0);
     const int label = p.labels[e];
@@ -296,7 +317,10 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           const unsigned char* ar = (const unsigned char*)(p.ffm_acc + (int64_t)j * Fk);
           for (int off = 0; off < row_bytes; off += 128) prefetch_l2(ar + off);
         }
-        if (e + 1 < p.n) { pf_j = p.idx[(e + 1) * FM + tid]; pf_x = p.val[(e + 1) * FM + tid]; }
+        if (e + estep < p.n) {
+          pf_j = p.idx[(e + estep) * FM + tid];
+          pf_x = p.val[(e + estep) * FM + tid];
+        }
       }
     } else {
       for (int s = tid; s < FM; s += TR_THREADS) {
@@ -432,7 +456,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           const int o = tid % Ow, pa = tid / Ow;
           if (pa < G) {
             double s = 0.0;
-            for (int i = pa; i < I; i += G) s += a[i] * (double)W[(int64_t)i * ld + o];
+            for (int i = pa; i < I; i += G) s += a[i] * ldm(W + (int64_t)i * ld + o, mg);
             part[pa * Ow + o] = s;
           }
           __syncthreads();
@@ -442,9 +466,9 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           if (G > 1) {
             for (int q = 0; q < G; ++q) z += part[q * Ow + o];
           } else {
-            for (int i = 0; i < I; ++i) z += a[i] * (double)W[(int64_t)i * ld + o];
+            for (int i = 0; i < I; ++i) z += a[i] * ldm(W + (int64_t)i * ld + o, mg);
           }
-          z += (double)bl[l][o];  // M:368
+          z += ldm(&bl[l][o], mg);  // M:368
           if (split) {
             // owner broadcasts its columns' pre-activations to every CTA (DSMEM)
             for (int rk = 0; rk < C; ++rk)
@@ -471,8 +495,8 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       }
       const int I = p.dims[NL - 1];
       double s = 0.0;
-      for (int i = tid; i < I; i += TR_THREADS) s += a[i] * (double)Wl[NL - 1][i];
-      nn_out = block_sum(s, red, bsc) + (double)bl[NL - 1][0];  // M:372-373
+      for (int i = tid; i < I; i += TR_THREADS) s += a[i] * ldm(&Wl[NL - 1][i], mg);
+      nn_out = block_sum(s, red, bsc) + ldm(&bl[NL - 1][0], mg);  // M:372-373
       nn_bad = __syncthreads_or(nn_bad);
     }
     TR_MARK(7);
@@ -486,7 +510,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       }
       break;
     }
-    if (pf_on && rank == 0 && tid < FM && e + 1 < p.n && pf_j >= 0 && pf_j < p.n_buckets) {
+    if (pf_on && rank == 0 && tid < FM && e + estep < p.n && pf_j >= 0 && pf_j < p.n_buckets) {
       const unsigned char* wr = (const unsigned char*)(p.ffm + (int64_t)pf_j * Fk);
       for (int off = 0; off < row_bytes; off += 128) prefetch_l2(wr + off);
       prefetch_l2(p.lr + pf_j);
@@ -514,13 +538,13 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         if (Ow <= 8) {  // narrow (cluster-split) slice: thread per row
           for (int r = tid; r < I; r += TR_THREADS) {
             double s = 0.0;
-            for (int c = 0; c < Ow; ++c) s += (double)W[(int64_t)r * ld + c] * dcur[cb + c];
+            for (int c = 0; c < Ow; ++c) s += ldm(W + (int64_t)r * ld + c, mg) * dcur[cb + c];
             (split ? dpart : dnext)[r] = s;
           }
         } else {
           for (int r = warp; r < I; r += TR_WARPS) {
             double s = 0.0;
-            for (int c = lane; c < Ow; c += 32) s += (double)W[(int64_t)r * ld + c] * dcur[cb + c];
+            for (int c = lane; c < Ow; c += 32) s += ldm(W + (int64_t)r * ld + c, mg) * dcur[cb + c];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) (split ? dpart : dnext)[r] = s;
@@ -542,8 +566,8 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
           for (int t = tid; t < I * Ow; t += TR_THREADS) {
             const int r = t / Ow, c = t - r * Ow;
             const double gr = __dmul_rn(a_in[r], dcur[cb + c]);
-            if (gr != 0.0 || !p.sparse) adagrad(&W[(int64_t)r * ld + c], &Wa[(int64_t)r * ld + c],
-                                                gr, p.lr_nn, pt);
+            if (gr != 0.0 || !p.sparse) adagrad_m(&W[(int64_t)r * ld + c], &Wa[(int64_t)r * ld + c],
+                                                  gr, p.lr_nn, pt, mg);
           }
         } else {
           for (int r = warp; r < I; r += TR_WARPS) {
@@ -553,13 +577,13 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
             float* war = Wa + (int64_t)r * ld;
             for (int c = lane; c < Ow; c += 32) {
               const double gr = __dmul_rn(ar, dcur[cb + c]);
-              if (gr != 0.0 || !p.sparse) adagrad(&wr[c], &war[c], gr, p.lr_nn, pt);
+              if (gr != 0.0 || !p.sparse) adagrad_m(&wr[c], &war[c], gr, p.lr_nn, pt, mg);
             }
           }
         }
         for (int c = tid; c < Ow; c += TR_THREADS) {  // M:557-572
           const double gr = dcur[cb + c];
-          if (gr != 0.0 || !p.sparse) adagrad(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt);
+          if (gr != 0.0 || !p.sparse) adagrad_m(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt, mg);
         }
         if (l > 0) {
           hoff -= I;
@@ -821,4 +845,78 @@ extern "C" int dffm_train_sequential(const dffm_model* model, const dffm_train_s
   }
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(train)");
   return DFFM_OK;
+}
+
+// K6: Hogwild-style trainer (T:242-336).  n_workers CTAs, each an
+// independent predict-then-learn loop over examples w, w + W, w + 2W, ...
+// against the SHARED store: no locks, no ordering between workers (a lost or
+// overwritten update is allowed, T:1-11; individual f32 stores never tear).
+// MLP state stays in global memory (L2-only accesses).  n_workers == 1 is the
+// sequential kernel itself, so its result is identical to train_sequential.
+extern "C" int dffm_train_hogwild(const dffm_model* model, const dffm_train_state* state,
+                                  const int32_t* idx, const float* val, const uint8_t* labels,
+                                  int32_t max_per_field, int64_t n, int32_t n_workers,
+                                  double* prob_out, void* scratch, uint64_t* status,
+                                  void* stream) {
+  if (n_workers < 1) { set_error("n_workers must be >= 1"); return DFFM_CONTRACT; }
+  if (n_workers == 1)
+    return dffm_train_sequential(model, state, idx, val, labels, max_per_field, n, prob_out,
+                                 scratch, status, stream);
+  (void)scratch;
+  TrainParams p{};
+  int smem = 0;
+  int rc = tr_validate(model, max_per_field, 1, p, &smem);
+  if (rc) return rc;
+  if (p.mlp_smem) {  // workers share the MLP in global memory
+    p.mlp_smem = 0;
+    smem = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 0).total;
+  }
+  p.hogwild = 1;
+  if (!state || !state->lr_acc || !state->ffm_acc) {
+    set_error("null optimizer state");
+    return DFFM_CONTRACT;
+  }
+  if (n < 0) { set_error("negative n"); return DFFM_CONTRACT; }
+  if (n == 0) return DFFM_OK;
+  if (!idx || !val || !labels || !prob_out || !status) {
+    set_error("null buffer");
+    return DFFM_CONTRACT;
+  }
+  for (int l = 0; l < p.n_layers; ++l) {
+    if (!state->W_acc[l] || !state->b_acc[l]) { set_error("null MLP acc"); return DFFM_CONTRACT; }
+    p.W_acc[l] = state->W_acc[l];
+    p.b_acc[l] = state->b_acc[l];
+  }
+  p.lr_acc = state->lr_acc;
+  p.ffm_acc = state->ffm_acc;
+  p.lr_ffm = state->lr_ffm;
+  p.lr_lr = state->lr_lr;
+  p.lr_nn = state->lr_nn;
+  p.power_t = state->power_t;
+  p.sparse = state->sparse;
+  p.idx = idx;
+  p.val = val;
+  p.labels = labels;
+  p.prob_out = prob_out;
+  p.status = status;
+  p.n = n;
+  int occ = 0;
+  rc = kernel_occupancy((const void*)train_kernel<1>, TR_THREADS, smem, &occ);
+  if (rc) return rc;
+  // concurrent workers only: a CTA that could not be resident would run later,
+  // in series with the others
+  const int64_t W = std::min<int64_t>({(int64_t)n_workers, (int64_t)occ * sm_count_current(), n});
+  train_kernel<1><<<(unsigned)W, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(train hogwild)");
+  return DFFM_OK;
+}
+
+extern "C" int dffm_hogwild_max_workers(const dffm_model* model, int32_t max_per_field) {
+  TrainParams p{};
+  int smem = 0;
+  if (tr_validate(model, max_per_field, 1, p, &smem)) return 0;
+  smem = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 0).total;
+  int occ = 0;
+  if (kernel_occupancy((const void*)train_kernel<1>, TR_THREADS, smem, &occ)) return 0;
+  return occ * sm_count_current();
 }
