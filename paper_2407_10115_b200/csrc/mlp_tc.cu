@@ -169,6 +169,9 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   const uint32_t tmem = *tmem_slot;
   const uint32_t RS = (uint32_t)p.tmem_cols >> 1;  // accumulator region stride (columns)
   const int64_t ntiles = (p.rows + TC_M - 1) / TC_M;
+  // newest rows first: the gather kernel wrote the slice in row order just
+  // before, so its last rows are the ones still resident in L2
+  auto tile_row = [&](int64_t t) { return ntiles - 1 - t; };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -184,7 +187,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
             if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
             unsigned char* st = smem + s * SB;
             mbar_arrive_expect_tx(&full[s], wbytes + (l == 0 ? 8192u : 0u));
-            if (l == 0) tma_load_2d(st, &tmx, c * TC_KC, (int)(t * TC_M), &full[s]);
+            if (l == 0) tma_load_2d(st, &tmx, c * TC_KC, (int)(tile_row(t) * TC_M), &full[s]);
             tma_load_1d(st + 16384, p.wblk[l] + (size_t)c * p.nout[l] * 32, wbytes, &full[s]);
           }
         }
@@ -323,7 +326,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
       int* xb = xbad + (tl & 1) * TC_PARTS * TC_M;
       if (h > 0) { xp[h * TC_M + r] = part; xb[h * TC_M + r] = nn_bad; }
       named_bar_sync(1, 32 * TC_EPI_WARPS);
-      const int64_t e = t * TC_M + r;
+      const int64_t e = tile_row(t) * TC_M + r;
       if (h == 0 && e < p.rows) {
         float acc_nn = part;
 #pragma unroll
