@@ -98,8 +98,13 @@ int dffm_forward(const dffm_model* model, const int32_t* idx, const float* val,
 /*
  * K1 kernel family (all compute identical results within the 1e-5 contract;
  * shapes a family cannot take fall back to family 2):
- *   0 row-coalesced, 1 warp-specialised (default), 2 CTA-synchronous,
- *   3 TMA 1-D ring, 4 TMA gather4 ring, -1 = from DFFM_FORWARD_KERNEL.
+ *   0 row-coalesced, 1 warp-specialised (fused MLP on CUDA cores),
+ *   2 CTA-synchronous, 3 TMA 1-D ring, 4 TMA gather4 ring,
+ *   5 staged rows + tcgen05 3xTF32 MLP (hidden widths multiples of 16, <= 256),
+ *   -1 = from DFFM_FORWARD_KERNEL; unset = 1, or 5 when the MLP has >= 64K
+ *   multiply-adds per example (cfg5) and fits.
+ * Family 5 keeps a per-(device, stream) device workspace (staged rows of one
+ * slice + the blocked hi/lo MLP weights), allocated on first use.
  * Process-wide; for A/B measurements and tests.
  */
 int dffm_set_forward_family(int32_t family);
@@ -142,6 +147,23 @@ int dffm_train_sequential(const dffm_model* model, const dffm_train_state* state
                           const int32_t* idx, const float* val, const uint8_t* labels,
                           int32_t max_per_field, int64_t n, double* prob_out,
                           void* scratch, uint64_t* status, void* stream);
+
+/*
+ * K6 Hogwild-style trainer: replaces hogwild_train (T:269-336).
+ * n_workers independent predict-then-learn loops run concurrently on the
+ * GPU (one CTA each; worker w takes examples w, w + W, ...) against the SHARED
+ * store with no locks -- concurrent updates may overwrite each other (T:1-11),
+ * f32 stores never tear.  prob_out[e] is example e's progressive prediction.
+ * n_workers == 1 is dffm_train_sequential exactly.  Workers beyond what can be
+ * resident at once are not launched (dffm_hogwild_max_workers).  An error in
+ * any worker stops every worker at its next example; the status word holds
+ * the smallest failing example index.
+ */
+int dffm_train_hogwild(const dffm_model* model, const dffm_train_state* state,
+                       const int32_t* idx, const float* val, const uint8_t* labels,
+                       int32_t max_per_field, int64_t n, int32_t n_workers, double* prob_out,
+                       void* scratch, uint64_t* status, void* stream);
+int dffm_hogwild_max_workers(const dffm_model* model, int32_t max_per_field);
 
 /*
  * K4 16-bit quantisation (formula PAPER.md:291-305).

@@ -60,6 +60,10 @@ SIGNATURES = {
     "dffm_train_sequential": (c_int32, [POINTER(DffmModel), POINTER(DffmTrainState), c_void_p,
                                         c_void_p, c_void_p, c_int32, c_int64, c_void_p,
                                         c_void_p, c_void_p, c_void_p]),
+    "dffm_train_hogwild": (c_int32, [POINTER(DffmModel), POINTER(DffmTrainState), c_void_p,
+                                     c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p,
+                                     c_void_p, c_void_p, c_void_p]),
+    "dffm_hogwild_max_workers": (c_int32, [POINTER(DffmModel), c_int32]),
     "fwq_minmax": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "fwq_header": (c_int32, [c_float, c_float, c_int32, c_int32, POINTER(c_float),
                              POINTER(c_float)]),
@@ -116,7 +120,9 @@ def raise_status(word: int, what: str = "", base: int = 0) -> None:
         raise errors.NumericError(f"{what}non-finite value in {block} block (example {example})",
                                   block=block, example=example)
     if code == CONTRACT:
-        raise errors.ContractError(f"{what}contract violation at example {example}")
+        exc = errors.ContractError(f"{what}contract violation at example {example}")
+        exc.example = example
+        raise exc
     raise errors.FieldwiseError(f"{what}device status {word:#x}")
 
 

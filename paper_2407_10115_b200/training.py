@@ -6,6 +6,8 @@ example by example, batch size 1) inside ONE persistent kernel (K2,
 csrc/train.cu) over a resident batch of examples; the host only feeds chunks
 and folds the returned probabilities into the progressive metrics.
 ``evaluate_stream`` is the score-only loop (T:221-236) over K1.
+``hogwild_train`` is the lock-free parallel mode (T:242-336) as K6: n_threads
+concurrent GPU workers sharing the store.
 """
 
 from __future__ import annotations
@@ -18,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ContractError, TrainAborted
+from .errors import ContractError, FieldwiseError, HogwildWorkerError, TrainAborted
 from .features import pack_examples
 from .metrics import StreamingEvaluator, window_auc
 from .model import WeightStore, _as_device, _status, predict_batch
@@ -83,6 +85,20 @@ class _Trainer:
         nbytes = int(_lib.lib().dffm_train_scratch_bytes(store.c_model_ref(), max_per_field))
         self.scratch = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=store.device)
 
+    def run_hogwild(self, idx, val, labels, prob_out, n_workers: int):
+        import ctypes
+        st = _status(self.store.device)
+        s = torch.cuda.current_stream(self.store.device)
+        st.clear()
+        rc = _lib.lib().dffm_train_hogwild(
+            self.store.c_model_ref(), ctypes.byref(self.ts), idx.data_ptr(), val.data_ptr(),
+            labels.data_ptr(), self.M, idx.shape[0], n_workers, prob_out.data_ptr(),
+            self.scratch.data_ptr(), st.ptr(), s.cuda_stream)
+        _lib.check(rc, "dffm_train_hogwild")
+        st.fetch_async()
+        s.synchronize()
+        st.raise_if_set("hogwild worker: ")
+
     def run(self, idx: torch.Tensor, val: torch.Tensor, labels: torch.Tensor,
             prob_out: torch.Tensor, check=True):
         import ctypes
@@ -146,6 +162,58 @@ def train_stream(examples, store: WeightStore, opts: TrainOptions | None = None)
     """train_stream over ParsedExample-like objects (T:188-218)."""
     idx, val, labels = pack_examples(list(examples), store.config.n_fields)
     return train_sequential(idx, val, labels, store, opts)
+
+
+def max_hogwild_workers(store: WeightStore, max_per_field: int) -> int:
+    """Workers K6 can run concurrently on this GPU for this model shape."""
+    return int(_lib.lib().dffm_hogwild_max_workers(store.c_model_ref(), max_per_field))
+
+
+def hogwild_train(idx, val, labels, store: WeightStore, opts: TrainOptions | None = None
+                  ) -> TrainReport:
+    """Lock-free parallel single pass (T:269-336) over padded arrays.
+
+    ``opts.n_threads`` workers run the predict-then-learn loop concurrently
+    against the SHARED store with no locks (worker w takes examples w,
+    w + n, ...); concurrent updates may overwrite each other (T:1-11).
+    Progressive metrics are computed over every example's pre-update
+    prediction; the rolling AUC series is reported only for one worker, where
+    the run is the sequential schedule itself (identical to train_stream).
+    A failing worker stops the pool and surfaces as HogwildWorkerError."""
+    opts = opts or TrainOptions()
+    n_workers = int(opts.n_threads)
+    if n_workers == 1:
+        try:
+            return train_sequential(idx, val, labels, store, opts)
+        except FieldwiseError as exc:
+            raise HogwildWorkerError(f"worker 0 failed: {exc}", worker_id=0) from exc
+    ev = StreamingEvaluator(opts.eval_window)
+    start = time.perf_counter()
+    dev = store.device
+    n = int(idx.shape[0])
+    M = int(idx.shape[2])
+    trainer = _Trainer(store, M, opts.sparse_updates)
+    probs = np.empty(n)
+    for c0 in range(0, n, opts.chunk):
+        c1 = min(n, c0 + opts.chunk)
+        ci = _as_device(idx[c0:c1], torch.int32, dev)
+        cv = _as_device(val[c0:c1], torch.float32, dev)
+        cl = _as_device(labels[c0:c1], torch.uint8, dev)
+        po = torch.empty(c1 - c0, dtype=torch.float64, device=dev)
+        try:
+            trainer.run_hogwild(ci, cv, cl, po, n_workers)
+        except FieldwiseError as exc:
+            store.mark_mutated()  # T:318: the workers' own bumps are not visible
+            ex = getattr(exc, "example", None)
+            wid = int(ex) % n_workers if ex is not None else -1
+            raise HogwildWorkerError(f"worker {wid} failed: {exc}", worker_id=wid) from exc
+        probs[c0:c1] = po.cpu().numpy()
+    store.mark_mutated()  # T:318
+    y = np.asarray(labels.cpu() if isinstance(labels, torch.Tensor) else labels)
+    ev.add_batch(probs, y)
+    rep = _report(ev, start, probs)
+    rep.rolling_auc_series = []
+    return rep
 
 
 def backward_update(state, example, label: int, store: WeightStore, sparse: bool = True) -> float:
