@@ -564,14 +564,22 @@ def bench_adagrad(args, dev, clk_index=0):
     labels = (torch.rand(n, generator=gen, device=dev) < p).to(torch.uint8)
     del teacher, p
     torch.cuda.empty_cache()
-    st = WeightStore(cfg, dev)
-    gen.manual_seed(wl.weight_seed)
-    for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
-        flat = t.view(-1)
-        for c0 in range(0, flat.numel(), 1 << 28):
-            c1 = min(flat.numel(), c0 + (1 << 28))
-            flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=dev) * wl.weight_scale)
+
+    def student():
+        st = WeightStore(cfg, dev)
+        gen.manual_seed(wl.weight_seed)
+        for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
+            flat = t.view(-1)
+            for c0 in range(0, flat.numel(), 1 << 28):
+                c1 = min(flat.numel(), c0 + (1 << 28))
+                flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=dev) * wl.weight_scale)
+        return st
+
+    st = student()
     warm = min(2000, n // 10)
+    # CPU baseline first (the oracle's own sequential loop on one core, over the
+    # touched rows of a bounded prefix -- the same rows the GPU then trains)
+    cpu = adagrad_cpu_baseline(st, idx[:warm], val[:warm], labels[:warm], cfg)
     train_sequential(idx[:warm], val[:warm], labels[:warm], st, TrainOptions())
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -583,12 +591,72 @@ def bench_adagrad(args, dev, clk_index=0):
         torch.cuda.synchronize()
     ms = s.elapsed_time(e)
     done = n - warm
+    del st
+    torch.cuda.empty_cache()
+    # K6: the same prefix through the Hogwild trainer with every worker the GPU
+    # holds at once (T:269-336); logloss compared with the sequential run above
+    from paper_2407_10115_b200.training import hogwild_train, max_hogwild_workers
+    sh = student()
+    w = max_hogwild_workers(sh, idx.shape[2])
+    hogwild_train(idx[:warm], val[:warm], labels[:warm], sh, TrainOptions(n_threads=w))
+    torch.cuda.synchronize()
+    hs, he = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hs.record()
+    hrep = hogwild_train(idx[warm:], val[warm:], labels[warm:], sh,
+                         TrainOptions(n_threads=w, chunk=1 << 22))
+    he.record()
+    torch.cuda.synchronize()
+    hms = hs.elapsed_time(he)
     return {"value": done / (ms / 1e3), "unit": "examples/s", "examples": done,
             "us_per_example": 1e3 * ms / done, "progressive_logloss": rep.progressive_logloss,
             "workload": f"{wl.name} prefix ({done} of {wl.n_examples} examples, exact "
                         "sequential schedule, batch size 1)",
             "dtype": "f64 arithmetic, f32 storage", "gpu_launches": -(-done // (1 << 22)),
-            "clocks": clk.summary()}
+            "clocks": clk.summary(), "cpu_baseline": cpu,
+            "hogwild": {"value": done / (hms / 1e3), "unit": "examples/s", "workers": w,
+                        "progressive_logloss": hrep.progressive_logloss,
+                        "logloss_rel_diff_vs_sequential":
+                            abs(hrep.progressive_logloss - rep.progressive_logloss)
+                            / rep.progressive_logloss,
+                        "contract": "S:204 within 2% relative of the N=1 run"}}
+
+
+def adagrad_cpu_baseline(st, idx, val, labels, cfg, budget_s=8.0):
+    """The oracle's sequential predict-then-learn loop (T:172-185 restated,
+    numpy f64) on one host core over a bounded prefix, against a compact copy
+    of the touched rows (monotone remap)."""
+    from oracle import fieldwise_oracle as fo
+    ih = idx.cpu().numpy()
+    u = np.unique(ih[ih >= 0])
+    bits = max(1, math.ceil(math.log2(max(len(u), 2))))
+    ost = fo.OracleStore.zeros(cfg.n_fields, cfg.k, cfg.hidden_sizes, bits)
+    import torch
+    ut = torch.as_tensor(u, dtype=torch.int64, device=st.device)
+    ost.lr[: len(u)] = st.lr[ut].cpu().numpy()
+    ost.lr[ost.n_features] = st.lr[-1].item()
+    ost.ffm[: len(u)] = st.ffm[ut].cpu().numpy()
+    ost.lr_acc[: len(u)] = st.lr_acc[ut].cpu().numpy()
+    ost.lr_acc[ost.n_features] = st.lr_acc[-1].item()
+    ost.ffm_acc[: len(u)] = st.ffm_acc[ut].cpu().numpy()
+    for i, ((w, b), (wa, ba)) in enumerate(zip(st.nn_layers, st.nn_accs)):
+        ost.layers[i][0][:] = w.cpu().numpy()
+        ost.layers[i][1][:] = b.cpu().numpy()
+        ost.layer_accs[i][0][:] = wa.cpu().numpy()
+        ost.layer_accs[i][1][:] = ba.cpu().numpy()
+    ridx = np.where(ih >= 0, np.searchsorted(u, np.maximum(ih, 0)), -1).astype(np.int32)
+    vh, lh = val.cpu().numpy(), labels.cpu().numpy()
+    t0 = time.perf_counter()
+    fo.train_sequential(ridx[:16], vh[:16], lh[:16], ost.copy(), cfg.lr_ffm, cfg.lr_lr,
+                        cfg.lr_nn, cfg.power_t)
+    per = (time.perf_counter() - t0) / 16
+    m = int(min(len(ih), max(16, budget_s / per)))
+    t0 = time.perf_counter()
+    fo.train_sequential(ridx[:m], vh[:m], lh[:m], ost, cfg.lr_ffm, cfg.lr_lr, cfg.lr_nn,
+                        cfg.power_t)
+    wall = time.perf_counter() - t0
+    return {"value": m / wall, "unit": "examples/s", "cores": 1, "kind": "port",
+            "sample": f"first {m} examples of the timed stream, oracle sequential "
+                      "predict-then-learn (the reference schedule is single-threaded)"}
 
 
 def cpu_baseline(st, idx, val, prob, wl, budget_s=12.0):
