@@ -67,9 +67,11 @@ def test_train_matches_oracle_cfg3_shape_with_duplicates():
     assert nbad == 0, f"{nbad} slots outside tolerance ({same:.4%} bit-identical)"
 
 
-def test_train_full_size_table_prefix():
-    """BASELINE cfg3 at full size (2^24 buckets): a 2,000-example prefix on the
-    GPU vs the oracle on the remapped touched rows."""
+@pytest.mark.parametrize("n", [2000, pytest.param(20000, marks=pytest.mark.slow)])
+def test_train_full_size_table_prefix(n):
+    """BASELINE cfg3 at full size (2^24 buckets): an n-example prefix on the GPU
+    vs the oracle on the remapped touched rows (touched rows after
+    a 20k prefix, |dw| <= 1e-5 max(|w|, 1e-3); progressive logloss per window)."""
     wl = configs.CFG3
     cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=24, lr_ffm=0.1,
                       lr_lr=0.1, lr_nn=0.1, power_t=0.5)
@@ -80,7 +82,6 @@ def test_train_full_size_table_prefix():
     for w, b in st.nn_layers:
         w.copy_(torch.randn(w.shape, generator=gen, device=DEV) * 0.05)
         b.copy_(torch.randn(b.shape, generator=gen, device=DEV) * 0.05)
-    n = 2000
     idx, val = synth.make_examples(wl, n, device=DEV)
     labels = synth.make_labels(n, 0.3, 5, device=DEV)
     ih, vh, lh = idx.cpu().numpy(), val.cpu().numpy(), labels.cpu().numpy()
@@ -95,6 +96,17 @@ def test_train_full_size_table_prefix():
                           ost.lr[:len(u)], ost.lr_acc[:len(u)]])
     nbad, same = close_weights(got, ref)
     assert nbad == 0, f"{nbad} touched slots outside tolerance ({same:.4%} bit-identical)"
+    got_mlp = np.concatenate([x.cpu().numpy().ravel() for wb in st.nn_layers for x in wb])
+    ref_mlp = np.concatenate([x.ravel() for wb in ost.layers for x in wb])
+    nbad, _ = close_weights(got_mlp, ref_mlp)
+    assert nbad == 0, f"{nbad} MLP slots outside tolerance"
+    # progressive logloss per window (Me:118-125), 1e-6 relative
+    y = lh.astype(np.int64)
+    lg = np.where(y == 1, -np.log(rep.probs), -np.log1p(-rep.probs))
+    lo = np.where(y == 1, -np.log(probs), -np.log1p(-probs))
+    w = max(500, n // 4)
+    for a in range(0, n, w):
+        assert abs(lg[a:a + w].mean() - lo[a:a + w].mean()) <= 1e-6 * lo[a:a + w].mean()
 
 
 def test_train_bad_label_is_contract_error_and_stops():
