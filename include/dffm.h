@@ -190,6 +190,34 @@ int fwq_dequantize(const uint16_t* q, int64_t n, float hmin, float hbucket, floa
 int fw_hash_fnv1a32(const uint8_t* bytes, const int64_t* offsets, int64_t n, int32_t bits,
                     uint32_t* out, void* stream);
 
+/*
+ * K7 FWP1 byte patches (file format S:381; no reference code).
+ * create (device buffers old[old_len], new[new_len]):
+ *   fwp_diff_count  -> number of ops (scratch: fwp_scratch_bytes(new_len) B)
+ *   fwp_diff_ops    -> ordered op ranges [starts[k], ends[k]) into new
+ *   fwp_encode_size -> offsets[k] of each op in the op stream, total bytes
+ *   fwp_encode      -> the op stream: varint(skip) varint(length) payload ...
+ * apply: fwp_parse_ops (HOST: the op headers are serial by format) then
+ *   fwp_scatter (device payload copy into the target buffer).
+ * fw_fnv1a64_host: the FNV-1a 64 digest of the header, host bytes.
+ * fwp_diff_count / fwp_encode_size synchronise `stream` to return a count.
+ */
+int64_t fwp_scratch_bytes(int64_t new_len);
+int fwp_diff_count(const uint8_t* old_, int64_t old_len, const uint8_t* new_, int64_t new_len,
+                   void* scratch, int64_t* n_ops_host, void* stream);
+int fwp_diff_ops(const uint8_t* old_, int64_t old_len, const uint8_t* new_, int64_t new_len,
+                 const void* scratch, int64_t* starts, int64_t* ends, void* stream);
+int fwp_encode_size(const int64_t* starts, const int64_t* ends, int64_t n_ops,
+                    int64_t* offsets, void* scratch, int64_t* total_host, void* stream);
+int fwp_encode(const uint8_t* new_, const int64_t* starts, const int64_t* ends,
+               const int64_t* offsets, int64_t n_ops, uint8_t* out, void* stream);
+int fwp_parse_ops(const uint8_t* ops_host, int64_t ops_len, int64_t target_len,
+                  int64_t* dst_off_host, int64_t* src_off_host, int64_t* len_host,
+                  int64_t max_ops, int64_t* n_ops_out);
+int fwp_scatter(uint8_t* dst, const uint8_t* src, const int64_t* dst_off, const int64_t* src_off,
+                const int64_t* len, int64_t n_ops, void* stream);
+uint64_t fw_fnv1a64_host(const uint8_t* data_host, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -621,3 +621,136 @@ def fnv1a32_batch(blob: np.ndarray, offsets: np.ndarray) -> np.ndarray:
         b = blob[offsets[:-1][live] + pos].astype(np.uint64)
         h[live] = ((h[live] ^ b) * np.uint64(FNV32_PRIME)) & np.uint64(0xFFFFFFFF)
     return h.astype(np.uint32)
+
+
+# --------------------------------------------------------------------------
+# weight transfer: varints and FWP1 byte patches (SPEC S:329-353, S:358-362,
+# S:381-382).  No reference code exists; pinned by the SPEC examples
+# and the declared choices below:
+#   * FWP1 header = magic, version u32 (= 1), source digest u64, target
+#     digest u64, target length u64, all little-endian
+#   * digest = FNV-1a 64 over the full byte content
+#   * a byte at offset i < len(new) differs if i >= len(old) or old[i] != new[i];
+#     differing runs separated by fewer than GAP_MERGE = 4 identical bytes are
+#     merged into one op; `skip` is relative to the END of the
+#     previous op (0 for the first), `length` counts payload bytes
+#   * apply: output = old[:target_length] zero-extended, ops written in order
+# --------------------------------------------------------------------------
+
+FNV64_OFFSET = 0xCBF29CE484222325
+FNV64_PRIME = 0x100000001B3
+PATCH_MAGIC = b"FWP1"
+PATCH_VERSION = 1
+GAP_MERGE = 4
+
+
+class OracleFormatError(Exception):
+    pass
+
+
+class OracleStaleBaseError(Exception):
+    pass
+
+
+class OracleCorruptionError(Exception):
+    pass
+
+
+def fnv1a64(data) -> int:
+    h = FNV64_OFFSET
+    for b in bytes(data):
+        h = ((h ^ b) * FNV64_PRIME) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def encode_varint(n: int) -> bytes:
+    """LEB128: 7-bit groups, little-endian, high bit = continuation."""
+    if n < 0 or n >= 1 << 64:
+        raise ValueError("varint out of range")
+    out = bytearray()
+    while True:
+        b = n & 0x7F
+        n >>= 7
+        if n:
+            out.append(b | 0x80)
+        else:
+            out.append(b)
+            return bytes(out)
+
+
+def decode_varint(buf, pos: int = 0):
+    """-> (value, bytes consumed); more than 10 bytes or truncation is a format error."""
+    n = 0
+    shift = 0
+    for i in range(10):
+        if pos + i >= len(buf):
+            raise OracleFormatError("truncated varint")
+        b = buf[pos + i]
+        n |= (b & 0x7F) << shift
+        if not b & 0x80:
+            if n >= 1 << 64:
+                raise OracleFormatError("varint overflow")
+            return n, i + 1
+        shift += 7
+    raise OracleFormatError("varint longer than 10 bytes")
+
+
+def diff_ops(old, new):
+    """Ordered (start, end_exclusive) ranges of the ops create_patch emits."""
+    old = np.frombuffer(bytes(old), np.uint8)
+    new = np.frombuffer(bytes(new), np.uint8)
+    m = min(len(old), len(new))
+    d = np.ones(len(new), bool)
+    d[:m] = old[:m] != new[:m]
+    pos = np.flatnonzero(d)
+    if len(pos) == 0:
+        return []
+    gaps = np.diff(pos) - 1
+    cut = np.flatnonzero(gaps >= GAP_MERGE)
+    starts = np.concatenate([[pos[0]], pos[cut + 1]])
+    ends = np.concatenate([pos[cut], [pos[-1]]]) + 1
+    return list(zip(starts.tolist(), ends.tolist()))
+
+
+def create_patch(old, new) -> bytes:
+    old, new = bytes(old), bytes(new)
+    out = bytearray(PATCH_MAGIC)
+    out += int(PATCH_VERSION).to_bytes(4, "little")
+    out += fnv1a64(old).to_bytes(8, "little") + fnv1a64(new).to_bytes(8, "little")
+    out += len(new).to_bytes(8, "little")
+    prev = 0
+    for a, b in diff_ops(old, new):
+        out += encode_varint(a - prev) + encode_varint(b - a) + new[a:b]
+        prev = b
+    return bytes(out)
+
+
+def apply_patch(old, patch) -> bytes:
+    old, patch = bytes(old), bytes(patch)
+    if len(patch) < 32 or patch[:4] != PATCH_MAGIC:
+        raise OracleFormatError("not a patch")
+    if int.from_bytes(patch[4:8], "little") != PATCH_VERSION:
+        raise OracleFormatError("unsupported patch version")
+    src = int.from_bytes(patch[8:16], "little")
+    dst = int.from_bytes(patch[16:24], "little")
+    tlen = int.from_bytes(patch[24:32], "little")
+    if fnv1a64(old) != src:
+        raise OracleStaleBaseError("source digest mismatch")
+    out = bytearray(old[:tlen]) + bytearray(max(0, tlen - len(old)))
+    pos, cur = 32, 0
+    while pos < len(patch):
+        skip, c1 = decode_varint(patch, pos)
+        pos += c1
+        ln, c2 = decode_varint(patch, pos)
+        pos += c2
+        start = cur + skip
+        if start + ln > tlen:
+            raise OracleFormatError("op overruns target length")
+        if pos + ln > len(patch):
+            raise OracleFormatError("truncated payload")
+        out[start:start + ln] = patch[pos:pos + ln]
+        pos += ln
+        cur = start + ln
+    if fnv1a64(out) != dst:
+        raise OracleCorruptionError("target digest mismatch")
+    return bytes(out)

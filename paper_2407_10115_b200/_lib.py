@@ -70,6 +70,18 @@ SIGNATURES = {
     "fwq_quantize": (c_int32, [c_void_p, c_int64, c_float, c_float, c_void_p, c_void_p]),
     "fwq_dequantize": (c_int32, [c_void_p, c_int64, c_float, c_float, c_void_p, c_void_p]),
     "fw_hash_fnv1a32": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    "fwp_scratch_bytes": (c_int64, [c_int64]),
+    "fwp_diff_count": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, POINTER(c_int64),
+                                 c_void_p]),
+    "fwp_diff_ops": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                               c_void_p]),
+    "fwp_encode_size": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                  POINTER(c_int64), c_void_p]),
+    "fwp_encode": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "fwp_parse_ops": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
+                                POINTER(c_int64)]),
+    "fwp_scatter": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+    "fw_fnv1a64_host": (c_uint64, [c_void_p, c_int64]),
 }
 
 _lib = None

@@ -187,3 +187,34 @@ def test_quant_roundtrip_bound_and_monotone():
     assert err[inner].max() <= hb / 2 + slack
     order = np.argsort(w, kind="stable")
     assert (np.diff(q[order].astype(np.int64)) >= 0).all()
+
+
+# ------------------------------------------------------------------ transfer
+
+
+def test_oracle_varint_and_patch_spec_examples():
+    assert fo.encode_varint(0) == b"\x00"
+    assert fo.encode_varint(127) == b"\x7f"
+    assert fo.encode_varint(128) == b"\x80\x01"
+    rng = np.random.default_rng(0)
+    for v in rng.integers(0, 2**63, 2000).tolist() + [2**64 - 1]:
+        e = fo.encode_varint(v)
+        assert fo.decode_varint(e) == (v, len(e))
+    p = fo.create_patch(bytes([1, 2, 3, 4]), bytes([1, 2, 9, 4]))
+    assert p[32:] == bytes([2, 1, 9])
+    assert fo.apply_patch(bytes([1, 2, 3, 4]), p) == bytes([1, 2, 9, 4])
+    assert len(fo.create_patch(b"xyz", b"xyz")) == 32
+    # gap rule: runs 3 identical bytes apart merge, 4 apart do not
+    assert fo.diff_ops(b"aaaaaaaaaa", b"Xaaa" + b"Xaaaaa") == [(0, 5)]
+    assert fo.diff_ops(b"aaaaaaaaaa", b"Xaaaa" + b"Xaaaa") == [(0, 1), (5, 6)]
+
+
+def test_host_digest_and_varints_match_oracle():
+    from paper_2407_10115_b200 import transfer
+    rng = np.random.default_rng(1)
+    for n in (0, 1, 7, 1000):
+        b = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        assert transfer.digest(b) == fo.fnv1a64(b)
+    for v in (0, 1, 127, 128, 300, 2**35 + 7, 2**64 - 1):
+        assert transfer.encode_varint(v) == fo.encode_varint(v)
+        assert transfer.decode_varint(transfer.encode_varint(v)) == (v, len(fo.encode_varint(v)))
