@@ -243,3 +243,68 @@ def test_forward_cfg2_full_table_sample():
     perm = torch.randperm(1 << 20, device=DEV)
     p2 = predict_batch(idx[perm], val[perm], st)
     assert torch.equal(p2, p[perm])
+
+
+def _full_store(wl):
+    """Seeded on-device table of the workload's full size (as bench.build_store)."""
+    cfg = ModelConfig(n_fields=wl.n_fields, k=wl.k, hidden_sizes=wl.hidden, hash_bits=wl.hash_bits)
+    st = WeightStore(cfg, DEV, "bf16" if wl.weight_dtype == "bf16" else "f32",
+                     with_optimizer=False)
+    gen = torch.Generator(device=DEV).manual_seed(wl.weight_seed)
+    for t in (st.lr, st.ffm):
+        flat = t.view(-1)
+        for c0 in range(0, flat.numel(), 1 << 28):
+            c1 = min(flat.numel(), c0 + (1 << 28))
+            flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=DEV) * wl.weight_scale)
+    for w, b in st.nn_layers:
+        w.copy_(torch.randn(w.shape, generator=gen, device=DEV) * wl.weight_scale)
+        b.copy_(torch.randn(b.shape, generator=gen, device=DEV) * wl.weight_scale)
+    return st
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg1", "cfg5"])
+def test_forward_full_size_config_sample(name):
+    """BASELINE cfg1 (whole 65,536 batch) and cfg5 (2^25 buckets, 43 GB bf16
+    table, 8,388,608 examples; 4,096 sampled) against the oracle."""
+    wl = {"cfg1": configs.CFG1, "cfg5": configs.CFG5}[name]
+    st = _full_store(wl)
+    cdf = synth.zipf_cdf(1 << wl.hash_bits, wl.zipf_alpha, DEV) if wl.dist == "zipf" else None
+    idx, val = synth.make_examples(wl, wl.n_examples, device=DEV, cdf=cdf)
+    del cdf
+    p = predict_batch(idx, val, st)
+    assert torch.isfinite(p).all()
+    n = idx.shape[0]
+    sel = torch.randperm(n, generator=torch.Generator().manual_seed(1))[: min(n, 4096)]
+    si, sv = idx[sel.to(DEV)].cpu().numpy(), val[sel.to(DEV)].cpu().numpy()
+    cst, ridx, _ = compact_oracle(st, si)
+    _, ref = fo.forward_batch(ridx, sv, cst)
+    assert rel_err(p[sel.to(DEV)].double().cpu().numpy(), ref).max() < RTOL
+
+
+@pytest.mark.slow
+def test_context_cache_full_size_cfg4_sample():
+    """BASELINE cfg4 at full size: u16-quantised 2^24 tables, 2,000 requests x
+    500 candidates through K3; 4,096 sampled candidates vs the oracle on the
+    merged examples."""
+    from paper_2407_10115_b200 import inference
+    from paper_2407_10115_b200.quant import quantize_store
+    wl = configs.CFG4
+    st, _ = quantize_store(_full_store(wl))
+    torch.cuda.empty_cache()
+    R, C, Fc = wl.n_requests, wl.n_candidates, wl.ctx_fields
+    cdf = synth.zipf_cdf(1 << wl.hash_bits, wl.zipf_alpha, DEV)
+    ci, cv = synth.make_examples(wl, R, seed=wl.data_seed, device=DEV, cdf=cdf, n_fields=Fc)
+    di, dv = synth.make_examples(wl, R * C, seed=wl.data_seed + 1, device=DEV, cdf=cdf,
+                                 n_fields=wl.n_fields - Fc, field_offset=Fc)
+    di, dv = di.view(R, C, wl.n_fields - Fc, -1), dv.view(R, C, wl.n_fields - Fc, -1)
+    p = inference.score_requests(ci, cv, di, dv, st)
+    g = torch.Generator().manual_seed(2)
+    rr = torch.randint(0, R, (4096,), generator=g)
+    cc = torch.randint(0, C, (4096,), generator=g)
+    mi = torch.cat([ci[rr.to(DEV)], di[rr.to(DEV), cc.to(DEV)]], 1).cpu().numpy()
+    mv = torch.cat([cv[rr.to(DEV)], dv[rr.to(DEV), cc.to(DEV)]], 1).cpu().numpy()
+    cst, ridx, _ = compact_oracle(st, mi)
+    _, ref = fo.forward_batch(ridx, mv, cst)
+    got = p[rr.to(DEV), cc.to(DEV)].double().cpu().numpy()
+    assert rel_err(got, ref).max() < RTOL
