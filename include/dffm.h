@@ -218,6 +218,18 @@ int fwp_scatter(uint8_t* dst, const uint8_t* src, const int64_t* dst_off, const 
                 const int64_t* len, int64_t n_ops, void* stream);
 uint64_t fw_fnv1a64_host(const uint8_t* data_host, int64_t n);
 
+/*
+ * K8 streaming evaluator: replaces StreamingEvaluator (Me:109-129) and
+ * window_auc (Me:21-34) over a device stream.  probs f64 [n] (clamped
+ * progressive predictions), labels u8 [n] in {0,1}.  Non-overlapping windows:
+ *   auc_out[n / window]            midrank (Mann-Whitney) AUC, NaN if one class
+ *   loss_out[ceil(n / window)]     per-window sums of clamped log-losses
+ *                                  (the last partial when window does not divide n)
+ * window in [2, 57344].
+ */
+int fw_eval_stream(const double* probs, const uint8_t* labels, int64_t n, int32_t window,
+                   double* auc_out, double* loss_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,8 @@ SIGNATURES = {
                                 POINTER(c_int64)]),
     "fwp_scatter": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "fw_fnv1a64_host": (c_uint64, [c_void_p, c_int64]),
+    "fw_eval_stream": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
+                                 c_void_p]),
 }
 
 _lib = None

@@ -71,6 +71,36 @@ def rig(pairs) -> float:
     return 1.0 - logloss(pairs) / entropy
 
 
+def stream_metrics_gpu(probs, labels, window: int = 30000):
+    """K8 (csrc/eval.cu): the StreamingEvaluator result for a whole device
+    stream -> (auc_series [(count, auc | None)], loss_sum, count).  AUC is the
+    exact Mann-Whitney count per window (same value as the midrank formula);
+    per-window loss sums are folded in stream order on the host."""
+    import torch
+
+    from . import _lib
+    if window < 2:
+        raise ContractError("window capacity must be >= 2")
+    p = probs.detach().reshape(-1).to(torch.float64).contiguous()
+    y = labels.detach().reshape(-1).to(device=p.device, dtype=torch.uint8).contiguous()
+    n = p.numel()
+    if n == 0:
+        return [], 0.0, 0
+    n_full, n_win = n // window, -(-n // window)
+    auc = torch.empty(max(n_full, 1), dtype=torch.float64, device=p.device)
+    loss = torch.empty(n_win, dtype=torch.float64, device=p.device)
+    _lib.check(_lib.lib().fw_eval_stream(p.data_ptr(), y.data_ptr(), n, window, auc.data_ptr(),
+                                         loss.data_ptr(),
+                                         torch.cuda.current_stream(p.device).cuda_stream),
+               "fw_eval_stream")
+    a = auc.cpu().numpy()[:n_full]
+    series = [((i + 1) * window, None if math.isnan(v) else float(v)) for i, v in enumerate(a)]
+    total = 0.0
+    for v in loss.cpu().numpy().tolist():
+        total += v
+    return series, total, n
+
+
 class StreamingEvaluator:
     """Progressive-validation accumulator (Me:109-129), batch-fed.
 

@@ -22,7 +22,7 @@ import torch
 from . import _lib
 from .errors import ContractError, FieldwiseError, HogwildWorkerError, TrainAborted
 from .features import pack_examples
-from .metrics import StreamingEvaluator, window_auc
+from .metrics import StreamingEvaluator, stream_metrics_gpu, window_auc
 from .model import WeightStore, _as_device, _status, predict_batch
 
 DEFAULT_EVAL_WINDOW = 30000  # T:31
@@ -123,6 +123,7 @@ def train_sequential(idx, val, labels, store: WeightStore, opts: TrainOptions | 
 
     idx int32 [n,F,M], val f32 [n,F,M], labels uint8 [n] (host or device)."""
     opts = opts or TrainOptions()
+    gpu_eval = evaluator is None  # K8 on the device stream unless the caller keeps state
     ev = evaluator or StreamingEvaluator(opts.eval_window)
     start = time.perf_counter()
     dev = store.device
@@ -130,6 +131,7 @@ def train_sequential(idx, val, labels, store: WeightStore, opts: TrainOptions | 
     M = int(idx.shape[2])
     trainer = _Trainer(store, M, opts.sparse_updates)
     probs = np.empty(n)
+    dprobs, dlabels = [], []
     for c0 in range(0, n, opts.chunk):
         c1 = min(n, c0 + opts.chunk)
         ci = _as_device(idx[c0:c1], torch.int32, dev)
@@ -146,9 +148,27 @@ def train_sequential(idx, val, labels, store: WeightStore, opts: TrainOptions | 
         store.version += c1 - c0  # one bump per example (M:532)
         p = po.cpu().numpy()
         probs[c0:c1] = p
-        ev.add_batch(p, np.asarray(labels[c0:c1].cpu() if isinstance(labels, torch.Tensor)
-                                   else labels[c0:c1]))
+        if gpu_eval:
+            dprobs.append(po)
+            dlabels.append(cl)
+        else:
+            ev.add_batch(p, np.asarray(labels[c0:c1].cpu() if isinstance(labels, torch.Tensor)
+                                       else labels[c0:c1]))
+    if gpu_eval:
+        return _report_gpu(dprobs, dlabels, opts.eval_window, start, probs)
     return _report(ev, start, probs)
+
+
+def _report_gpu(dprobs, dlabels, window, start, probs, with_auc=True):
+    if dprobs:
+        series, loss_sum, count = stream_metrics_gpu(torch.cat(dprobs), torch.cat(dlabels), window)
+    else:
+        series, loss_sum, count = [], 0.0, 0
+    wall = time.perf_counter() - start
+    return TrainReport(examples_seen=count,
+                       progressive_logloss=loss_sum / count if count else float("nan"),
+                       rolling_auc_series=series if with_auc else [], wall_time=wall,
+                       throughput=count / wall if wall > 0 else 0.0, probs=probs)
 
 
 def _report(ev, start, probs):
@@ -187,13 +207,13 @@ def hogwild_train(idx, val, labels, store: WeightStore, opts: TrainOptions | Non
             return train_sequential(idx, val, labels, store, opts)
         except FieldwiseError as exc:
             raise HogwildWorkerError(f"worker 0 failed: {exc}", worker_id=0) from exc
-    ev = StreamingEvaluator(opts.eval_window)
     start = time.perf_counter()
     dev = store.device
     n = int(idx.shape[0])
     M = int(idx.shape[2])
     trainer = _Trainer(store, M, opts.sparse_updates)
     probs = np.empty(n)
+    dprobs, dlabels = [], []
     for c0 in range(0, n, opts.chunk):
         c1 = min(n, c0 + opts.chunk)
         ci = _as_device(idx[c0:c1], torch.int32, dev)
@@ -208,12 +228,10 @@ def hogwild_train(idx, val, labels, store: WeightStore, opts: TrainOptions | Non
             wid = int(ex) % n_workers if ex is not None else -1
             raise HogwildWorkerError(f"worker {wid} failed: {exc}", worker_id=wid) from exc
         probs[c0:c1] = po.cpu().numpy()
+        dprobs.append(po)
+        dlabels.append(cl)
     store.mark_mutated()  # T:318
-    y = np.asarray(labels.cpu() if isinstance(labels, torch.Tensor) else labels)
-    ev.add_batch(probs, y)
-    rep = _report(ev, start, probs)
-    rep.rolling_auc_series = []
-    return rep
+    return _report_gpu(dprobs, dlabels, opts.eval_window, start, probs, with_auc=False)
 
 
 def backward_update(state, example, label: int, store: WeightStore, sparse: bool = True) -> float:
