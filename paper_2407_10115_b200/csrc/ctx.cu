@@ -35,6 +35,7 @@ struct CtxParams {
   int Fc, Mc, Fd, Md;
   int64_t R;
   int C;
+  int cblk;  // candidates per work unit (a multiple of TE)
 };
 
 struct CtxSmem {
@@ -92,55 +93,66 @@ ctx_kernel(CtxParams q) {
   build_pairtab(pairtab, F);
   const float bias = load_elem<T>((const T*)p.lr + p.n_buckets, p.dlr);
 
-  for (int64_t r = blockIdx.x; r < q.R; r += gridDim.x) {
+  // work unit = (request, block of cblk candidates): balances the tail and
+  // keeps every SM busy when requests are few; the context cache is rebuilt
+  // only when a unit starts a different request
+  const int nub = (q.C + q.cblk - 1) / q.cblk;
+  const int64_t nunits = q.R * nub;
+  int64_t cached_r = -1;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t r = u / nub;
+    const int cbeg = (int)(u % nub) * q.cblk, cend = min(q.C, cbeg + q.cblk);
     __syncthreads();
-    // ---------------------------------------------- build_context_cache
-    if (warp == 0) {
-      int bad = 0;
-      const double lrs = stage_slots<T>(p, q.cidx + r * Fc * Mc, q.cval + r * Fc * Mc, Fc * Mc,
-                                        csidx, csval, lane, bad);
-      const double tot = warp_sum(lrs);
-      if (lane == 0) *lrp = tot;
-      if (__any_sync(0xffffffffu, bad) && lane == 0)
-        atomicMin((unsigned long long*)p.status,
-                  (unsigned long long)status_key(p.status_base + r * q.C, DFFM_BLOCK_NONE,
-                                                 DFFM_CONTRACT));
-    }
-    __syncthreads();
-    for (int x = threadIdx.x; x < Fc; x += FWD_THREADS) {
-      unsigned char pr = 0;
-      for (int m = 0; m < Mc; ++m) pr |= (csidx[x * Mc + m] >= 0);
-      cpres[x] = pr;
-    }
-    for (int t = threadIdx.x; t < Fc * F * k; t += FWD_THREADS) {
-      const int x = t / (F * k), gk = t % (F * k);
-      float acc = 0.f;
-      for (int m = 0; m < Mc; ++m) {
-        const int j = csidx[x * Mc + m];
-        if (j >= 0) acc = fmaf(csval[x * Mc + m], load_elem<T>(ffm + (int64_t)j * F * k + gk, p.dffm), acc);
+    if (r != cached_r) {
+      cached_r = r;
+      // ---------------------------------------------- build_context_cache
+      if (warp == 0) {
+        int bad = 0;
+        const double lrs = stage_slots<T>(p, q.cidx + r * Fc * Mc, q.cval + r * Fc * Mc, Fc * Mc,
+                                          csidx, csval, lane, bad);
+        const double tot = warp_sum(lrs);
+        if (lane == 0) *lrp = tot;
+        if (__any_sync(0xffffffffu, bad) && lane == 0)
+          atomicMin((unsigned long long*)p.status,
+                    (unsigned long long)status_key(p.status_base + r * q.C, DFFM_BLOCK_NONE,
+                                                   DFFM_CONTRACT));
       }
-      Sctx[t] = acc;
-    }
-    __syncthreads();
-    for (int pp = threadIdx.x; pp < P; pp += FWD_THREADS) {
-      const uint32_t pr = pairtab[pp];
-      const int f1 = pr & 0xFF, f2 = pr >> 8;
-      float pv = 0.f;
-      if (f2 < Fc && (cpres[f1] & cpres[f2])) {
-        const float* a = Sctx + (f1 * F + f2) * k;
-        const float* b = Sctx + (f2 * F + f1) * k;
-        for (int c = 0; c < k; ++c) pv = fmaf(a[c], b[c], pv);
+      __syncthreads();
+      for (int x = threadIdx.x; x < Fc; x += FWD_THREADS) {
+        unsigned char pr = 0;
+        for (int m = 0; m < Mc; ++m) pr |= (csidx[x * Mc + m] >= 0);
+        cpres[x] = pr;
       }
-      cpair[pp] = pv;
-    }
-    __syncthreads();
+      for (int t = threadIdx.x; t < Fc * F * k; t += FWD_THREADS) {
+        const int x = t / (F * k), gk = t % (F * k);
+        float acc = 0.f;
+        for (int m = 0; m < Mc; ++m) {
+          const int j = csidx[x * Mc + m];
+          if (j >= 0) acc = fmaf(csval[x * Mc + m], load_elem<T>(ffm + (int64_t)j * F * k + gk, p.dffm), acc);
+        }
+        Sctx[t] = acc;
+      }
+      __syncthreads();
+      for (int pp = threadIdx.x; pp < P; pp += FWD_THREADS) {
+        const uint32_t pr = pairtab[pp];
+        const int f1 = pr & 0xFF, f2 = pr >> 8;
+        float pv = 0.f;
+        if (f2 < Fc && (cpres[f1] & cpres[f2])) {
+          const float* a = Sctx + (f1 * F + f2) * k;
+          const float* b = Sctx + (f2 * F + f1) * k;
+          for (int c = 0; c < k; ++c) pv = fmaf(a[c], b[c], pv);
+        }
+        cpair[pp] = pv;
+      }
+      __syncthreads();
+    }  // cache for request r built
     const double lr_ctx = (double)bias + *lrp;
 
     // ---------------------------------------------- predict_batch
-    for (int c0 = 0; c0 < q.C; c0 += TE) {
+    for (int c0 = cbeg; c0 < cend; c0 += TE) {
       for (int el = warp; el < TE; el += FWD_WARPS) {
         const int cand = c0 + el;
-        if (cand >= q.C) { zero_column(X, exd, flag, el, TE, XS, D, lane); continue; }
+        if (cand >= cend) { zero_column(X, exd, flag, el, TE, XS, D, lane); continue; }
         const int64_t e = r * q.C + cand;
         int bad = 0;
         const double lrs = stage_slots<T>(p, q.didx + e * DM, q.dval + e * DM, DM, sidx, sval,
@@ -198,7 +210,7 @@ ctx_kernel(CtxParams q) {
         merge_finish(X, exd, flag, el, TE, XS, P, D, lane, lr_out, s1, pbad);
       }
       __syncthreads();
-      const int nvalid = (q.C - c0) < TE ? (q.C - c0) : TE;
+      const int nvalid = (cend - c0) < TE ? (cend - c0) : TE;
       mlp_tile(p, X, Ha, Hb, exd, flag, r * q.C + c0, nvalid);
     }
   }
@@ -225,10 +237,19 @@ static CtxKernel select_ctx(int K, int MU) {
 }
 
 static int launch_ctx(CtxKernel kern, const CtxParams& q, int smem, cudaStream_t s) {
+  {  // DFFM_CTX_SMEM_KB: pad the per-CTA shared memory (fewer CTAs per SM, more L1 for W)
+    static int pad = -1;
+    if (pad < 0) {
+      const char* v = getenv("DFFM_CTX_SMEM_KB");
+      pad = v ? atoi(v) * 1024 : 0;
+    }
+    if (pad > smem && pad <= max_smem_optin_current()) smem = pad;
+  }
   int occ = 0;
   int rc = kernel_occupancy((const void*)kern, FWD_THREADS, smem, &occ);
   if (rc) return rc;
-  const int64_t grid = std::min<int64_t>(q.R, (int64_t)sm_count_current() * occ);
+  const int64_t nunits = q.R * ((q.C + q.cblk - 1) / q.cblk);
+  const int64_t grid = std::min<int64_t>(nunits, (int64_t)sm_count_current() * occ);
   kern<<<(unsigned)grid, FWD_THREADS, smem, s>>>(q);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(ctx)");
   return DFFM_OK;
@@ -282,7 +303,15 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
   const bool use_tc = ctx_mlp && strcmp(ctx_mlp, "tc") == 0 && tc_eligible(p, smax);
   if (use_tc) p.hmax = 0;
   CtxSmem L;
-  int TE = 32;
+  static int te_env = -1, cblk_env = -1;
+  if (te_env < 0) {
+    const char* v = getenv("DFFM_CTX_TE");
+    te_env = v ? atoi(v) : 32;
+    if (te_env < 2 || te_env > 32 || (te_env & 1)) te_env = 32;
+    const char* c = getenv("DFFM_CTX_CBLK");
+    cblk_env = c ? atoi(c) : 128;
+  }
+  int TE = te_env;
   for (;; TE >>= 1) {
     p.TE = TE;
     p.XS = TE + 2;
@@ -293,6 +322,7 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
     set_error("context scorer needs %d B shared memory (> %d)", L.total, smax);
     return DFFM_SIZING;
   }
+  q.cblk = std::max(p.TE, cblk_env / p.TE * p.TE);
   const int K = pick_k_template(p.k, model->wdtype);
   const int MU = cand_m <= 4 ? cand_m : 0;
   CtxKernel kern = nullptr;
