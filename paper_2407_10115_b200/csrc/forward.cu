@@ -13,6 +13,7 @@
 #include "forward_g4.cuh"
 #include "mlp_tc.cuh"
 #include "forward_rowstage.cuh"
+#include "forward_rsw.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -37,6 +38,8 @@ int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int sme
                         cudaStream_t s);
 template <typename T>
 int launch_forward_rowstage_t(const FwdParams& p, int K, int NB, int smem, cudaStream_t s);
+template <typename T>
+int launch_forward_rsw_t(const FwdParams& p, const RswSmem& L, int K, cudaStream_t s);
 
 enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3, FAM_G4 = 4, FAM_TC = 5 };
 static int g_family = -1;  // set by env (first call) or dffm_set_forward_family()
@@ -324,6 +327,33 @@ static bool try_rowstage_forward(const dffm_model* m, FwdParams& p, int smax, cu
   return false;
 }
 
+// K1 v8 staging gather: warp-specialised circular row ring (M <= 4)
+static bool try_rsw_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
+                            int* rc) {
+  if (!p.xout || p.M < 1 || p.M > 4 || p.P < 1 || p.F * p.M > RSW_MAXFM || p.F > 255) return false;
+  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
+  const int k = p.k;
+  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
+  if (((uintptr_t)p.ffm & 15) || ((uintptr_t)p.lr & 3)) return false;
+  static int nx_env = -1;
+  if (nx_env < 0) {
+    const char* v = getenv("DFFM_RSW_NX");
+    nx_env = v ? std::min(RSW_MAXX, std::max(2, atoi(v))) : 6;
+  }
+  const int row_bytes = p.F * k * esz;
+  for (int nx = std::max(nx_env, RSW_NMW); nx >= std::max(2, RSW_NMW); --nx) {
+    const RswSmem L = rsw_smem_layout(p.F, p.M, p.P, row_bytes, nx, smax);
+    if (L.R < p.F * p.M || L.R < 2 * p.F) continue;
+    switch (m->wdtype) {
+      case DFFM_W_F32: *rc = launch_forward_rsw_t<float>(p, L, k, s); break;
+      case DFFM_W_BF16: *rc = launch_forward_rsw_t<__nv_bfloat16>(p, L, k, s); break;
+      default: *rc = launch_forward_rsw_t<uint16_t>(p, L, k, s); break;
+    }
+    return true;
+  }
+  return false;
+}
+
 bool tc_eligible(const FwdParams& p, int smax) {
   const int NH = p.n_layers - 1;
   if (NH < 1 || NH > TC_MAXH) return false;
@@ -421,7 +451,8 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
   static int gather_env = -2;
   if (gather_env == -2) {
     const char* v = getenv("DFFM_TC_GATHER");
-    gather_env = (v && strcmp(v, "g4") == 0) ? FAM_G4 : (v && strcmp(v, "rows") == 0) ? FAM_ROWS
+    gather_env = (v && strcmp(v, "rowstage") == 0) ? 100
+                 : (v && strcmp(v, "g4") == 0) ? FAM_G4 : (v && strcmp(v, "rows") == 0) ? FAM_ROWS
                  : (v && strcmp(v, "tma") == 0) ? FAM_TMA : (v && strcmp(v, "ws") == 0) ? FAM_WS
                  : -1;  // default: row staging when it applies, else ws
   }
@@ -443,7 +474,9 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     a.fout = plan.flags;
     a.Kp = plan.Kp;
     bool launched = false;
-    if (gather_env < 0) launched = try_rowstage_forward(m, a, smax, s, rc);
+    if (gather_env < 0) launched = try_rsw_forward(m, a, smax, s, rc);
+    if (gather_env == 100 || (gather_env < 0 && !launched))
+      launched = try_rowstage_forward(m, a, smax, s, rc);
     if (gather_env == FAM_G4) launched = try_g4_forward(m, a, smax, s, rc, true);
     else if (gather_env == FAM_ROWS) launched = try_rows_forward(m, a, smax, s, rc, true);
     else if (gather_env == FAM_TMA) launched = try_tma_forward(m, a, smax, s, rc, true);

@@ -11,6 +11,7 @@
 #include "forward_rows.cuh"
 #include "forward_g4.cuh"
 #include "forward_rowstage.cuh"
+#include "forward_rsw.cuh"
 
 namespace dffm {
 
@@ -213,5 +214,40 @@ int launch_forward_rowstage_t(const FwdParams& p, int K, int NB, int smem, cudaS
 }
 
 template int launch_forward_rowstage_t<DFFM_INST_T>(const FwdParams&, int, int, int, cudaStream_t);
+
+
+// ---------------------------------------------------------------- K1 v8 (warp-specialised row ring)
+using RswKernel = void (*)(FwdParams, RswSmem);
+template <typename T>
+static RswKernel select_rsw(int K, int MU) {
+#define DFFM_SEL(KK)                                          \
+  if (K == KK) {                                              \
+    if (MU == 1) return fwd_rsw_kernel<KK, T, 1>;             \
+    if (MU == 2) return fwd_rsw_kernel<KK, T, 2>;             \
+    if (MU == 3) return fwd_rsw_kernel<KK, T, 3>;             \
+    if (MU == 4) return fwd_rsw_kernel<KK, T, 4>;             \
+  }
+  if constexpr (sizeof(T) == 4) { DFFM_SEL(4) }
+  DFFM_SEL(8)
+  DFFM_SEL(16)
+#undef DFFM_SEL
+  return nullptr;
+}
+
+template <typename T>
+int launch_forward_rsw_t(const FwdParams& p, const RswSmem& L, int K, cudaStream_t s) {
+  RswKernel kern = select_rsw<T>(K, p.M);
+  if (!kern) { set_error("no row-ring kernel for k=%d M=%d", K, p.M); return DFFM_SIZING; }
+  int occ = 0;
+  int rc = kernel_occupancy((const void*)kern, RSW_THREADS, L.total, &occ);
+  if (rc) return rc;
+  const int64_t grid = std::min<int64_t>(p.n, (int64_t)sm_count_current());
+  if (grid <= 0) return DFFM_OK;
+  kern<<<(unsigned)grid, RSW_THREADS, L.total, s>>>(p, L);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rsw)");
+  return DFFM_OK;
+}
+
+template int launch_forward_rsw_t<DFFM_INST_T>(const FwdParams&, const RswSmem&, int, cudaStream_t);
 
 }  // namespace dffm

@@ -1,0 +1,398 @@
+// K1 v8 gather for the tensor-core MLP path: warp-specialised whole-row
+// staging through one circular shared-memory row ring per SM (any M <= 4).
+//
+// Why (profiles/r01_k1_cfg5_rowstage_mlp_tc_ncu.json): the CTA-synchronous
+// row-staging kernel (forward_rowstage.cuh) spends ~55% of its warp cycles in
+// barrier / mbarrier waits -- three CTA barriers per example -- while DRAM
+// is 31% busy.  Here no CTA barrier is left on the per-example path:
+//
+//   NPROD producer warps  read example i's padded slots (one example ahead
+//       in registers), allocate its present rows in a circular ring of R
+//       row slots (allocation and release in example order), write the slot
+//       metadata and issue one 1-D bulk (TMA) copy per present row; the
+//       ring is shared by all in-flight examples, so multi-slot data (cfg2:
+//       ~47 of 72 slots present) packs densely and ~4-6 examples are
+//       resident or in flight per SM.
+//   NPW pair warps      process 32-pair chunks; chunk c of example i goes to
+//       warp (i*nch + c) % npw (npw = min(NPW, nch)), so the warps drift
+//       across examples and stay balanced however P divides.  Each chunk writes its raw pair values,
+//       an f64 partial sum and a non-finite bit, then arrives on pdone[i].
+//       The last chunk of an example frees its ring rows.
+//   NMW merge warps     (example i on warp i % NMW) load the LR weights
+//       while the pairs are formed, then: lr_out (M:327, M:338), f64 mean /
+//       population std over [lr_out, pairs] (M:355-360), the standardised row
+//       (zero padded to Kp) written with 16-byte stores, lr_out + sum(pairs)
+//       and the stage bits -> the staging buffers read by mlp_tc_kernel.
+//
+// Same arithmetic as the other K1 families: per pair the slot rows are summed
+// in f32 in slot order (S[f1][f2] = sum_m x_m w_m[f2], M:339) and dotted in
+// f32; statistics in f64 with a fixed reduction order (deterministic).
+#pragma once
+
+#include "forward_kernel.cuh"
+
+namespace dffm {
+
+#ifndef DFFM_RSW_NPW
+#define DFFM_RSW_NPW 8
+#endif
+#ifndef DFFM_RSW_NPROD
+#define DFFM_RSW_NPROD 2
+#endif
+#ifndef DFFM_RSW_NMW
+#define DFFM_RSW_NMW 2
+#endif
+constexpr int RSW_NPW = DFFM_RSW_NPW;
+constexpr int RSW_NPROD = DFFM_RSW_NPROD;
+constexpr int RSW_NMW = DFFM_RSW_NMW;
+constexpr int RSW_THREADS = (RSW_NPW + RSW_NPROD + RSW_NMW) * 32;
+constexpr int RSW_MAXX = 8;     // example slots (metadata + pair values)
+constexpr int RSW_MAXFM = 128;  // padded slots per example (4 per producer lane)
+
+struct RswSmem {
+  int off_bar, off_pair, off_cnt, off_slot, off_ring, total;
+  int slot_bytes, off_sidx, off_sval, off_rpos, off_xv, off_part, off_pbad;  // within a slot
+  int row_stride, R, NX, nch;
+};
+
+// Example-slot block: sidx[FM] i32, sval[FM] f32, rpos[FM] u16, xv[P+1] f32,
+// part[nch] f64, pbad[nch] i32; the ring takes the rest of `smem_max`.
+__host__ __device__ inline RswSmem rsw_smem_layout(int F, int M, int P, int row_bytes, int NX,
+                                                   int smem_max) {
+  RswSmem s;
+  const int FM = F * M;
+  s.NX = NX;
+  s.nch = (P + 31) / 32;
+  s.row_stride = row_bytes + 16;  // rotates banks row to row
+  int q = 0;
+  s.off_part = q; q = align16(q + s.nch * 8);
+  s.off_sidx = q; q = align16(q + FM * 4);
+  s.off_sval = q; q = align16(q + FM * 4);
+  s.off_rpos = q; q = align16(q + FM * 2);
+  s.off_pbad = q; q = align16(q + s.nch * 4);
+  s.off_xv = q; q = align16(q + (P + 1) * 4);
+  s.slot_bytes = q;
+  int o = 0;
+  s.off_bar = o; o = align16(o + 3 * RSW_MAXX * 8);
+  s.off_pair = o; o = align16(o + P * 2);
+  s.off_cnt = o; o = align16(o + RSW_NPROD * RSW_MAXX * 4);
+  s.off_slot = o; o = align16(o + NX * s.slot_bytes);
+  s.off_ring = o;
+  s.R = (smem_max - o) / s.row_stride;
+  if (s.R > 65535) s.R = 65535;
+  s.total = o + (s.R > 0 ? s.R : 0) * s.row_stride;
+  return s;
+}
+
+template <int K, typename T, int MU>
+__global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, RswSmem L) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int F = p.F, P = p.P, D = p.D;
+  constexpr int M = MU;
+  const int FM = F * M;
+  constexpr int SEGB = K * (int)sizeof(T);
+  const int row_bytes = F * SEGB;
+  const int RSB = L.row_stride, R = L.R, NX = L.NX, nch = L.nch;
+  uint64_t* full = (uint64_t*)(smem + L.off_bar);  // [NX] producers -> pair/merge warps
+  uint64_t* pdone = full + RSW_MAXX;               // [NX] pair chunks -> producers/merge
+  uint64_t* mfree = pdone + RSW_MAXX;              // [NX] merge warp -> producers
+  uint16_t* pairtab = (uint16_t*)(smem + L.off_pair);
+  int* cnt_all = (int*)(smem + L.off_cnt);  // [NPROD][MAXX] rows per slot (producer-private)
+  unsigned char* slots = smem + L.off_slot;
+  unsigned char* ring = smem + L.off_ring;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const T* lrt = (const T*)p.lr;
+
+  for (int f1 = threadIdx.x; f1 < F; f1 += RSW_THREADS) {
+    const int base = f1 * F - f1 * (f1 + 1) / 2;
+    for (int f2 = f1 + 1; f2 < F; ++f2) pairtab[base + f2 - f1 - 1] = (uint16_t)(f1 | (f2 << 8));
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NX; ++b) {
+      mbar_init(&full[b], RSW_NPROD);
+      mbar_init(&pdone[b], nch);
+      mbar_init(&mfree[b], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int64_t my_n = p.n > blockIdx.x ? (p.n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto slot = [&](int xs) { return slots + (size_t)xs * L.slot_bytes; };
+
+  if (warp >= RSW_NPW + RSW_NPROD) {
+    // ================================================================ merge warps
+    const int mw = warp - RSW_NPW - RSW_NPROD;
+    const float bias = load_elem<T>(lrt + p.n_buckets, p.dlr);
+    int xs = mw % NX;
+    uint32_t par = (uint32_t)((mw / NX) & 1);
+    for (int64_t i = mw; i < my_n; i += RSW_NMW) {
+      const int64_t e = blockIdx.x + i * gridDim.x;
+      unsigned char* sb = slot(xs);
+      const int* sidx = (const int*)(sb + L.off_sidx);
+      const float* sval = (const float*)(sb + L.off_sval);
+      mbar_wait(&full[xs], par);
+      // LR terms (M:338) in flight while the pairs are formed
+      float lw[RSW_MAXFM / 32], lx[RSW_MAXFM / 32];
+#pragma unroll
+      for (int c = 0; c < RSW_MAXFM / 32; ++c) {
+        const int s = lane + 32 * c;
+        const int j = s < FM ? sidx[s] : -1;
+        lx[c] = j >= 0 ? sval[s] : 0.f;
+        lw[c] = j >= 0 ? load_elem<T>(lrt + j, p.dlr) : 0.f;
+      }
+      mbar_wait(&pdone[xs], par);
+      const double* part = (const double*)(sb + L.off_part);
+      const int* pb = (const int*)(sb + L.off_pbad);
+      const float* xv = (const float*)(sb + L.off_xv);
+      double ps = 0.0;
+      int pbad = 0;
+      for (int c = lane; c < nch; c += 32) { ps += part[c]; pbad |= pb[c]; }
+      const double psum = warp_sum(ps);
+      pbad = __any_sync(0xffffffffu, pbad);
+      double lrs = 0.0;
+#pragma unroll
+      for (int c = 0; c < RSW_MAXFM / 32; ++c) lrs += (double)lx[c] * (double)lw[c];
+      const double lr_out = (double)bias + warp_sum(lrs);  // M:327
+      // MergeNorm (M:355-360): population std + MERGE_EPS
+      const double mu = (psum + lr_out) / D;
+      double s2 = 0.0;
+      for (int pp = lane; pp < P; pp += 32) {
+        const double d = (double)xv[1 + pp] - mu;
+        s2 += d * d;
+      }
+      s2 = warp_sum(s2) + (lr_out - mu) * (lr_out - mu);
+      const double denom = sqrt(s2 / D) + 1e-6;
+      const double rden = 1.0 / denom;  // one f64 division per example
+      const float m0 = (float)((lr_out - mu) * rden);
+      int mbad = 0;
+      float4* row = (float4*)(p.xout + e * p.Kp);
+      for (int q = lane; q < (p.Kp >> 2); q += 32) {
+        float v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int c = 4 * q + t;
+          float m = 0.f;
+          if (c == 0) m = m0;
+          else if (c < D) m = (float)(((double)xv[c] - mu) * rden);
+          mbad |= !isfinite(m);
+          v[t] = m;
+        }
+        row[q] = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      mbad = __any_sync(0xffffffffu, mbad);
+      if (lane == 0) {
+        p.rout[e] = lr_out + psum;
+        p.fout[e] = (!isfinite(lr_out) ? 1 : 0) | (pbad ? 2 : 0) | (mbad ? 4 : 0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mfree[xs]);
+      xs += RSW_NMW;
+      while (xs >= NX) { xs -= NX; par ^= 1u; }
+    }
+  } else if (warp >= RSW_NPW) {
+    // ================================================================ producer warps
+    const int pw = warp - RSW_NPW;
+    int* my_cnt = cnt_all + pw * RSW_MAXX;
+    constexpr int SPL = RSW_MAXFM / 32;
+    int nj[SPL];
+    float nx[SPL];
+    auto load_ex = [&](int64_t i) {
+      const int64_t e = blockIdx.x + i * gridDim.x;
+#pragma unroll
+      for (int c = 0; c < SPL; ++c) {
+        const int s = lane + 32 * c;
+        const bool ok = i < my_n && s < FM;
+        nj[c] = ok ? __ldg(p.idx + e * FM + s) : -1;
+        nx[c] = ok ? __ldg(p.val + e * FM + s) : 0.f;
+      }
+    };
+    load_ex(0);
+    int head = 0, tail = 0;  // ring rows allocated / released (mod R)
+    int used = 0;            // rows currently allocated
+    int64_t tail_ex = 0;     // oldest example whose rows are still allocated
+    const uint32_t lt = (1u << lane) - 1u;
+    int xs = 0, ts = 0;         // slot of example i / of tail_ex
+    uint32_t fpar = 1, tpar = 0;  // mfree parity for example i - NX / pdone parity of tail_ex
+    for (int64_t i = 0; i < my_n; ++i) {
+      const int64_t e = blockIdx.x + i * gridDim.x;
+      int cj[SPL];
+      float cx[SPL];
+      int bad = 0;
+#pragma unroll
+      for (int c = 0; c < SPL; ++c) {
+        int j = nj[c];
+        if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }  // ContractError (bad index)
+        cj[c] = j;
+        cx[c] = nx[c];
+      }
+      load_ex(i + 1);
+      if (pw == 0 && __any_sync(0xffffffffu, bad) && lane == 0)
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
+                                                 DFFM_CONTRACT));
+      uint32_t mask[SPL];
+      int cnt = 0;
+#pragma unroll
+      for (int c = 0; c < SPL; ++c) {
+        mask[c] = __ballot_sync(0xffffffffu, cj[c] >= 0);
+        cnt += __popc(mask[c]);
+      }
+      // example slot free (its merge of example i - NX is done, so are its
+      // pairs): retire that example's rows now, before the slot is reused
+      if (i >= NX) {
+        mbar_wait(&mfree[xs], fpar);
+        if (tail_ex == i - NX) {
+          const int tc = my_cnt[xs];
+          tail += tc;
+          if (tail >= R) tail -= R;
+          used -= tc;
+          ++tail_ex;
+          if (++ts == NX) { ts = 0; tpar ^= 1u; }
+        }
+      }
+      // ring space: release the oldest examples' rows once their pairs are
+      // formed (examples i-NX+1 .. i-1: their slots are not reused yet)
+      while (used + cnt > R) {
+        mbar_wait(&pdone[ts], tpar);
+        const int tc = my_cnt[ts];
+        tail += tc;
+        if (tail >= R) tail -= R;
+        used -= tc;
+        ++tail_ex;
+        if (++ts == NX) { ts = 0; tpar ^= 1u; }
+      }
+      // slot metadata (this warp writes the slots it issues) + one bulk copy per row
+      unsigned char* sb = slot(xs);
+      int* sidx = (int*)(sb + L.off_sidx);
+      float* sval = (float*)(sb + L.off_sval);
+      uint16_t* rpos = (uint16_t*)(sb + L.off_rpos);
+      int before = 0, mine = 0;
+      int rp[SPL];
+#pragma unroll
+      for (int c = 0; c < SPL; ++c) {
+        const int s = lane + 32 * c;
+        int r = head + before + __popc(mask[c] & lt);
+        if (r >= R) r -= R;
+        rp[c] = cj[c] >= 0 ? r : -1;
+        before += __popc(mask[c]);
+        const bool own = ((lane + c) % RSW_NPROD) == pw;
+        if (own && s < FM) {
+          sidx[s] = cj[c];
+          sval[s] = cx[c];
+          rpos[s] = (uint16_t)(cj[c] >= 0 ? r : 0xFFFF);
+        }
+        mine += __popc(__ballot_sync(0xffffffffu, own && cj[c] >= 0));
+      }
+      if (lane == 0) {
+        my_cnt[xs] = cnt;
+        if (mine) mbar_arrive_expect_tx(&full[xs], (uint32_t)(mine * row_bytes));
+        else mbar_arrive(&full[xs]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < SPL; ++c) {
+        if (rp[c] >= 0 && ((lane + c) % RSW_NPROD) == pw)
+          tma_load_1d(ring + (size_t)rp[c] * RSB,
+                      (const unsigned char*)p.ffm + (int64_t)cj[c] * row_bytes,
+                      (uint32_t)row_bytes, &full[xs]);
+      }
+      head += cnt;
+      if (head >= R) head -= R;
+      used += cnt;
+      if (++xs == NX) { xs = 0; fpar ^= 1u; }
+    }
+  } else {
+    // ================================================================ pair warps
+    // Only min(NPW, nch) pair warps take chunks, so every active warp has a
+    // chunk in every example and walks the examples in order: when it waits
+    // on full[] for example i it has seen example i-NX's phase complete, and
+    // the slot cannot be reissued before its own chunk of i is done -- the
+    // mbarrier parity waits never alias across phases (same argument for the
+    // merge warps: pdone(i-NMW) complete => every pair warp is past i-NMW).
+    const int npw = RSW_NPW < nch ? RSW_NPW : nch;
+    // chunk counter g = warp + t*npw walked incrementally: example i, chunk c,
+    // slot xs, phase parity (no 64-bit divisions on the per-chunk path)
+    int64_t i = warp < npw ? 0 : my_n;
+    int c = warp;
+    int xs = 0;
+    uint32_t par = 0;
+    int64_t cur = -1;
+    const unsigned char* sb = nullptr;
+    const int* sidx = nullptr;
+    const float* sval = nullptr;
+    const uint16_t* rpos = nullptr;
+    for (; i < my_n;) {
+      if (i != cur) {
+        mbar_wait(&full[xs], par);
+        cur = i;
+        sb = slot(xs);
+        sidx = (const int*)(sb + L.off_sidx);
+        sval = (const float*)(sb + L.off_sval);
+        rpos = (const uint16_t*)(sb + L.off_rpos);
+      }
+      const int pp = c * 32 + lane;
+      float pv = 0.f;
+      if (pp < P) {
+        const uint32_t pr = pairtab[pp];
+        const int f1 = pr & 0xFF, f2 = pr >> 8;
+        float a[K], bb[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) { a[t] = 0.f; bb[t] = 0.f; }
+        bool p1 = false, p2 = false;
+        constexpr int PER = 16 / (int)sizeof(T);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int r1 = rpos[f1 * M + m];
+          if (r1 != 0xFFFF) {
+            p1 = true;
+            const float x1 = sval[f1 * M + m];
+            const unsigned char* q1 = ring + (size_t)r1 * RSB + f2 * SEGB;
+#pragma unroll
+            for (int u = 0; u < SEGB / 16; ++u) {
+              float w[PER];
+              unpack16<T>(*(const uint4*)(q1 + u * 16), w, p.dffm);
+#pragma unroll
+              for (int t = 0; t < PER; ++t) a[u * PER + t] = fmaf(x1, w[t], a[u * PER + t]);
+            }
+          }
+          const int r2 = rpos[f2 * M + m];
+          if (r2 != 0xFFFF) {
+            p2 = true;
+            const float x2 = sval[f2 * M + m];
+            const unsigned char* q2 = ring + (size_t)r2 * RSB + f1 * SEGB;
+#pragma unroll
+            for (int u = 0; u < SEGB / 16; ++u) {
+              float w[PER];
+              unpack16<T>(*(const uint4*)(q2 + u * 16), w, p.dffm);
+#pragma unroll
+              for (int t = 0; t < PER; ++t) bb[u * PER + t] = fmaf(x2, w[t], bb[u * PER + t]);
+            }
+          }
+        }
+        if (p1 && p2) {  // inactive pairs stay exactly 0 (M:346-351)
+#pragma unroll
+          for (int t = 0; t < K; ++t) pv = fmaf(a[t], bb[t], pv);
+        }
+        float* xv = (float*)(sb + L.off_xv);
+        xv[1 + pp] = pv;
+      }
+      const double s = warp_sum((double)pv);
+      const int bad = __any_sync(0xffffffffu, !isfinite(pv));
+      if (lane == 0) {
+        ((double*)(sb + L.off_part))[c] = s;
+        ((int*)(sb + L.off_pbad))[c] = bad;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pdone[xs]);
+      c += npw;
+      while (c >= nch) {
+        c -= nch;
+        ++i;
+        if (++xs == NX) { xs = 0; par ^= 1u; }
+      }
+    }
+  }
+}
+
+}  // namespace dffm

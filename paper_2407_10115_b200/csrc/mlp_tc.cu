@@ -130,6 +130,10 @@ __device__ __forceinline__ void epi_drain(HalfRow& acc, uint64_t* accf, uint64_t
   ++dg;
 }
 
+// first 16-column block of part h of an N-wide layer (N % 16 == 0): the
+// N/16 blocks are dealt to the TC_PARTS parts as evenly as possible
+__device__ __forceinline__ int part_blk(int h, int N) { return (h * (N >> 4)) / TC_PARTS; }
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
 mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   extern __shared__ unsigned char smem_raw[];
@@ -256,9 +260,12 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
       int nn_bad = 0;
       for (int l = 0; l < NH; ++l) {
         const int nck = p.kin[l] >> 4, N = p.nout[l];
-        const int hc = N / TC_PARTS;       // columns per part (multiple of 16)
+        // this part's 16-column blocks [b0, b1) of layer l (parts may be empty
+        // when N < 64) and of the previous layer (ownership of its A chunks)
+        const int b0 = part_blk(h, N), hc = (part_blk(h + 1, N) - b0) * 16;
         const int ngr = (nck + TC_GROUP - 1) / TC_GROUP;
-        const int hcp = l > 0 ? p.nout[l - 1] / TC_PARTS : 0;  // previous layer's part width
+        const int pb0 = l > 0 ? part_blk(h, p.nout[l - 1]) : 0;
+        const int pb1 = l > 0 ? part_blk(h + 1, p.nout[l - 1]) : 0;
         for (int gi = 0; gi < ngr; ++gi) {
           const int cend = min(nck, (gi + 1) * TC_GROUP);
           for (int c = gi * TC_GROUP; c < cend; ++c, ++g) {
@@ -273,8 +280,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
                 const float4 x = a[i];
                 lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
               }
-            } else if ((c * 16) / hcp == h) {  // this part holds the chunk's 16 columns
-              const int cbl = (c * 16 - h * hcp) >> 4;
+            } else if (c >= pb0 && c < pb1) {  // this part holds the chunk's 16 columns
+              const int cbl = c - pb0;
 #pragma unroll
               for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
                 if (cb == cbl) {
@@ -294,11 +301,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
             if (lane == 0) mbar_arrive(&aready[s]);
           }
           if (gi > 0)  // one group behind the MMAs
-            epi_drain(acc, accf, tempty, dg, lane_base, RS, h * hc, hc >> 4, gi == 1, lane);
+            epi_drain(acc, accf, tempty, dg, lane_base, RS, b0 * 16, hc >> 4, gi == 1, lane);
         }
-        epi_drain(acc, accf, tempty, dg, lane_base, RS, h * hc, hc >> 4, ngr == 1, lane);
+        epi_drain(acc, accf, tempty, dg, lane_base, RS, b0 * 16, hc >> 4, ngr == 1, lane);
         // acc = this part's pre-activations of layer l: + bias, ReLU (M:368-370)
-        const float* __restrict__ bl = p.bias[l] + h * hc;
+        const float* __restrict__ bl = p.bias[l] + b0 * 16;
 #pragma unroll
         for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
           if (cb < (hc >> 4)) {
@@ -312,8 +319,9 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
         }
       }
       // ---- output layer (M:372-373): the parts' partial dots meet in shared memory
-      const int hcl = p.nout[NH - 1] / TC_PARTS;
-      const float* __restrict__ wo = p.w_out + h * hcl;
+      const int lb0 = part_blk(h, p.nout[NH - 1]);
+      const int hcl = (part_blk(h + 1, p.nout[NH - 1]) - lb0) * 16;
+      const float* __restrict__ wo = p.w_out + lb0 * 16;
       float part = 0.f;
 #pragma unroll
       for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {

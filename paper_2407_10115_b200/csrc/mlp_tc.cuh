@@ -18,7 +18,7 @@ constexpr int TC_PARTS = DFFM_TC_PARTS;  // epilogue warps per TMEM lane quadran
 constexpr int TC_EPI_WARPS = 4 * TC_PARTS;
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, then epilogue
 constexpr int TC_PART_MAX = 256 / TC_PARTS;  // accumulator columns per epilogue thread
-constexpr int TC_WIDTH_MULT = 16 * TC_PARTS; // hidden widths: multiples of this, <= 256
+constexpr int TC_WIDTH_MULT = 16;            // hidden widths: multiples of this, <= 256
 #ifndef DFFM_TC_GROUP
 #define DFFM_TC_GROUP 8
 #endif

@@ -308,3 +308,78 @@ def test_context_cache_full_size_cfg4_sample():
     _, ref = fo.forward_batch(ridx, mv, cst)
     got = p[rr.to(DEV), cc.to(DEV)].double().cpu().numpy()
     assert rel_err(got, ref).max() < RTOL
+
+
+RING_CASES = [
+    # F, k, hidden, M, bits, n, wdtype
+    (24, 8, (64, 32), 3, 12, 1000, "f32"),
+    (8, 4, (32, 16), 4, 10, 513, "f32"),
+    (40, 16, (256, 128), 1, 11, 300, "bf16"),
+    (16, 16, (64,), 2, 10, 257, "u16"),
+    (32, 8, (128, 64), 4, 10, 200, "f32"),   # F*M = 128 slots (the kernel's maximum)
+    (2, 8, (16,), 2, 6, 90, "bf16"),          # P = 1: one pair chunk per example
+]
+
+
+@pytest.mark.parametrize("F,k,hidden,M,bits,n,wdtype", RING_CASES)
+def test_forward_row_ring_gather_matches_oracle(F, k, hidden, M, bits, n, wdtype):
+    """K1 v8 (warp-specialised circular row ring feeding the tcgen05 MLP,
+    forward_rsw.cuh): ragged multi-slot fields, fully empty examples (no rows
+    allocated), every table dtype, against the oracle."""
+    from paper_2407_10115_b200 import _lib
+    from paper_2407_10115_b200.quant import quantize_store
+    rng = np.random.default_rng(F * 7919 + M)
+    ost = fo.random_store(F, k, hidden, bits, seed=F + M)
+    idx = rng.integers(-1, 1 << bits, size=(n, F, M)).astype(np.int32)
+    idx = np.sort(np.where(idx < 0, np.iinfo(np.int32).max, idx), axis=2)
+    idx = np.where(idx == np.iinfo(np.int32).max, -1, idx)
+    for e in range(n):
+        for f in range(F):
+            live = np.unique(idx[e, f][idx[e, f] >= 0])
+            idx[e, f] = -1
+            idx[e, f, :len(live)] = live
+    idx[::11] = -1      # empty examples
+    idx[5::13, 1:] = -1  # one present field
+    val = np.where(idx >= 0, rng.lognormal(size=idx.shape), 0).astype(np.float32)
+    st = store_from_oracle(ost)
+    if wdtype == "bf16":
+        st = WeightStore.from_flat(st.config, ost.flat(False), DEV, "bf16", False)
+    elif wdtype == "u16":
+        st, _ = quantize_store(st)
+    _lib.check(_lib.lib().dffm_set_forward_family(5))
+    try:
+        lg = torch.empty(n, device=DEV)
+        p = predict_batch(idx, val, st, logits=lg).double().cpu().numpy()
+    finally:
+        _lib.lib().dffm_set_forward_family(-1)
+    cst, ridx, _ = compact_oracle(st, idx)
+    lref, ref = fo.forward_batch(ridx, val, cst)
+    assert rel_err(p, ref).max() < RTOL
+    np.testing.assert_allclose(lg.double().cpu().numpy(), lref, rtol=1e-5, atol=1e-5)
+
+
+def test_forward_row_ring_nonfinite_and_bad_index():
+    """Row-ring gather: the first non-finite example/block and a bad bucket
+    index (ContractError) are reported like the reference loop would."""
+    from paper_2407_10115_b200 import _lib
+    ost = fo.random_store(4, 4, (16,), 6, seed=2)
+    idx = np.full((300, 4, 2), -1, np.int32)
+    idx[:, 0, 0] = 1
+    idx[:, 1, 0] = 2
+    idx[:, 2, 0] = 5
+    o = ost.copy()
+    o.ffm[9, 2, 0] = np.inf
+    ix = idx.copy()
+    ix[170, 1, 1] = 9
+    ix[233, 1, 1] = 9
+    _lib.check(_lib.lib().dffm_set_forward_family(5))
+    try:
+        with pytest.raises(NumericError) as ei:
+            predict_batch(ix, (ix >= 0).astype(np.float32), store_from_oracle(o))
+        assert ei.value.example == 170 and ei.value.block == "ffm"
+        ix = idx.copy()
+        ix[77, 3, 0] = 1 << 6
+        with pytest.raises(ContractError):
+            predict_batch(ix, (ix >= 0).astype(np.float32), store_from_oracle(ost))
+    finally:
+        _lib.lib().dffm_set_forward_family(-1)
