@@ -125,6 +125,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 // arrive on `bar` once all of this thread's prior cp.async copies have landed
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
@@ -184,6 +191,35 @@ __device__ __forceinline__ void unpack8(const uint2& u, float* o, const Deq& d) 
   unpack16<T>(w, t, d);
 #pragma unroll
   for (int i = 0; i < (int)(8 / sizeof(T)); ++i) o[i] = t[i];
+}
+
+// d + <a, b> over one 16-byte chunk of T values, f32 sequential in element
+// order; bf16 uses the mixed-precision FMA (FHFMA.BF16: exact bf16 products,
+// one f32 rounding per step -- the same bits as widening first)
+template <typename T>
+__device__ __forceinline__ float dot16_acc(const uint4& a, const uint4& b, float d, const Deq& q) {
+  constexpr int PER = 16 / (int)sizeof(T);
+  float x[PER], y[PER];
+  unpack16<T>(a, x, q);
+  unpack16<T>(b, y, q);
+#pragma unroll
+  for (int t = 0; t < PER; ++t) d = fmaf(x[t], y[t], d);
+  return d;
+}
+template <>
+__device__ __forceinline__ float dot16_acc<__nv_bfloat16>(const uint4& a, const uint4& b, float d,
+                                                          const Deq&) {
+  const uint32_t xa[4] = {a.x, a.y, a.z, a.w}, xb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm("{.reg .b16 al, ah, bl, bh;\n\t"
+        "mov.b32 {al, ah}, %1;\n\t"
+        "mov.b32 {bl, bh}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, al, bl, %0;\n\t"
+        "fma.rn.f32.bf16 %0, ah, bh, %0;\n\t}"
+        : "+f"(d)
+        : "r"(xa[i]), "r"(xb[i]));
+  return d;
 }
 
 // Load one k-vector segment (K elements of T, naturally aligned) as floats.

@@ -340,6 +340,7 @@ static bool try_rsw_forward(const dffm_model* m, FwdParams& p, int smax, cudaStr
     const char* v = getenv("DFFM_RSW_NX");
     nx_env = v ? std::min(RSW_MAXX, std::max(2, atoi(v))) : 6;
   }
+
   const int row_bytes = p.F * k * esz;
   for (int nx = std::max(nx_env, RSW_NMW); nx >= std::max(2, RSW_NMW); --nx) {
     const RswSmem L = rsw_smem_layout(p.F, p.M, p.P, row_bytes, nx, smax);

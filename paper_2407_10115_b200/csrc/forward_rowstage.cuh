@@ -59,13 +59,6 @@ __host__ __device__ inline RsSmem rs_smem_layout(int F, int P, int row_bytes, in
   return s;
 }
 
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // CTA-wide f64 sums of NV values per thread, results in every thread (one
 // barrier; fixed order: deterministic)

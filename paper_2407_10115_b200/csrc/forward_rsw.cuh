@@ -6,8 +6,8 @@
 // barrier / mbarrier waits -- three CTA barriers per example -- while DRAM
 // is 31% busy.  Here no CTA barrier is left on the per-example path:
 //
-//   NPROD producer warps  read example i's padded slots (one example ahead
-//       in registers), allocate its present rows in a circular ring of R
+//   NPROD producer warps  read example i's padded slots (streamed IDXD
+//       examples ahead into shared memory by cp.async), allocate its present rows in a circular ring of R
 //       row slots (allocation and release in example order), write the slot
 //       metadata and issue one 1-D bulk (TMA) copy per present row; the
 //       ring is shared by all in-flight examples, so multi-slot data (cfg2:
@@ -19,7 +19,8 @@
 //       an f64 partial sum and a non-finite bit, then arrives on pdone[i].
 //       The last chunk of an example frees its ring rows.
 //   NMW merge warps     (example i on warp i % NMW) load the LR weights
-//       while the pairs are formed, then: lr_out (M:327, M:338), f64 mean /
+//       while the pairs are formed, then: sum(pairs) and the non-finite
+//       check, lr_out (M:327, M:338), f64 mean /
 //       population std over [lr_out, pairs] (M:355-360), the standardised row
 //       (zero padded to Kp) written with 16-byte stores, lr_out + sum(pairs)
 //       and the stage bits -> the staging buffers read by mlp_tc_kernel.
@@ -34,29 +35,34 @@
 namespace dffm {
 
 #ifndef DFFM_RSW_NPW
-#define DFFM_RSW_NPW 8
+#define DFFM_RSW_NPW 12
 #endif
 #ifndef DFFM_RSW_NPROD
 #define DFFM_RSW_NPROD 2
 #endif
+#ifndef DFFM_RSW_IDXD
+#define DFFM_RSW_IDXD 4
+#endif
 #ifndef DFFM_RSW_NMW
-#define DFFM_RSW_NMW 2
+#define DFFM_RSW_NMW 3
 #endif
 constexpr int RSW_NPW = DFFM_RSW_NPW;
 constexpr int RSW_NPROD = DFFM_RSW_NPROD;
 constexpr int RSW_NMW = DFFM_RSW_NMW;
+constexpr int RSW_IDXD = DFFM_RSW_IDXD;  // examples of idx/val in flight per producer (power of 2)
+static_assert((RSW_IDXD & (RSW_IDXD - 1)) == 0, "RSW_IDXD must be a power of two");
 constexpr int RSW_THREADS = (RSW_NPW + RSW_NPROD + RSW_NMW) * 32;
 constexpr int RSW_MAXX = 8;     // example slots (metadata + pair values)
 constexpr int RSW_MAXFM = 128;  // padded slots per example (4 per producer lane)
 
 struct RswSmem {
-  int off_bar, off_pair, off_cnt, off_slot, off_ring, total;
-  int slot_bytes, off_sidx, off_sval, off_rpos, off_xv, off_part, off_pbad;  // within a slot
+  int off_bar, off_pair, off_cnt, off_pidx, off_slot, off_ring, total;
+  int slot_bytes, off_sidx, off_sval, off_rpos, off_xv;  // within a slot
   int row_stride, R, NX, nch;
 };
 
-// Example-slot block: sidx[FM] i32, sval[FM] f32, rpos[FM] u16, xv[P+1] f32,
-// part[nch] f64, pbad[nch] i32; the ring takes the rest of `smem_max`.
+// Example-slot block: sidx[FM] i32, sval[FM] f32, rpos[FM] u16, xv[P+1] f32;
+// the ring takes the rest of `smem_max`.
 __host__ __device__ inline RswSmem rsw_smem_layout(int F, int M, int P, int row_bytes, int NX,
                                                    int smem_max) {
   RswSmem s;
@@ -65,17 +71,16 @@ __host__ __device__ inline RswSmem rsw_smem_layout(int F, int M, int P, int row_
   s.nch = (P + 31) / 32;
   s.row_stride = row_bytes + 16;  // rotates banks row to row
   int q = 0;
-  s.off_part = q; q = align16(q + s.nch * 8);
   s.off_sidx = q; q = align16(q + FM * 4);
   s.off_sval = q; q = align16(q + FM * 4);
   s.off_rpos = q; q = align16(q + FM * 2);
-  s.off_pbad = q; q = align16(q + s.nch * 4);
   s.off_xv = q; q = align16(q + (P + 1) * 4);
   s.slot_bytes = q;
   int o = 0;
   s.off_bar = o; o = align16(o + 3 * RSW_MAXX * 8);
   s.off_pair = o; o = align16(o + P * 2);
   s.off_cnt = o; o = align16(o + RSW_NPROD * RSW_MAXX * 4);
+  s.off_pidx = o; o = align16(o + RSW_NPROD * RSW_IDXD * 2 * FM * 4);
   s.off_slot = o; o = align16(o + NX * s.slot_bytes);
   s.off_ring = o;
   s.R = (smem_max - o) / s.row_stride;
@@ -142,12 +147,14 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
         lw[c] = j >= 0 ? load_elem<T>(lrt + j, p.dlr) : 0.f;
       }
       mbar_wait(&pdone[xs], par);
-      const double* part = (const double*)(sb + L.off_part);
-      const int* pb = (const int*)(sb + L.off_pbad);
       const float* xv = (const float*)(sb + L.off_xv);
       double ps = 0.0;
       int pbad = 0;
-      for (int c = lane; c < nch; c += 32) { ps += part[c]; pbad |= pb[c]; }
+      for (int pp = lane; pp < P; pp += 32) {  // sum(pairs) (M:351, M:377) in f64
+        const float v = xv[1 + pp];
+        ps += (double)v;
+        pbad |= !isfinite(v);
+      }
       const double psum = warp_sum(ps);
       pbad = __any_sync(0xffffffffu, pbad);
       double lrs = 0.0;
@@ -195,19 +202,27 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
     const int pw = warp - RSW_NPW;
     int* my_cnt = cnt_all + pw * RSW_MAXX;
     constexpr int SPL = RSW_MAXFM / 32;
-    int nj[SPL];
-    float nx[SPL];
-    auto load_ex = [&](int64_t i) {
-      const int64_t e = blockIdx.x + i * gridDim.x;
+    // idx / val of examples i+1 .. i+IDXD-1 stream into a private shared ring
+    // by 4-byte cp.async (one commit group per example), so the producer never
+    // waits a global-load latency per example
+    int* pidx = (int*)(smem + L.off_pidx) + pw * RSW_IDXD * 2 * FM;  // [IDXD][idx FM | val FM]
+    auto issue_ex = [&](int64_t i) {
+      if (i < my_n) {
+        const int64_t e = blockIdx.x + i * gridDim.x;
+        int* d = pidx + (int)(i & (RSW_IDXD - 1)) * 2 * FM;
 #pragma unroll
-      for (int c = 0; c < SPL; ++c) {
-        const int s = lane + 32 * c;
-        const bool ok = i < my_n && s < FM;
-        nj[c] = ok ? __ldg(p.idx + e * FM + s) : -1;
-        nx[c] = ok ? __ldg(p.val + e * FM + s) : 0.f;
+        for (int c = 0; c < SPL; ++c) {
+          const int s = lane + 32 * c;
+          if (s < FM) {
+            cp_async4(d + s, p.idx + e * FM + s);
+            cp_async4(d + FM + s, p.val + e * FM + s);
+          }
+        }
       }
+      cp_async_commit();
     };
-    load_ex(0);
+#pragma unroll 1
+    for (int d = 0; d < RSW_IDXD; ++d) issue_ex(d);
     int head = 0, tail = 0;  // ring rows allocated / released (mod R)
     int used = 0;            // rows currently allocated
     int64_t tail_ex = 0;     // oldest example whose rows are still allocated
@@ -219,14 +234,19 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       int cj[SPL];
       float cx[SPL];
       int bad = 0;
+      cp_async_wait<RSW_IDXD - 1>();  // this lane's copies of example i have landed
+      {
+        const int* d = pidx + (int)(i & (RSW_IDXD - 1)) * 2 * FM;
 #pragma unroll
-      for (int c = 0; c < SPL; ++c) {
-        int j = nj[c];
-        if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }  // ContractError (bad index)
-        cj[c] = j;
-        cx[c] = nx[c];
+        for (int c = 0; c < SPL; ++c) {
+          const int s = lane + 32 * c;
+          int j = s < FM ? d[s] : -1;
+          if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }  // ContractError (bad index)
+          cj[c] = j;
+          cx[c] = s < FM ? __int_as_float(d[FM + s]) : 0.f;
+        }
       }
-      load_ex(i + 1);
+      issue_ex(i + RSW_IDXD);
       if (pw == 0 && __any_sync(0xffffffffu, bad) && lane == 0)
         atomicMin((unsigned long long*)p.status,
                   (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
@@ -302,6 +322,7 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       used += cnt;
       if (++xs == NX) { xs = 0; fpar ^= 1u; }
     }
+    cp_async_wait<0>();
   } else {
     // ================================================================ pair warps
     // Only min(NPW, nch) pair warps take chunks, so every active warp has a
@@ -332,56 +353,71 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
         rpos = (const uint16_t*)(sb + L.off_rpos);
       }
       const int pp = c * 32 + lane;
-      float pv = 0.f;
       if (pp < P) {
         const uint32_t pr = pairtab[pp];
         const int f1 = pr & 0xFF, f2 = pr >> 8;
-        float a[K], bb[K];
-#pragma unroll
-        for (int t = 0; t < K; ++t) { a[t] = 0.f; bb[t] = 0.f; }
-        bool p1 = false, p2 = false;
-        constexpr int PER = 16 / (int)sizeof(T);
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          const int r1 = rpos[f1 * M + m];
-          if (r1 != 0xFFFF) {
-            p1 = true;
-            const float x1 = sval[f1 * M + m];
+        float pv = 0.f;
+        if constexpr (M == 1) {
+          // one row per field: pair = x1*x2*<w1[f2], w2[f1]> -- the raw segment
+          // dot in f32 (bf16: FHFMA, exact products of the stored values), then
+          // one scale (x = 1.0 for categorical fields: the same bits as
+          // scaling each side first)
+          const int r1 = rpos[f1], r2 = rpos[f2];
+          if (r1 != 0xFFFF && r2 != 0xFFFF) {  // inactive pairs stay exactly 0 (M:346-351)
             const unsigned char* q1 = ring + (size_t)r1 * RSB + f2 * SEGB;
-#pragma unroll
-            for (int u = 0; u < SEGB / 16; ++u) {
-              float w[PER];
-              unpack16<T>(*(const uint4*)(q1 + u * 16), w, p.dffm);
-#pragma unroll
-              for (int t = 0; t < PER; ++t) a[u * PER + t] = fmaf(x1, w[t], a[u * PER + t]);
-            }
-          }
-          const int r2 = rpos[f2 * M + m];
-          if (r2 != 0xFFFF) {
-            p2 = true;
-            const float x2 = sval[f2 * M + m];
             const unsigned char* q2 = ring + (size_t)r2 * RSB + f1 * SEGB;
+            float d = 0.f;
 #pragma unroll
             for (int u = 0; u < SEGB / 16; ++u) {
-              float w[PER];
-              unpack16<T>(*(const uint4*)(q2 + u * 16), w, p.dffm);
+              const uint4 w1 = *(const uint4*)(q1 + u * 16);
+              const uint4 w2 = *(const uint4*)(q2 + u * 16);
+              d = dot16_acc<T>(w1, w2, d, p.dffm);
+            }
+            const float x1 = sval[f1], x2 = sval[f2];
+            pv = (x1 == 1.f && x2 == 1.f) ? d : (x1 * x2) * d;
+          }
+        } else {
+          float a[K], bb[K];
 #pragma unroll
-              for (int t = 0; t < PER; ++t) bb[u * PER + t] = fmaf(x2, w[t], bb[u * PER + t]);
+          for (int t = 0; t < K; ++t) { a[t] = 0.f; bb[t] = 0.f; }
+          bool p1 = false, p2 = false;
+          constexpr int PER = 16 / (int)sizeof(T);
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            const int r1 = rpos[f1 * M + m];
+            if (r1 != 0xFFFF) {
+              p1 = true;
+              const float x1 = sval[f1 * M + m];
+              const unsigned char* q1 = ring + (size_t)r1 * RSB + f2 * SEGB;
+#pragma unroll
+              for (int u = 0; u < SEGB / 16; ++u) {
+                float w[PER];
+                unpack16<T>(*(const uint4*)(q1 + u * 16), w, p.dffm);
+#pragma unroll
+                for (int t = 0; t < PER; ++t) a[u * PER + t] = fmaf(x1, w[t], a[u * PER + t]);
+              }
+            }
+            const int r2 = rpos[f2 * M + m];
+            if (r2 != 0xFFFF) {
+              p2 = true;
+              const float x2 = sval[f2 * M + m];
+              const unsigned char* q2 = ring + (size_t)r2 * RSB + f1 * SEGB;
+#pragma unroll
+              for (int u = 0; u < SEGB / 16; ++u) {
+                float w[PER];
+                unpack16<T>(*(const uint4*)(q2 + u * 16), w, p.dffm);
+#pragma unroll
+                for (int t = 0; t < PER; ++t) bb[u * PER + t] = fmaf(x2, w[t], bb[u * PER + t]);
+              }
             }
           }
-        }
-        if (p1 && p2) {  // inactive pairs stay exactly 0 (M:346-351)
+          if (p1 && p2) {  // inactive pairs stay exactly 0 (M:346-351)
 #pragma unroll
-          for (int t = 0; t < K; ++t) pv = fmaf(a[t], bb[t], pv);
+            for (int t = 0; t < K; ++t) pv = fmaf(a[t], bb[t], pv);
+          }
         }
         float* xv = (float*)(sb + L.off_xv);
         xv[1 + pp] = pv;
-      }
-      const double s = warp_sum((double)pv);
-      const int bad = __any_sync(0xffffffffu, !isfinite(pv));
-      if (lane == 0) {
-        ((double*)(sb + L.off_part))[c] = s;
-        ((int*)(sb + L.off_pbad))[c] = bad;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&pdone[xs]);
