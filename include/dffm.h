@@ -184,6 +184,23 @@ int fwq_dequantize(const uint16_t* q, int64_t n, float hmin, float hbucket, floa
                    void* stream);
 
 /*
+ * K9 ragged batch -> padded layout (the batched form of Fe:121-172 examples):
+ * ex_off int64 [n+1] (absolute; this call reads idx/val at ex_off[e] - nnz_base),
+ * cnt u8 [n][n_fields] features per field, idx i32 / val f32 [nnz] in example,
+ * field, slot order  ->  out_idx i32 / out_val f32 [n][n_fields][max_per_field]
+ * (-1 / 0 padding), ready for dffm_forward.  A count above max_per_field or a
+ * count sum that disagrees with ex_off sets DFFM_CONTRACT for that example in
+ * the status word (status_base + e).  Device pointers, async on `stream`.
+ */
+int dffm_unpack_ragged(const int64_t* ex_off, const uint8_t* cnt, const int32_t* idx,
+                       const float* val, int64_t n, int32_t n_fields, int32_t max_per_field,
+                       int64_t nnz_base, int32_t* out_idx, float* out_val, int64_t status_base,
+                       uint64_t* status, void* stream);
+
+/* Kernels launched by this library so far (all devices and threads). */
+int64_t dffm_launch_count(void);
+
+/*
  * K5 feature hashing (H:28-50): out[i] = fnv1a32(bytes[off[i]:off[i+1]]) & (2^bits-1)
  * (bits = 32 returns the raw hash).
  */

@@ -70,6 +70,10 @@ SIGNATURES = {
     "fwq_quantize": (c_int32, [c_void_p, c_int64, c_float, c_float, c_void_p, c_void_p]),
     "fwq_dequantize": (c_int32, [c_void_p, c_int64, c_float, c_float, c_void_p, c_void_p]),
     "fw_hash_fnv1a32": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    "dffm_unpack_ragged": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                     c_int32, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
+                                     c_void_p]),
+    "dffm_launch_count": (c_int64, []),
     "fwp_scratch_bytes": (c_int64, [c_int64]),
     "fwp_diff_count": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, POINTER(c_int64),
                                  c_void_p]),

@@ -1,3 +1,4 @@
+#include <atomic>
 // Library-wide C ABI helpers: error text, device queries.
 #include <stdarg.h>
 #include <stdio.h>
@@ -25,6 +26,9 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 static std::mutex g_mu;
 static std::unordered_map<int, int> g_sms, g_smem;
+
+static std::atomic<long long> g_launches{0};
+void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 int sm_count_current() {
   int dev = 0;
@@ -93,3 +97,5 @@ int dffm_device_sm_count(int device) {
 }
 
 }  // extern "C"
+
+extern "C" int64_t dffm_launch_count(void) { return (int64_t)dffm::g_launches.load(); }

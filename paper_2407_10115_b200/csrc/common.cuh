@@ -17,6 +17,9 @@ int max_smem_optin_current();
 // Raise the kernel's dynamic-smem limit to the device opt-in maximum (once per
 // kernel and device) and return resident blocks/SM for this smem size (cached).
 int kernel_occupancy(const void* func, int threads, int smem, int* occ);
+// Count of kernels this library has launched (all devices, all threads):
+// dffm_launch_count() reports it, so a bench can state its own launches.
+void note_launches(int k);
 
 #define DFFM_CUDA_TRY(expr, what)                 \
   do {                                            \

@@ -250,7 +250,7 @@ static int launch_ctx(CtxKernel kern, const CtxParams& q, int smem, cudaStream_t
   if (rc) return rc;
   const int64_t nunits = q.R * ((q.C + q.cblk - 1) / q.cblk);
   const int64_t grid = std::min<int64_t>(nunits, (int64_t)sm_count_current() * occ);
-  kern<<<(unsigned)grid, FWD_THREADS, smem, s>>>(q);
+  note_launches(1), kern<<<(unsigned)grid, FWD_THREADS, smem, s>>>(q);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(ctx)");
   return DFFM_OK;
 }

@@ -128,7 +128,7 @@ extern "C" int fw_eval_stream(const double* probs, const uint8_t* labels, int64_
                   "cudaFuncSetAttribute(eval)");
     configured = 1;
   }
-  eval_window_kernel<<<(unsigned)n_win, EV_THREADS, smem, (cudaStream_t)stream>>>(
+  note_launches(1), eval_window_kernel<<<(unsigned)n_win, EV_THREADS, smem, (cudaStream_t)stream>>>(
       probs, labels, n, window, n_full, auc_out, loss_out);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(eval)");
   return DFFM_OK;

@@ -44,7 +44,7 @@ int launch_forward_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s
   if (rc) return rc;
   const int64_t ntiles = (p.n + p.TE - 1) / p.TE;
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current() * occ);
-  kern<<<(unsigned)grid, FWD_THREADS, smem, s>>>(p);
+  note_launches(1), kern<<<(unsigned)grid, FWD_THREADS, smem, s>>>(p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward)");
   return DFFM_OK;
 }
@@ -73,7 +73,7 @@ int launch_forward_tma_t(const TmaParams& q, int K, int smem, cudaStream_t s) {
   if (rc) return rc;
   const int64_t ntiles = (q.f.n + q.f.TE - 1) / q.f.TE;
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current() * occ);
-  kern<<<(unsigned)grid, TMA_THREADS, smem, s>>>(q);
+  note_launches(1), kern<<<(unsigned)grid, TMA_THREADS, smem, s>>>(q);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_tma)");
   return DFFM_OK;
 }
@@ -108,7 +108,7 @@ int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_
   if (rc) return rc;
   const int64_t ntiles = (p.n + p.TE - 1) / p.TE;
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current() * occ);
-  kern<<<(unsigned)grid, WS_THREADS, smem, s>>>(p);
+  note_launches(1), kern<<<(unsigned)grid, WS_THREADS, smem, s>>>(p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_ws)");
   return DFFM_OK;
 }
@@ -146,7 +146,7 @@ int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s) {
   if (rc) return rc;
   const int64_t ntiles = (p.n + p.TE - 1) / p.TE;
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current() * occ);
-  kern<<<(unsigned)grid, RW_THREADS, smem, s>>>(p);
+  note_launches(1), kern<<<(unsigned)grid, RW_THREADS, smem, s>>>(p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rows)");
   return DFFM_OK;
 }
@@ -176,7 +176,7 @@ int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int sme
   if (rc) return rc;
   const int64_t ntiles = (q.f.n + q.f.TE - 1) / q.f.TE;
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current());
-  kern<<<(unsigned)grid, G4_THREADS, smem, s>>>(tm, q);
+  note_launches(1), kern<<<(unsigned)grid, G4_THREADS, smem, s>>>(tm, q);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_g4)");
   return DFFM_OK;
 }
@@ -208,7 +208,7 @@ int launch_forward_rowstage_t(const FwdParams& p, int K, int NB, int smem, cudaS
   int rc = kernel_occupancy((const void*)kern, RS_THREADS, smem, &occ);
   if (rc) return rc;
   const int64_t grid = std::min<int64_t>(p.n, (int64_t)sm_count_current() * occ);
-  kern<<<(unsigned)grid, RS_THREADS, smem, s>>>(p);
+  note_launches(1), kern<<<(unsigned)grid, RS_THREADS, smem, s>>>(p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rowstage)");
   return DFFM_OK;
 }
@@ -243,7 +243,7 @@ int launch_forward_rsw_t(const FwdParams& p, const RswSmem& L, int K, cudaStream
   if (rc) return rc;
   const int64_t grid = std::min<int64_t>(p.n, (int64_t)sm_count_current());
   if (grid <= 0) return DFFM_OK;
-  kern<<<(unsigned)grid, RSW_THREADS, L.total, s>>>(p, L);
+  note_launches(1), kern<<<(unsigned)grid, RSW_THREADS, L.total, s>>>(p, L);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rsw)");
   return DFFM_OK;
 }

@@ -32,7 +32,7 @@ extern "C" int fw_hash_fnv1a32(const uint8_t* bytes, const int64_t* offsets, int
   const uint32_t mask = bits == 32 ? 0xFFFFFFFFu : ((1u << bits) - 1u);
   const int64_t sms = sm_count_current();
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, sms * 8));
-  fnv1a_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(bytes, offsets, n, mask, out);
+  note_launches(1), fnv1a_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(bytes, offsets, n, mask, out);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(fw_hash_fnv1a32)");
   return DFFM_OK;
 }

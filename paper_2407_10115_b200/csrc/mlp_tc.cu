@@ -391,7 +391,7 @@ __global__ void tc_prep_weights_kernel(const float* __restrict__ W, int K, int N
 int launch_tc_prep_weights(const float* W, int K, int N, int Kp, float* dst, cudaStream_t s) {
   const int64_t total = (int64_t)Kp * N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
-  tc_prep_weights_kernel<<<blocks, 256, 0, s>>>(W, K, N, Kp, dst);
+  note_launches(1), tc_prep_weights_kernel<<<blocks, 256, 0, s>>>(W, K, N, Kp, dst);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(tc_prep_weights)");
   return DFFM_OK;
 }
@@ -402,7 +402,7 @@ int launch_mlp_tc(const CUtensorMap& tmx, const MlpTcParams& p, int smem, cudaSt
   if (rc) return rc;
   const int64_t ntiles = (p.rows + TC_M - 1) / TC_M;
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sm_count_current());
-  mlp_tc_kernel<<<(unsigned)grid, TC_THREADS, smem, s>>>(tmx, p);
+  note_launches(1), mlp_tc_kernel<<<(unsigned)grid, TC_THREADS, smem, s>>>(tmx, p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(mlp_tc)");
   return DFFM_OK;
 }

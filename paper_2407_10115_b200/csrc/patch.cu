@@ -239,9 +239,9 @@ extern "C" int fwp_diff_count(const uint8_t* old_, int64_t old_len, const uint8_
   int64_t* cnt_e = cnt_s + nb;
   int64_t* tot = cnt_e + nb;
   PatchIn in{old_, old_len, new_, new_len};
-  patch_count_kernel<<<(unsigned)nb, PB_THREADS, 0, s>>>(in, cnt_s, cnt_e);
-  scan_i64_kernel<<<1, 1024, 0, s>>>(cnt_s, nb, tot);
-  scan_i64_kernel<<<1, 1024, 0, s>>>(cnt_e, nb, tot + 1);
+  note_launches(1), patch_count_kernel<<<(unsigned)nb, PB_THREADS, 0, s>>>(in, cnt_s, cnt_e);
+  note_launches(1), scan_i64_kernel<<<1, 1024, 0, s>>>(cnt_s, nb, tot);
+  note_launches(1), scan_i64_kernel<<<1, 1024, 0, s>>>(cnt_e, nb, tot + 1);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(patch count)");
   int64_t h[2];
   DFFM_CUDA_TRY(cudaMemcpyAsync(h, tot, 16, cudaMemcpyDeviceToHost, s), "copy(patch count)");
@@ -262,7 +262,7 @@ extern "C" int fwp_diff_ops(const uint8_t* old_, int64_t old_len, const uint8_t*
   const int64_t nb = n_blocks(new_len);
   const int64_t* off_s = (const int64_t*)scratch;
   PatchIn in{old_, old_len, new_, new_len};
-  patch_ops_kernel<<<(unsigned)nb, PB_THREADS, 0, (cudaStream_t)stream>>>(in, off_s, off_s + nb,
+  note_launches(1), patch_ops_kernel<<<(unsigned)nb, PB_THREADS, 0, (cudaStream_t)stream>>>(in, off_s, off_s + nb,
                                                                           starts, ends);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(patch ops)");
   return DFFM_OK;
@@ -276,9 +276,9 @@ extern "C" int fwp_encode_size(const int64_t* starts, const int64_t* ends, int64
   if (n_ops == 0) return DFFM_OK;
   const cudaStream_t s = (cudaStream_t)stream;
   const int grid = (int)std::min<int64_t>((n_ops + 255) / 256, (int64_t)sm_count_current() * 8);
-  patch_size_kernel<<<grid, 256, 0, s>>>(starts, ends, n_ops, offsets);
+  note_launches(1), patch_size_kernel<<<grid, 256, 0, s>>>(starts, ends, n_ops, offsets);
   int64_t* tot = (int64_t*)scratch;
-  scan_i64_kernel<<<1, 1024, 0, s>>>(offsets, n_ops, tot);
+  note_launches(1), scan_i64_kernel<<<1, 1024, 0, s>>>(offsets, n_ops, tot);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(patch size)");
   DFFM_CUDA_TRY(cudaMemcpyAsync(total_host, tot, 8, cudaMemcpyDeviceToHost, s), "copy(size)");
   DFFM_CUDA_TRY(cudaStreamSynchronize(s), "sync(patch size)");
@@ -289,7 +289,7 @@ extern "C" int fwp_encode(const uint8_t* new_, const int64_t* starts, const int6
                           const int64_t* offsets, int64_t n_ops, uint8_t* out, void* stream) {
   if (n_ops == 0) return DFFM_OK;
   const int grid = (int)std::min<int64_t>((n_ops * 32 + 255) / 256, (int64_t)sm_count_current() * 16);
-  patch_encode_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(new_, starts, ends, offsets, n_ops,
+  note_launches(1), patch_encode_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(new_, starts, ends, offsets, n_ops,
                                                               out);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(patch encode)");
   return DFFM_OK;
@@ -337,7 +337,7 @@ extern "C" int fwp_scatter(uint8_t* dst, const uint8_t* src, const int64_t* dst_
                            void* stream) {
   if (n_ops == 0) return DFFM_OK;
   const int grid = (int)std::min<int64_t>((n_ops * 32 + 255) / 256, (int64_t)sm_count_current() * 16);
-  patch_scatter_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dst, src, dst_off, src_off, len,
+  note_launches(1), patch_scatter_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dst, src, dst_off, src_off, len,
                                                                n_ops);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(patch scatter)");
   return DFFM_OK;

@@ -139,9 +139,9 @@ extern "C" int fwq_minmax(const float* w, int64_t n, float* minmax_out, uint64_t
   if (!w || !minmax_out || !first_nonfinite) { set_error("null buffer"); return DFFM_CONTRACT; }
   cudaStream_t s = (cudaStream_t)stream;
   uint32_t* mm = (uint32_t*)minmax_out;
-  minmax_init<<<1, 1, 0, s>>>(mm);
-  minmax_kernel<<<stream_grid(n), 256, 0, s>>>(w, n, mm, first_nonfinite);
-  minmax_finish<<<1, 1, 0, s>>>(mm);
+  note_launches(1), minmax_init<<<1, 1, 0, s>>>(mm);
+  note_launches(1), minmax_kernel<<<stream_grid(n), 256, 0, s>>>(w, n, mm, first_nonfinite);
+  note_launches(1), minmax_finish<<<1, 1, 0, s>>>(mm);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(fwq_minmax)");
   return DFFM_OK;
 }
@@ -170,7 +170,7 @@ extern "C" int fwq_quantize(const float* w, int64_t n, float hmin, float hbucket
                             void* stream) {
   if (n < 0 || (n && (!w || !q))) { set_error("bad quantize args"); return DFFM_CONTRACT; }
   if (!n) return DFFM_OK;
-  quant_kernel<<<stream_grid(n), 256, 0, (cudaStream_t)stream>>>(w, n, (double)hmin,
+  note_launches(1), quant_kernel<<<stream_grid(n), 256, 0, (cudaStream_t)stream>>>(w, n, (double)hmin,
                                                                   (double)hbucket, q);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(fwq_quantize)");
   return DFFM_OK;
@@ -180,7 +180,7 @@ extern "C" int fwq_dequantize(const uint16_t* q, int64_t n, float hmin, float hb
                               void* stream) {
   if (n < 0 || (n && (!q || !out))) { set_error("bad dequantize args"); return DFFM_CONTRACT; }
   if (!n) return DFFM_OK;
-  dequant_kernel<<<stream_grid(n), 256, 0, (cudaStream_t)stream>>>(q, n, hmin, hbucket, out);
+  note_launches(1), dequant_kernel<<<stream_grid(n), 256, 0, (cudaStream_t)stream>>>(q, n, hmin, hbucket, out);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(fwq_dequantize)");
   return DFFM_OK;
 }

@@ -824,7 +824,7 @@ extern "C" int dffm_train_sequential(const dffm_model* model, const dffm_train_s
   if (C == 1) {
     rc = kernel_occupancy((const void*)train_kernel<1>, TR_THREADS, smem, &occ);
     if (rc) return rc;
-    train_kernel<1><<<1, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
+    note_launches(1), train_kernel<1><<<1, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
   } else {
     // one thread-block cluster of C CTAs on C SMs (DSMEM exchange per example)
     rc = kernel_occupancy((const void*)train_kernel<TR_CLUSTER>, TR_THREADS, smem, &occ);
@@ -906,7 +906,7 @@ extern "C" int dffm_train_hogwild(const dffm_model* model, const dffm_train_stat
   // concurrent workers only: a CTA that could not be resident would run later,
   // in series with the others
   const int64_t W = std::min<int64_t>({(int64_t)n_workers, (int64_t)occ * sm_count_current(), n});
-  train_kernel<1><<<(unsigned)W, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
+  note_launches(1), train_kernel<1><<<(unsigned)W, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(train hogwild)");
   return DFFM_OK;
 }

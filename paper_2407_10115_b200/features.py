@@ -74,3 +74,60 @@ def unpack_row(idx_row, val_row):
         if sel.any():
             out.append((f, idx_row[f][sel].astype(np.int64), val_row[f][sel].astype(np.float64)))
     return out
+
+
+class RaggedBatch:
+    """The batched canonical form of ParsedExamples (Fe:121-172), CSR over
+    (example, field): ``ex_off`` int64 [n+1] (example e's features are
+    ``idx[ex_off[e]:ex_off[e+1]]``), ``cnt`` uint8 [n, F] (features per field,
+    0 = absent), ``idx`` int32 / ``val`` float32 [nnz] in example, field, slot
+    order.  It carries only present features, so it is the cheaper host->device
+    format when fields are sparse (cfg2: 47.4 of 72 padded slots) --
+    ``dffm_unpack_ragged`` (K9) expands it to the padded layout on the device.
+    Arrays may be numpy or (pinned) torch tensors."""
+
+    def __init__(self, ex_off, cnt, idx, val, max_per_field: int):
+        self.ex_off, self.cnt, self.idx, self.val = ex_off, cnt, idx, val
+        self.max_per_field = int(max_per_field)
+
+    @property
+    def n(self) -> int:
+        return int(self.cnt.shape[0])
+
+    @property
+    def n_fields(self) -> int:
+        return int(self.cnt.shape[1])
+
+    def nbytes(self) -> int:
+        return sum(int(a.nbytes if hasattr(a, "nbytes") else a.numel() * a.element_size())
+                   for a in (self.ex_off, self.cnt, self.idx, self.val))
+
+    @classmethod
+    def from_padded(cls, idx, val) -> "RaggedBatch":
+        """Padded [n, F, M] (slots 0..m_f-1 live, then -1) -> ragged (numpy)."""
+        idx = np.asarray(idx)
+        val = np.asarray(val)
+        n, F, M = idx.shape
+        live = idx >= 0
+        cnt = live.sum(axis=2).astype(np.uint8)
+        ex_off = np.zeros(n + 1, np.int64)
+        np.cumsum(cnt.sum(axis=1, dtype=np.int64), out=ex_off[1:])
+        return cls(ex_off, cnt, np.ascontiguousarray(idx[live], dtype=np.int32),
+                   np.ascontiguousarray(val[live], dtype=np.float32), M)
+
+    @classmethod
+    def from_examples(cls, examples, n_fields: int, max_per_field: int | None = None):
+        idx, val, labels = pack_examples(examples, n_fields, max_per_field)
+        return cls.from_padded(idx, val), labels
+
+    def to_padded(self):
+        """Host-side inverse (tests): -> (idx int32 [n,F,M], val f32 [n,F,M])."""
+        cnt = np.asarray(self.cnt)
+        n, F = cnt.shape
+        M = self.max_per_field
+        idx = np.full((n, F, M), -1, np.int32)
+        val = np.zeros((n, F, M), np.float32)
+        live = np.arange(M)[None, None, :] < cnt[:, :, None]
+        idx[live] = np.asarray(self.idx)
+        val[live] = np.asarray(self.val)
+        return idx, val

@@ -422,6 +422,17 @@ def predict_batch(idx, val, store: WeightStore, out: torch.Tensor | None = None,
     return out
 
 
+def _chunk_bounds(n: int, chunk: int):
+    """[c0, c1) chunks of a host batch: sizes ramp up chunk/8, chunk/4, ...,
+    chunk so the first (unoverlapped) host->device copy is short."""
+    out, c0, sz = [], 0, max(1, chunk // 8)
+    while c0 < n:
+        c1 = min(n, c0 + sz)
+        out.append((c0, c1))
+        c0, sz = c1, min(chunk, sz * 2)
+    return out
+
+
 class HostPredictor:
     """Public host-buffer entry point: pinned host idx/val in, host probs out.
 
@@ -458,8 +469,7 @@ class HostPredictor:
         with torch.cuda.stream(ks):
             self.status.clear()
         cs.wait_stream(ks)
-        for i, c0 in enumerate(range(0, n, self.chunk)):
-            c1 = min(n, c0 + self.chunk)
+        for i, (c0, c1) in enumerate(_chunk_bounds(n, self.chunk)):
             b = i & 1
             ib = self.idx_buf[b][: c1 - c0]
             vb = self.val_buf[b][: c1 - c0]
@@ -473,6 +483,73 @@ class HostPredictor:
             with torch.cuda.stream(ks):
                 ks.wait_event(h2d_done[b])
                 rc = lib.dffm_forward(cm, ib.data_ptr(), vb.data_ptr(), M, c1 - c0,
+                                      pb.data_ptr(), None, c0, self.status.ptr(), ks.cuda_stream)
+                _lib.check(rc, "dffm_forward")
+                self.launches += 1
+                out_host[c0:c1].copy_(pb, non_blocking=True)
+                free[b].record(ks)
+        with torch.cuda.stream(ks):
+            self.status.fetch_async()
+        ks.synchronize()
+        if check:
+            self.status.raise_if_set("forward: ")
+        return out_host
+
+
+    def predict_ragged(self, batch, out_host: torch.Tensor, check: bool = True) -> torch.Tensor:
+        """Host-buffer entry point for ragged batches (``features.RaggedBatch``
+        of pinned torch tensors): per chunk the present features only are
+        copied (ex_off, cnt, idx, val slices), K9 (``dffm_unpack_ragged``)
+        expands them to the padded layout in HBM and K1 scores them; copies of
+        chunk i+1 overlap chunk i's kernels, as in ``__call__``."""
+        n, F = int(batch.cnt.shape[0]), int(batch.cnt.shape[1])
+        M = batch.max_per_field
+        lib = _lib.lib()
+        cm = self.store.c_model_ref()
+        cs, ks = self.copy_stream, self.compute_stream
+        dev = self.store.device
+        if not hasattr(self, "rg_off"):
+            self.rg_off = [torch.empty(self.chunk + 1, dtype=torch.int64, device=dev)
+                           for _ in range(2)]
+            self.rg_cnt = [torch.empty((self.chunk, F), dtype=torch.uint8, device=dev)
+                           for _ in range(2)]
+            self.rg_cap = 0
+        off_h = batch.ex_off
+        bounds = _chunk_bounds(n, self.chunk)
+        nnz_max = max(int(off_h[c1]) - int(off_h[c0]) for c0, c1 in bounds) if bounds else 0
+        if nnz_max > self.rg_cap:
+            self.rg_cap = nnz_max
+            self.rg_idx = [torch.empty(nnz_max, dtype=torch.int32, device=dev) for _ in range(2)]
+            self.rg_val = [torch.empty(nnz_max, dtype=torch.float32, device=dev) for _ in range(2)]
+        h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        with torch.cuda.stream(ks):
+            self.status.clear()
+        cs.wait_stream(ks)
+        for i, (c0, c1) in enumerate(bounds):
+            b = i & 1
+            z0, z1 = int(off_h[c0]), int(off_h[c1])
+            ob, cb = self.rg_off[b][: c1 - c0 + 1], self.rg_cnt[b][: c1 - c0]
+            ib, vb = self.rg_idx[b][: z1 - z0], self.rg_val[b][: z1 - z0]
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(free[b])
+                ob.copy_(off_h[c0:c1 + 1], non_blocking=True)
+                cb.copy_(batch.cnt[c0:c1], non_blocking=True)
+                ib.copy_(batch.idx[z0:z1], non_blocking=True)
+                vb.copy_(batch.val[z0:z1], non_blocking=True)
+                h2d_done[b].record(cs)
+            pi = self.idx_buf[b][: c1 - c0]
+            pv = self.val_buf[b][: c1 - c0]
+            pb = self.prob_buf[b][: c1 - c0]
+            with torch.cuda.stream(ks):
+                ks.wait_event(h2d_done[b])
+                _lib.check(lib.dffm_unpack_ragged(ob.data_ptr(), cb.data_ptr(), ib.data_ptr(),
+                                                  vb.data_ptr(), c1 - c0, F, M, z0,
+                                                  pi.data_ptr(), pv.data_ptr(), c0,
+                                                  self.status.ptr(), ks.cuda_stream),
+                           "dffm_unpack_ragged")
+                rc = lib.dffm_forward(cm, pi.data_ptr(), pv.data_ptr(), M, c1 - c0,
                                       pb.data_ptr(), None, c0, self.status.ptr(), ks.cuda_stream)
                 _lib.check(rc, "dffm_forward")
                 self.launches += 1

@@ -1,0 +1,93 @@
+"""K9 ragged -> padded unpack (dffm_unpack_ragged) and the ragged host-buffer
+path (HostPredictor.predict_ragged): bit-exact against the padded layout and
+the padded path; contract violations reported at the first bad example."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fieldwise_oracle as fo
+from paper_2407_10115_b200 import _lib, configs, synth
+from paper_2407_10115_b200.errors import ContractError
+from paper_2407_10115_b200.features import RaggedBatch
+from paper_2407_10115_b200.model import HostPredictor, ModelConfig, StatusWord, WeightStore, \
+    predict_batch
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+def _unpack(rb, status_base=0):
+    n, F, M = rb.n, rb.n_fields, rb.max_per_field
+    t = [torch.as_tensor(a).to(DEV) for a in (rb.ex_off, rb.cnt, rb.idx, rb.val)]
+    oi = torch.empty((n, F, M), dtype=torch.int32, device=DEV)
+    ov = torch.empty((n, F, M), dtype=torch.float32, device=DEV)
+    st = StatusWord(DEV)
+    st.clear()
+    _lib.check(_lib.lib().dffm_unpack_ragged(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(),
+                                             t[3].data_ptr(), n, F, M, int(rb.ex_off[0]),
+                                             oi.data_ptr(), ov.data_ptr(), status_base, st.ptr(),
+                                             torch.cuda.current_stream().cuda_stream))
+    st.fetch_async()
+    torch.cuda.synchronize()
+    return oi.cpu().numpy(), ov.cpu().numpy(), st
+
+
+@pytest.mark.parametrize("F,M,n", [(24, 3, 5000), (40, 1, 777), (3, 6, 64), (255, 1, 33)])
+def test_unpack_ragged_bit_exact(F, M, n):
+    rng = np.random.default_rng(F * 31 + M)
+    cnt = rng.integers(0, M + 1, size=(n, F))
+    cnt[::9] = 0
+    idx = np.full((n, F, M), -1, np.int32)
+    val = np.zeros((n, F, M), np.float32)
+    live = np.arange(M)[None, None, :] < cnt[:, :, None]
+    idx[live] = rng.integers(0, 1 << 24, size=int(live.sum()))
+    val[live] = rng.lognormal(size=int(live.sum())).astype(np.float32)
+    rb = RaggedBatch.from_padded(idx, val)
+    oi, ov, st = _unpack(rb)
+    st.raise_if_set()
+    assert np.array_equal(oi, idx) and np.array_equal(ov.view(np.uint32), val.view(np.uint32))
+
+
+def test_unpack_ragged_contract_errors():
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, 100, size=(50, 4, 2)).astype(np.int32)
+    val = np.ones_like(idx, np.float32)
+    rb = RaggedBatch.from_padded(idx, val)
+    bad = RaggedBatch(rb.ex_off, rb.cnt.copy(), rb.idx, rb.val, 2)
+    bad.cnt[23, 1] = 3  # more than max_per_field
+    _, _, st = _unpack(bad, status_base=1000)
+    with pytest.raises(ContractError) as ei:
+        st.raise_if_set()
+    assert ei.value.example == 1023
+    bad = RaggedBatch(rb.ex_off.copy(), rb.cnt, rb.idx, rb.val, 2)
+    bad.ex_off[31:] += 1  # example 30's count sum disagrees with its offsets
+    _, _, st = _unpack(bad)
+    with pytest.raises(ContractError) as ei:
+        st.raise_if_set()
+    assert ei.value.example == 30
+
+
+@pytest.mark.parametrize("wl_name", ["CFG2", "CFG5"])
+def test_host_predictor_ragged_equals_padded(wl_name):
+    """The ragged host path (K9 + K1, chunked, overlapped copies) returns the
+    bits of the padded device run, several chunks with a ragged tail."""
+    wl = getattr(configs, wl_name)
+    bits = 12
+    ost = fo.random_store(wl.n_fields, wl.k, wl.hidden, bits, seed=7, scale=0.05)
+    cfg = ModelConfig(n_fields=wl.n_fields, k=wl.k, hidden_sizes=wl.hidden, hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, "bf16" if wl_name == "CFG5" else "f32",
+                               False)
+    n = 3 * 4096 + 123
+    idx, val = synth.make_examples(wl, n, seed=9, hash_bits=bits)
+    ref = predict_batch(idx, val, st).cpu()
+    rb = RaggedBatch.from_padded(idx.numpy(), val.numpy())
+    rbh = RaggedBatch(*(torch.from_numpy(a).pin_memory() for a in (rb.ex_off, rb.cnt, rb.idx,
+                                                                  rb.val)), rb.max_per_field)
+    hp = HostPredictor(st, n, idx.shape[2], chunk=4096)
+    out = torch.empty(n, dtype=torch.float32).pin_memory()
+    hp.predict_ragged(rbh, out)
+    assert torch.equal(out, ref)
+    out2 = torch.empty(n, dtype=torch.float32).pin_memory()
+    hp(idx.pin_memory(), val.pin_memory(), out2)
+    assert torch.equal(out2, ref)

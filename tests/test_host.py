@@ -92,6 +92,27 @@ def test_pack_examples_canonicalises():
         features.pack_examples([Ex(2, [])], 3)
 
 
+def test_ragged_batch_round_trip():
+    """RaggedBatch (the CSR form K9 unpacks on the device) is lossless against
+    the padded layout, including empty fields and empty examples."""
+    rng = np.random.default_rng(3)
+    n, F, M = 300, 7, 3
+    idx = np.full((n, F, M), -1, np.int32)
+    val = np.zeros((n, F, M), np.float32)
+    cnt = rng.integers(0, M + 1, size=(n, F))
+    cnt[::17] = 0
+    for e in range(n):
+        for f in range(F):
+            c = cnt[e, f]
+            idx[e, f, :c] = np.sort(rng.choice(1000, c, replace=False))
+            val[e, f, :c] = rng.lognormal(size=c)
+    rb = features.RaggedBatch.from_padded(idx, val)
+    assert rb.ex_off[-1] == (idx >= 0).sum() and rb.cnt.dtype == np.uint8
+    assert rb.nbytes() == 8 * (n + 1) + n * F + 8 * int(rb.ex_off[-1])
+    i2, v2 = rb.to_padded()
+    assert np.array_equal(i2, idx) and np.array_equal(v2, val)
+
+
 def test_metrics_match_reference():
     g = load("metrics")
     ev = metrics.StreamingEvaluator(30000)
