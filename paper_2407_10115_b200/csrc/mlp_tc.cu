@@ -142,10 +142,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   uint64_t* full = (uint64_t*)(smem + S * SB);
   uint64_t* aready = full + S;
   uint64_t* empty = aready + S;
-  uint64_t* accf = empty + S;    // [2] TMEM region holds a finished group
+  uint64_t* lready = empty + S;  // [S] split warps: the stage's A_lo is written (every chunk)
+  uint64_t* accf = lready + S;   // [2] TMEM region holds a finished group
   uint64_t* tempty = accf + 2;   // [2] TMEM region drained by the epilogue
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  float* xpart = (float*)(smem + S * SB + (3 * S + 4) * 8 + 16);  // [2][TC_PARTS][TC_M]
+  float* xpart = (float*)(smem + S * SB + (4 * S + 4) * 8 + 16);  // [2][TC_PARTS][TC_M]
   int* xbad = (int*)(xpart + 2 * TC_PARTS * TC_M);                 // [2][TC_PARTS][TC_M]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -154,6 +155,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
       mbar_init(&full[s], 1);
       mbar_init(&aready[s], TC_EPI_WARPS);
       mbar_init(&empty[s], 1);
+      mbar_init(&lready[s], TC_SPLIT_WARPS);
     }
     for (int r = 0; r < 2; ++r) {
       mbar_init(&accf[r], 1);
@@ -201,6 +203,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       uint32_t g = 0, gg = 0;  // chunk counter, accumulation-group counter
+      uint32_t apar = 0;       // per-stage phase bits of aready (used by layer >= 1 chunks only)
       uint32_t d = tmem;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int l = 0; l < NH; ++l) {
@@ -216,7 +219,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
             }
             const int s = (int)(g % S);
             const uint32_t u = g / S;
-            mbar_wait(&aready[s], u & 1);
+            if (l > 0) {  // A chunk written by the epilogue from the previous layer
+              mbar_wait(&aready[s], (apar >> s) & 1u);
+              apar ^= 1u << s;
+            }
+            mbar_wait(&lready[s], u & 1);
             mbar_wait(&full[s], u & 1);
             tc_fence_after();
             const uint32_t st = smem_u32(smem + s * SB);
@@ -246,6 +253,37 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
         }
       }
     }
+  } else if (warp >= 2 + TC_EPI_WARPS) {
+    // ------------------------------------------------------------ split warps
+    // A_lo = x - trunc_tf32(x) of each landed layer-0 X chunk (same swizzled
+    // positions), off the epilogue warps so accumulator drains never hold
+    // the MMAs back; they walk every chunk in order and arrive on lready[s]
+    // for each (layer >= 1 chunks: nothing to split), which keeps the
+    // mbarrier phases of full/lready in lock step with the MMA issuer.
+    const int sw = warp - 2 - TC_EPI_WARPS;
+    uint32_t g = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int l = 0; l < NH; ++l) {
+        const int nck = p.kin[l] >> 4;
+        for (int c = 0; c < nck; ++c, ++g) {
+          const int s = (int)(g % S);
+          mbar_wait(&full[s], (g / S) & 1);
+          if (l == 0) {
+            unsigned char* st = smem + s * SB;
+            const float4* a = (const float4*)st;
+            float4* lo = (float4*)(st + 8192);
+#pragma unroll
+            for (int i = sw * 32 + lane; i < 512; i += 32 * TC_SPLIT_WARPS) {
+              const float4 x = a[i];
+              lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+            }
+            fence_async_smem();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lready[s]);
+        }
+      }
+    }
   } else {
     // ------------------------------------------------------------ epilogue warps
     const int ew = warp - 2;               // 0 .. TC_EPI_WARPS-1
@@ -269,18 +307,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
         for (int gi = 0; gi < ngr; ++gi) {
           const int cend = min(nck, (gi + 1) * TC_GROUP);
           for (int c = gi * TC_GROUP; c < cend; ++c, ++g) {
+            if (l == 0) continue;  // layer 0's A (hi: TMA, lo: split warps)
             const int s = (int)(g % S);
-            mbar_wait(&full[s], (g / S) & 1);
+            mbar_wait(&full[s], (g / S) & 1);  // stage free again (W landed)
             unsigned char* st = smem + s * SB;
-            if (l == 0) {  // A_lo of the landed X chunk (same swizzled positions)
-              const float4* a = (const float4*)st;
-              float4* lo = (float4*)(st + 8192);
-#pragma unroll
-              for (int i = ew * 32 + lane; i < 512; i += 32 * TC_EPI_WARPS) {
-                const float4 x = a[i];
-                lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
-              }
-            } else if (c >= pb0 && c < pb1) {  // this part holds the chunk's 16 columns
+            if (c >= pb0 && c < pb1) {  // this part holds the chunk's 16 columns
               const int cbl = c - pb0;
 #pragma unroll
               for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {

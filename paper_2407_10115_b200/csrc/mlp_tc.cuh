@@ -16,7 +16,12 @@ constexpr int TC_MAXH = 4;      // hidden layers (M:70-71)
 #endif
 constexpr int TC_PARTS = DFFM_TC_PARTS;  // epilogue warps per TMEM lane quadrant (column parts)
 constexpr int TC_EPI_WARPS = 4 * TC_PARTS;
-constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, then epilogue
+#ifndef DFFM_TC_SPLIT_WARPS
+#define DFFM_TC_SPLIT_WARPS 2
+#endif
+constexpr int TC_SPLIT_WARPS = DFFM_TC_SPLIT_WARPS;  // layer-0 A_lo producers
+// warp 0 TMA, warp 1 MMA, then the epilogue warps, then the split warps
+constexpr int TC_THREADS = 64 + 32 * (TC_EPI_WARPS + TC_SPLIT_WARPS);
 constexpr int TC_PART_MAX = 256 / TC_PARTS;  // accumulator columns per epilogue thread
 constexpr int TC_WIDTH_MULT = 16;            // hidden widths: multiples of this, <= 256
 #ifndef DFFM_TC_GROUP
@@ -49,10 +54,10 @@ __host__ __device__ inline int tc_stage_bytes(int nmax) {
   return (16384 + nmax * 128 + 1023) & ~1023;
 }
 // dynamic shared memory: 1 KB alignment slack, stages, barriers
-// (full/aready/empty per stage, accf/tempty per TMEM region), TMEM slot, and
-// the two halves' row exchange (double-buffered by tile)
+// (full/aready/empty/lready per stage, accf/tempty per TMEM region), TMEM
+// slot, and the parts' row exchange (double-buffered by tile)
 __host__ __device__ inline int tc_smem_bytes(int stages, int stage_bytes) {
-  return 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16 + 2 * TC_PARTS * TC_M * 8;
+  return 1024 + stages * stage_bytes + (4 * stages + 4) * 8 + 16 + 2 * TC_PARTS * TC_M * 8;
 }
 
 int launch_mlp_tc(const CUtensorMap& tmx, const MlpTcParams& p, int smem, cudaStream_t s);

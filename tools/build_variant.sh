@@ -6,7 +6,7 @@ set -e
 NAME=$1; shift
 OUT=build_var/$NAME
 mkdir -p $OUT
-SRC=paper_2407_10115_b200/csrc
+SRC=${SRC:-paper_2407_10115_b200/csrc}
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $*"
 pids=()
 for f in $SRC/*.cu; do
