@@ -15,7 +15,7 @@ for f in ["bench.json", "bench_cfg5.json", "bench_cfg4.json", "bench_cfg1.json",
     if os.path.exists(os.path.join(src, f)):
         shutil.copy(os.path.join(src, f), os.path.join(dst, f"{tag}_{f}"))
 summ = {}
-for rep, name in [("k1_full", "k1_cfg2_fwd_ws"), ("k1_cfg5_full", "k1_cfg5_rowstage_mlp_tc"),
+for rep, name in [("k1_full", "k1_cfg2_fwd_ws"), ("k1_cfg5_full", "k1_cfg5_rsw_mlp_tc"),
                   ("k2_full", "k2_train")]:
     path = os.path.join(src, rep + ".ncu-rep")
     if not os.path.exists(path):
@@ -34,9 +34,10 @@ traffic = {"_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of 
                     "kernel (ncu --set full, profiles/*_ncu.json)"}
 if "k1_cfg2_fwd_ws" in summ:
     traffic["cfg2_deepffm_fwd"] = summ["k1_cfg2_fwd_ws"][0]["dram_bytes_per_launch"]
-if "k1_cfg5_rowstage_mlp_tc" in summ:
-    ks = summ["k1_cfg5_rowstage_mlp_tc"]
+if "k1_cfg5_rsw_mlp_tc" in summ:
+    ks = summ["k1_cfg5_rsw_mlp_tc"]
     traffic["cfg5_large_bf16_per_slice"] = sum(k["dram_bytes_per_launch"] for k in ks)
+    traffic["cfg5_large_bf16"] = ks[0]["dram_bytes_per_launch"]  # the gather (dominant) kernel
 with open(os.path.join(dst, "ncu_traffic.json"), "w") as fh:
     json.dump(traffic, fh, indent=1)
 print("copied; traffic:", traffic)
