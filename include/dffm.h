@@ -197,6 +197,31 @@ int dffm_unpack_ragged(const int64_t* ex_off, const uint8_t* cnt, const int32_t*
                        int64_t nnz_base, int32_t* out_idx, float* out_val, int64_t status_base,
                        uint64_t* status, void* stream);
 
+/*
+ * K10 text parse (Fe:175-235, H:28-50): lines text[line_off[i]:line_off[i+1]]
+ * (no newline) of the reference's example grammar -> canonical hashed features.
+ *   fw_parse_scratch_bytes -> device scratch size for (n_lines, text_bytes)
+ *   fw_parse_lines: labels u8 [n], line_status i32 [n] (0 ok, else the kind of
+ *     ParseError: 1 label, 2 no blocks, 3 empty block, 4 unknown field, 5 bad
+ *     value, 6 non-finite value, 7 raw index out of range, 8 unsupported
+ *     (non-ASCII whitespace / non-ASCII digits), 9 > 1024 features, 10 > 255
+ *     features in one field), cnt u8 [n][n_fields], ex_off int64 [n+1]
+ *     (ex_off[n] = total features), max_cnt (largest field count, device i32).
+ *     Schema: field names as bytes[name_off[f]:name_off[f+1]], numeric u8 [F].
+ *   fw_parse_emit (after reading ex_off[n]): idx i32 / val f32 [nnz] (val64
+ *     f64 optional) in field-id order, ascending index within a field.
+ * Failed lines hold no features; the caller raises at the first failed line.
+ */
+int64_t fw_parse_scratch_bytes(int64_t n_lines, int64_t text_bytes);
+int fw_parse_lines(const uint8_t* text, const int64_t* line_off, int64_t n_lines,
+                   int64_t text_bytes, const uint8_t* names, const int32_t* name_off,
+                   const uint8_t* numeric, int32_t n_fields, int32_t hash_bits, void* scratch,
+                   uint8_t* labels, int32_t* line_status, uint8_t* cnt, int64_t* ex_off,
+                   int32_t* max_cnt, void* stream);
+int fw_parse_emit(const int64_t* line_off, int64_t n_lines, int64_t text_bytes,
+                  const void* scratch, const int64_t* ex_off, int32_t* idx, float* val,
+                  double* val64_opt, void* stream);
+
 /* Kernels launched by this library so far (all devices and threads). */
 int64_t dffm_launch_count(void);
 

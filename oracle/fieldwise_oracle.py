@@ -754,3 +754,110 @@ def apply_patch(old, patch) -> bytes:
     if fnv1a64(out) != dst:
         raise OracleCorruptionError("target digest mismatch")
     return bytes(out)
+
+
+# text parsing (Fe:1-235) -- checker for K10 (fw_parse_lines)
+# --------------------------------------------------------------------------
+
+
+class OracleParseError(Exception):
+    pass
+
+
+# str.split() / str.strip() whitespace restricted to ASCII (Fe:190, Fe:222: the
+# K10 contract rejects lines holding non-ASCII bytes that could decode to
+# Unicode whitespace; every ASCII byte str.isspace() accepts is here)
+ASCII_WS = b" \t\n\r\x0b\x0c\x1c\x1d\x1e\x1f"
+
+
+def _split_ws(b: bytes):
+    out, cur = [], bytearray()
+    for c in b:
+        if c in ASCII_WS:
+            if cur:
+                out.append(bytes(cur))
+                cur = bytearray()
+        else:
+            cur.append(c)
+    if cur:
+        out.append(bytes(cur))
+    return out
+
+
+def parse_line(line: bytes, field_names, numeric, hash_bits: int):
+    """Restatement of parse_example (Fe:221-235) + _parse_blocks (Fe:175-219)
+    over the line's UTF-8 bytes.  Returns (label, {field_id: {index: value}})
+    with fields in first-appearance order; raises OracleParseError where the
+    reference raises ParseError."""
+    ids = {n.encode("utf-8"): i for i, n in enumerate(field_names)}
+    numeric = {n.encode("utf-8") for n in numeric}
+    segs = line.split(b"|")
+    head = segs[0].strip(ASCII_WS)
+    if head == b"1":
+        label = 1
+    elif head in (b"0", b"-1"):
+        label = 0
+    else:
+        raise OracleParseError("malformed label")  # Fe:229
+    if len(segs) < 2:
+        raise OracleParseError("no field blocks")  # Fe:231
+    max_index = 1 << hash_bits
+    per = {}
+    for seg in segs[1:]:
+        atoms = _split_ws(seg)
+        if not atoms:
+            raise OracleParseError("empty field block")  # Fe:191
+        name = atoms[0]
+        if name not in ids:
+            raise OracleParseError("unknown field")  # InputSchema.field_id
+        fid = ids[name]
+        feats = per.setdefault(fid, {})
+        for atom in atoms[1:]:
+            token, sep, raw = atom.partition(b":")
+            if sep:
+                try:
+                    value = float(raw.decode("utf-8"))  # Fe:201
+                except (ValueError, UnicodeDecodeError):
+                    raise OracleParseError("bad value") from None
+                if not math.isfinite(value):
+                    raise OracleParseError("non-finite value")
+            else:
+                value = 1.0
+            if token.startswith(b"@") and len(token) > 1 and token[1:].isdigit():
+                index = int(token[1:])  # Fe:209-214
+                if index >= max_index:
+                    raise OracleParseError("raw index out of range")
+            else:
+                index = fnv1a32(name + FIELD_TOKEN_SEP + token) & (max_index - 1)  # H:43-50
+                if name in numeric:
+                    value = math.log1p(value) if value > 0 else value  # Fe:33-39
+            feats[index] = feats.get(index, 0.0) + value  # Fe:219
+    return label, per
+
+
+def parse_lines_ragged(lines, field_names, numeric, hash_bits: int):
+    """Lines -> (ok [n] bool, labels [n], ex_off [n+1], cnt [n,F], idx [nnz], val64 [nnz]):
+    the canonical features of every parsable line in field-id order, indices
+    ascending within a field (the layout K10 writes); failed lines hold none."""
+    F = len(field_names)
+    n = len(lines)
+    ok = np.zeros(n, bool)
+    labels = np.zeros(n, np.uint8)
+    cnt = np.zeros((n, F), np.int64)
+    idx, val, off = [], [], [0]
+    for i, ln in enumerate(lines):
+        try:
+            lab, per = parse_line(ln, field_names, numeric, hash_bits)
+        except OracleParseError:
+            off.append(off[-1])
+            continue
+        ok[i] = True
+        labels[i] = lab
+        for fid in sorted(per):
+            items = sorted(per[fid].items())
+            cnt[i, fid] = len(items)
+            idx += [k for k, _ in items]
+            val += [v for _, v in items]
+        off.append(len(idx))
+    return (ok, labels, np.array(off, np.int64), cnt, np.array(idx, np.int64),
+            np.array(val, np.float64))

@@ -1,0 +1,510 @@
+// K10: text example lines -> canonical hashed features (Fe:175-235, H:28-50),
+// the step before the forward / training path.
+//
+// Line grammar (Fe:3-10): label ws '|' field_name (ws token[':' value])* ...
+// The reference parses one line at a time in Python (~340 µs per line);
+// here every line is independent:
+//   A  fw_parse_lines, thread per line: label (Fe:223-229), '|' blocks,
+//      ASCII-whitespace atoms (Fe:190), field-name lookup, values (Python
+//      float() grammar: sign, digits with single '_' separators, '.', exponent;
+//      non-finite rejected, Fe:201-208), raw '@digits' indices (Fe:209-214),
+//      FNV-1a 32 of name 0x1F token masked to hash_bits (H:43-50), log1p for
+//      numeric fields (Fe:33-39) -> raw (field, index, value) entries in token
+//      order into a per-line scratch window (a token needs >= 2 bytes of line,
+//      so len/2 + 1 entries always fit).
+//   B  warp per line: bitonic sort of (field, index, token position) keys in
+//      shared memory (<= 1024 features per line, else PS_TOO_LONG), duplicates
+//      summed in occurrence order in f64 (Fe:219), per-field counts (<= 255);
+//   C  exclusive scan of the per-line feature counts -> ex_off;
+//   D  fw_parse_emit, warp per line: the canonical entries -> the ragged batch
+//      (ex_off, cnt, idx i32, val f32 and optionally val f64) that K9 / K1 take.
+// Values: exactly rounded on Clinger's fast path (<= 19 significant digits
+// whose mantissa fits 2^53 and |exp10| <= 22 -- every short decimal); else a
+// double-double product with 10^e (error ~2^-100 before the final rounding).
+// Lines holding a byte sequence that decodes to Unicode (non-ASCII)
+// whitespace, or non-ASCII bytes in a value or raw index, are rejected with
+// PARSE_UNSUPPORTED instead of being tokenised differently from str.split().
+#include <math.h>
+
+#include "common.cuh"
+#include "pow10_dd.h"
+
+namespace dffm {
+
+enum ParseStatus {
+  PS_OK = 0, PS_LABEL = 1, PS_NO_BLOCKS = 2, PS_EMPTY_BLOCK = 3, PS_UNKNOWN_FIELD = 4,
+  PS_BAD_VALUE = 5, PS_NONFINITE = 6, PS_RAW_RANGE = 7, PS_UNSUPPORTED = 8, PS_TOO_LONG = 9,
+  PS_FIELD_CAP = 10, PS_BLANK = 11
+};
+
+constexpr int PB_WARPS = 2;
+constexpr int PB_CAP = 1024;  // raw entries per line the sort stage takes
+
+__device__ __forceinline__ bool is_ws(uint32_t c) {
+  return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f);
+}
+
+// exact m * 10^e10 for m < 2^53, |e10| <= 22 (Clinger: both operands exact, one
+// IEEE rounding); else the double-double product (m_hi + m_lo)(t_hi + t_lo)
+// rounded once (relative error ~2^-100 before that rounding).  Results below
+// ~1e-290 are scaled through 10^-60 (a second rounding: subnormals may differ
+// by one ulp).
+__device__ double decimal_to_double(uint64_t m, int e10) {
+  if (m == 0) return 0.0;
+  if (m < (1ull << 53) && e10 >= -22 && e10 <= 22) {
+    const double a = (double)m;
+    return e10 >= 0 ? a * c_pow10_dd[e10 - POW10_MIN].x : a / c_pow10_dd[-e10 - POW10_MIN].x;
+  }
+  if (e10 > POW10_MAX) return INFINITY;
+  if (e10 < -290) {
+    if (e10 < -400) return 0.0;
+    return decimal_to_double(m, e10 + 60) * 1e-60;
+  }
+  const double mh = (double)m;
+  const double ml = (double)(int64_t)(m - (uint64_t)mh);  // exact remainder (|.| < 2^11)
+  const double2 t = c_pow10_dd[e10 - POW10_MIN];
+  const double ph = mh * t.x;
+  const double pl = fma(mh, t.x, -ph) + (mh * t.y + ml * t.x);
+  return ph + pl;
+}
+
+// Python float() over bytes [b, e) (no surrounding whitespace: atoms are
+// whitespace-split).  Returns PS_OK / PS_BAD_VALUE / PS_NONFINITE / PS_UNSUPPORTED.
+__device__ int parse_float(const uint8_t* s, int64_t b, int64_t e, double* out) {
+  int64_t i = b;
+  bool neg = false;
+  if (i < e && (s[i] == '+' || s[i] == '-')) { neg = s[i] == '-'; ++i; }
+  // inf / infinity / nan (any case): valid float() spellings, non-finite here
+  {
+    const int64_t L = e - i;
+    auto lower = [&](int64_t k) { uint32_t c = s[i + k]; return (c >= 'A' && c <= 'Z') ? c + 32 : c; };
+    if (L == 3 && ((lower(0) == 'i' && lower(1) == 'n' && lower(2) == 'f') ||
+                   (lower(0) == 'n' && lower(1) == 'a' && lower(2) == 'n')))
+      return PS_NONFINITE;
+    if (L == 8) {
+      const char* w = "infinity";
+      bool m = true;
+      for (int k = 0; k < 8; ++k) m &= lower(k) == (uint32_t)w[k];
+      if (m) return PS_NONFINITE;
+    }
+  }
+  uint64_t m = 0;
+  int nd = 0;          // significant digits kept in m (<= 19)
+  int drop = 0;        // integer digits dropped past 19 (scale up)
+  int frac = 0;        // fraction digits kept (scale down)
+  bool any = false, zero_lead = true;
+  // integer part: digits with single '_' between digits
+  int64_t j = i;
+  bool prev_digit = false;
+  for (; j < e; ++j) {
+    const uint32_t c = s[j];
+    if (c >= '0' && c <= '9') {
+      any = true;
+      prev_digit = true;
+      if (zero_lead && c == '0') continue;
+      zero_lead = false;
+      if (nd < 19) { m = m * 10 + (c - '0'); ++nd; } else { ++drop; }
+    } else if (c == '_') {
+      if (!prev_digit || j + 1 >= e || s[j + 1] < '0' || s[j + 1] > '9') return PS_BAD_VALUE;
+      prev_digit = false;
+    } else {
+      break;
+    }
+  }
+  bool any_frac = false;
+  if (j < e && s[j] == '.') {
+    ++j;
+    prev_digit = false;
+    for (; j < e; ++j) {
+      const uint32_t c = s[j];
+      if (c >= '0' && c <= '9') {
+        any_frac = true;
+        prev_digit = true;
+        if (zero_lead && c == '0') { ++frac; continue; }
+        zero_lead = false;
+        if (nd < 19) { m = m * 10 + (c - '0'); ++nd; ++frac; }
+      } else if (c == '_') {
+        if (!prev_digit || j + 1 >= e || s[j + 1] < '0' || s[j + 1] > '9') return PS_BAD_VALUE;
+        prev_digit = false;
+      } else {
+        break;
+      }
+    }
+  }
+  if (!any && !any_frac) {
+    for (int64_t k = i; k < e; ++k) if (s[k] >= 0x80) return PS_UNSUPPORTED;
+    return PS_BAD_VALUE;
+  }
+  int64_t ex = 0;
+  if (j < e && (s[j] == 'e' || s[j] == 'E')) {
+    ++j;
+    bool eneg = false;
+    if (j < e && (s[j] == '+' || s[j] == '-')) { eneg = s[j] == '-'; ++j; }
+    bool ed = false;
+    prev_digit = false;
+    for (; j < e; ++j) {
+      const uint32_t c = s[j];
+      if (c >= '0' && c <= '9') {
+        ed = true;
+        prev_digit = true;
+        if (ex < 100000000) ex = ex * 10 + (c - '0');
+      } else if (c == '_') {
+        if (!prev_digit || j + 1 >= e || s[j + 1] < '0' || s[j + 1] > '9') return PS_BAD_VALUE;
+        prev_digit = false;
+      } else {
+        break;
+      }
+    }
+    if (!ed) return PS_BAD_VALUE;
+    if (eneg) ex = -ex;
+  }
+  if (j != e) {
+    for (int64_t k = i; k < e; ++k) if (s[k] >= 0x80) return PS_UNSUPPORTED;
+    return PS_BAD_VALUE;
+  }
+  double v;
+  if (m == 0) {
+    v = 0.0;
+  } else {
+    int64_t e10 = ex + drop - frac;
+    if (e10 > 400) v = INFINITY;
+    else if (e10 < -420) v = 0.0;
+    else v = decimal_to_double(m, (int)e10);
+  }
+  if (!isfinite(v)) return PS_NONFINITE;
+  *out = neg ? -v : v;
+  return PS_OK;
+}
+
+// the Unicode whitespace code points str.split() also splits on, as UTF-8
+__device__ __forceinline__ bool unicode_ws_at(const uint8_t* s, int64_t p, int64_t e) {
+  const uint32_t c0 = s[p];
+  if (c0 == 0xC2 && p + 1 < e) return s[p + 1] == 0x85 || s[p + 1] == 0xA0;
+  if (c0 == 0xE1 && p + 2 < e) return s[p + 1] == 0x9A && s[p + 2] == 0x80;
+  if (c0 == 0xE2 && p + 2 < e) {
+    const uint32_t c1 = s[p + 1], c2 = s[p + 2];
+    if (c1 == 0x80) return (c2 >= 0x80 && c2 <= 0x8A) || c2 == 0xA8 || c2 == 0xA9 || c2 == 0xAF;
+    if (c1 == 0x81) return c2 == 0x9F;
+    return false;
+  }
+  if (c0 == 0xE3 && p + 2 < e) return s[p + 1] == 0x80 && s[p + 2] == 0x80;
+  return false;
+}
+
+struct ParseParams {
+  const uint8_t* text;
+  const int64_t* line_off;
+  int64_t n;
+  const uint8_t* names;
+  const int32_t* name_off;
+  const uint8_t* numeric;
+  int F;
+  int hash_bits;
+  uint64_t* ent_key;  // (fid << 40) | (index << 11) | token position   (scratch)
+  double* ent_val;    // scratch
+  int32_t* ent_n;     // [n] raw entries, then canonical entries per line
+  uint8_t* labels;
+  int32_t* status;
+};
+
+__device__ __forceinline__ int64_t ent_base(const ParseParams& p, int64_t i) {
+  return (p.line_off[i] - p.line_off[0]) / 2 + i;
+}
+
+__global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  const uint8_t* s = p.text;
+  const int64_t b = p.line_off[i], e = p.line_off[i + 1];
+  const int64_t eb = ent_base(p, i);
+  int st = PS_OK, ne = 0;
+  uint8_t label = 0;
+  // unsupported (non-ASCII whitespace) anywhere in the line; whitespace-only
+  // lines are "blank" (skipped by the stream loops, T:176)
+  bool blank = true;
+  for (int64_t q = b; q < e; ++q) {
+    blank &= is_ws(s[q]);
+    if (s[q] >= 0xC2 && unicode_ws_at(s, q, e)) { st = PS_UNSUPPORTED; break; }
+  }
+  if (st == PS_OK && blank) st = PS_BLANK;
+  // label (Fe:223-229)
+  int64_t bar = b;
+  while (bar < e && s[bar] != '|') ++bar;
+  if (st == PS_OK) {
+    int64_t h0 = b, h1 = bar;
+    while (h0 < h1 && is_ws(s[h0])) ++h0;
+    while (h1 > h0 && is_ws(s[h1 - 1])) --h1;
+    const int64_t L = h1 - h0;
+    if (L == 1 && s[h0] == '1') label = 1;
+    else if ((L == 1 && s[h0] == '0') || (L == 2 && s[h0] == '-' && s[h0 + 1] == '1')) label = 0;
+    else st = PS_LABEL;
+    if (st == PS_OK && bar >= e) st = PS_NO_BLOCKS;
+  }
+  const uint32_t mask = (uint32_t)((1ull << p.hash_bits) - 1);
+  const int64_t max_index = 1ll << p.hash_bits;
+  int64_t q = bar;
+  while (st == PS_OK && q < e) {  // one '|' block per iteration; q at its '|'
+    int64_t se = q + 1;
+    while (se < e && s[se] != '|') ++se;
+    int64_t a = q + 1;
+    while (a < se && is_ws(s[a])) ++a;
+    if (a >= se) { st = PS_EMPTY_BLOCK; break; }
+    int64_t ae = a;
+    while (ae < se && !is_ws(s[ae])) ++ae;
+    // field name lookup (InputSchema.field_id)
+    int fid = -1;
+    const int64_t nl = ae - a;
+    for (int f = 0; f < p.F && fid < 0; ++f) {
+      const int32_t o0 = p.name_off[f], o1 = p.name_off[f + 1];
+      if (o1 - o0 != nl) continue;
+      bool eq = true;
+      for (int64_t k = 0; k < nl && eq; ++k) eq = p.names[o0 + k] == s[a + k];
+      if (eq) fid = f;
+    }
+    if (fid < 0) { st = PS_UNKNOWN_FIELD; break; }
+    uint32_t hname = 0x811C9DC5u;
+    for (int64_t k = a; k < ae; ++k) hname = (hname ^ s[k]) * 0x01000193u;
+    hname = (hname ^ 0x1Fu) * 0x01000193u;
+    const bool numeric = p.numeric[fid] != 0;
+    int64_t t = ae;
+    while (st == PS_OK) {  // atoms after the name
+      while (t < se && is_ws(s[t])) ++t;
+      if (t >= se) break;
+      int64_t te = t;
+      while (te < se && !is_ws(s[te])) ++te;
+      int64_t colon = t;
+      while (colon < te && s[colon] != ':') ++colon;
+      double value = 1.0;
+      if (colon < te) {
+        const int r = parse_float(s, colon + 1, te, &value);
+        if (r != PS_OK) { st = r; break; }
+      }
+      int64_t index;
+      bool raw = s[t] == '@' && colon - t >= 2;
+      for (int64_t k = t + 1; raw && k < colon; ++k) {
+        if (s[k] >= 0x80) { st = PS_UNSUPPORTED; break; }
+        raw = s[k] >= '0' && s[k] <= '9';
+      }
+      if (st != PS_OK) break;
+      if (raw) {  // Fe:209-214
+        int64_t v = 0;
+        bool big = false;
+        for (int64_t k = t + 1; k < colon; ++k) {
+          v = v * 10 + (s[k] - '0');
+          if (v >= max_index) { big = true; break; }
+        }
+        if (big) { st = PS_RAW_RANGE; break; }
+        index = v;
+      } else {  // H:43-50 (+ Fe:215-218 numeric transform)
+        uint32_t h = hname;
+        for (int64_t k = t; k < colon; ++k) h = (h ^ s[k]) * 0x01000193u;
+        index = h & mask;
+        if (numeric && value > 0) value = log1p(value);
+      }
+      p.ent_key[eb + ne] = ((uint64_t)fid << 40) | ((uint64_t)index << 11) | (uint64_t)ne;
+      p.ent_val[eb + ne] = value;
+      ++ne;
+      t = te;
+    }
+    q = se;
+  }
+  if (st == PS_OK && ne > PB_CAP) st = PS_TOO_LONG;
+  p.labels[i] = label;
+  p.status[i] = st;
+  p.ent_n[i] = st == PS_OK ? ne : 0;
+}
+
+// B: per line, sort the raw entries by (field, index, position), sum
+// duplicates in occurrence order, count per field; canonical entries are
+// written back to the line's scratch window
+__global__ void __launch_bounds__(PB_WARPS * 32) parse_canon_kernel(ParseParams p, uint8_t* cnt,
+                                                                    int32_t* max_cnt) {
+  __shared__ uint64_t key[PB_WARPS][PB_CAP];
+  __shared__ double sval[PB_WARPS][PB_CAP];
+  __shared__ int fcnt[PB_WARPS][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* k = key[warp];
+  double* sv = sval[warp];
+  int* fc = fcnt[warp];
+  for (int64_t i = (int64_t)blockIdx.x * PB_WARPS + warp; i < p.n;
+       i += (int64_t)gridDim.x * PB_WARPS) {
+    const int ne = p.ent_n[i];
+    const int64_t eb = ent_base(p, i);
+    for (int f = lane; f < p.F; f += 32) fc[f] = 0;
+    int np2 = 1;
+    while (np2 < ne) np2 <<= 1;
+    for (int t = lane; t < np2; t += 32) {
+      k[t] = t < ne ? p.ent_key[eb + t] : ~0ull;
+      if (t < ne) sv[t] = p.ent_val[eb + t];
+    }
+    __syncwarp();
+    for (int size = 2; size <= np2; size <<= 1) {  // bitonic sort, ascending
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = lane; t < np2; t += 32) {
+          const int u = t ^ stride;
+          if (u > t) {
+            const uint64_t x = k[t], y = k[u];
+            const bool up = (t & size) == 0;
+            if ((x > y) == up) { k[t] = y; k[u] = x; }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    // runs of equal (field, index): the run's first lane sums it in position order
+    int nu = 0;
+    for (int t0 = 0; t0 < ne; t0 += 32) {
+      const int t = t0 + lane;
+      bool start = false;
+      uint64_t kk = 0;
+      if (t < ne) {
+        kk = k[t] >> 11;
+        start = t == 0 || (k[t - 1] >> 11) != kk;
+      }
+      const uint32_t bm = __ballot_sync(0xffffffffu, start);
+      if (start) {
+        double v = 0.0;
+        for (int r = t; r < ne && (k[r] >> 11) == kk; ++r) v += sv[k[r] & 2047];  // Fe:219 order
+        const int u = nu + __popc(bm & ((1u << lane) - 1u));
+        p.ent_val[eb + u] = v;  // raw entries live in shared memory now
+        p.ent_key[eb + u] = kk;
+        atomicAdd(&fc[(int)(kk >> 29)], 1);
+      }
+      nu += __popc(bm);
+    }
+    __syncwarp();
+    int big = 0, mx = 0;
+    for (int f = lane; f < p.F; f += 32) {
+      const int c = fc[f];
+      big |= c > 255;
+      mx = max(mx, c);
+      cnt[i * p.F + f] = (uint8_t)min(c, 255);
+    }
+    big = __any_sync(0xffffffffu, big);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      if (big && p.status[i] == PS_OK) p.status[i] = PS_FIELD_CAP;
+      p.ent_n[i] = big ? 0 : nu;
+      if (!big) atomicMax(max_cnt, mx);
+    }
+    if (big)
+      for (int f = lane; f < p.F; f += 32) cnt[i * p.F + f] = 0;
+    __syncwarp();
+  }
+}
+
+// C: ex_off = exclusive scan of the canonical counts (one CTA; a few µs per 1M lines)
+__global__ void __launch_bounds__(1024) parse_scan_kernel(const int32_t* ent_n, int64_t n,
+                                                          int64_t* ex_off) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b = t * per, e = min(n, b + per);
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += ent_n[i];
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int64_t run = t ? part[t - 1] : 0;
+  for (int64_t i = b; i < e; ++i) { ex_off[i] = run; run += ent_n[i]; }
+  if (t == 1023) ex_off[n] = part[1023];
+}
+
+// D: canonical entries -> ragged batch arrays
+__global__ void __launch_bounds__(256) parse_emit_kernel(ParseParams p, const int64_t* ex_off,
+                                                         int32_t* idx, float* val, double* val64) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < p.n; i += (int64_t)gridDim.x * 8) {
+    const int nu = p.ent_n[i];
+    const int64_t eb = ent_base(p, i), o = ex_off[i];
+    for (int u = lane; u < nu; u += 32) {
+      const uint64_t kk = p.ent_key[eb + u];
+      idx[o + u] = (int32_t)(kk & ((1ull << 29) - 1));
+      const double v = p.ent_val[eb + u];
+      val[o + u] = (float)v;
+      if (val64) val64[o + u] = v;
+    }
+  }
+}
+
+}  // namespace dffm
+
+using namespace dffm;
+
+static ParseParams parse_params(const int64_t* line_off, int64_t n, int64_t text_bytes,
+                                void* scratch) {
+  ParseParams p{};
+  p.line_off = line_off;
+  p.n = n;
+  const int64_t cap = text_bytes / 2 + n + 1;
+  p.ent_key = (uint64_t*)scratch;
+  p.ent_val = (double*)(p.ent_key + cap);
+  p.ent_n = (int32_t*)(p.ent_val + cap);
+  return p;
+}
+
+extern "C" int64_t fw_parse_scratch_bytes(int64_t n_lines, int64_t text_bytes) {
+  const int64_t cap = text_bytes / 2 + n_lines + 1;
+  return cap * 16 + n_lines * 4 + 256;
+}
+
+extern "C" int fw_parse_lines(const uint8_t* text, const int64_t* line_off, int64_t n_lines,
+                              int64_t text_bytes, const uint8_t* names, const int32_t* name_off,
+                              const uint8_t* numeric, int32_t n_fields, int32_t hash_bits,
+                              void* scratch, uint8_t* labels, int32_t* line_status, uint8_t* cnt,
+                              int64_t* ex_off, int32_t* max_cnt, void* stream) {
+  if (n_lines < 0 || n_fields < 1 || n_fields > 255 || hash_bits < 1 || hash_bits > 29) {
+    set_error("bad parse args (n=%lld F=%d bits=%d)", (long long)n_lines, n_fields, hash_bits);
+    return DFFM_CONTRACT;
+  }
+  if (!text || !line_off || !names || !name_off || !numeric || !scratch || !labels ||
+      !line_status || !cnt || !ex_off || !max_cnt) {
+    set_error("null buffer");
+    return DFFM_CONTRACT;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  DFFM_CUDA_TRY(cudaMemsetAsync(max_cnt, 0, 4, s), "memset(max_cnt)");
+  if (!n_lines) {
+    DFFM_CUDA_TRY(cudaMemsetAsync(ex_off, 0, 8, s), "memset(ex_off)");
+    return DFFM_OK;
+  }
+  ParseParams p = parse_params(line_off, n_lines, text_bytes, scratch);
+  p.text = text;
+  p.names = names;
+  p.name_off = name_off;
+  p.numeric = numeric;
+  p.F = n_fields;
+  p.hash_bits = hash_bits;
+  p.labels = labels;
+  p.status = line_status;
+  note_launches(1), parse_lines_kernel<<<(unsigned)((n_lines + 127) / 128), 128, 0, s>>>(p);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_lines)");
+  const int64_t sms = sm_count_current();
+  const unsigned gb = (unsigned)std::min<int64_t>((n_lines + PB_WARPS - 1) / PB_WARPS, sms * 16);
+  note_launches(1), parse_canon_kernel<<<gb, PB_WARPS * 32, 0, s>>>(p, cnt, max_cnt);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_canon)");
+  note_launches(1), parse_scan_kernel<<<1, 1024, 0, s>>>(p.ent_n, n_lines, ex_off);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_scan)");
+  return DFFM_OK;
+}
+
+extern "C" int fw_parse_emit(const int64_t* line_off, int64_t n_lines, int64_t text_bytes,
+                             const void* scratch, const int64_t* ex_off, int32_t* idx, float* val,
+                             double* val64_opt, void* stream) {
+  if (n_lines < 0) { set_error("bad n_lines"); return DFFM_CONTRACT; }
+  if (!n_lines) return DFFM_OK;
+  if (!line_off || !scratch || !ex_off || !idx || !val) { set_error("null buffer"); return DFFM_CONTRACT; }
+  ParseParams p = parse_params(line_off, n_lines, text_bytes, const_cast<void*>(scratch));
+  const int64_t sms = sm_count_current();
+  const unsigned g = (unsigned)std::min<int64_t>((n_lines + 7) / 8, sms * 16);
+  note_launches(1), parse_emit_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(p, ex_off, idx, val,
+                                                                         val64_opt);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_emit)");
+  return DFFM_OK;
+}

@@ -131,3 +131,174 @@ class RaggedBatch:
         idx[live] = np.asarray(self.idx)
         val[live] = np.asarray(self.val)
         return idx, val
+
+
+# --------------------------------------------------------------------------- text input (K10)
+
+MIN_HASH_BITS, MAX_HASH_BITS = 10, 29  # H:24-25
+
+PARSE_ERRORS = {
+    1: "malformed label (want 0, 1, or -1)",        # Fe:229
+    2: "example has no field blocks",               # Fe:231
+    3: "empty field block (missing field name after '|')",  # Fe:191
+    4: "unknown field name",                        # InputSchema.field_id
+    5: "bad value",                                 # Fe:203-205
+    6: "non-finite value",                          # Fe:206-207
+    7: "raw index out of range for hash_bits",      # Fe:211-214
+    8: "non-ASCII whitespace or digits (not supported by the GPU parser)",
+    9: "more than 1024 features in one line (GPU parser limit)",
+    10: "more than 255 features in one field (GPU parser limit)",
+    11: "blank line",  # skipped by the reference's stream loops (T:176, T:227)
+}
+
+
+class InputSchema:
+    """Ordered field list + numeric flags + hash_bits (API of the reference's
+    InputSchema, Fe:42-118: same validation, from_text/to_text format)."""
+
+    def __init__(self, field_names, numeric_fields=frozenset(), hash_bits: int = 18):
+        from .errors import ParseError
+        self.field_names = tuple(field_names)
+        self.numeric_fields = frozenset(numeric_fields)
+        self.hash_bits = int(hash_bits)
+        if not self.field_names:
+            raise ParseError("schema declares no fields")
+        if len(set(self.field_names)) != len(self.field_names):
+            raise ParseError("schema field names must be unique")
+        if not MIN_HASH_BITS <= self.hash_bits <= MAX_HASH_BITS:
+            raise ParseError(f"hash_bits must be in [{MIN_HASH_BITS}, {MAX_HASH_BITS}],"
+                             f" got {self.hash_bits}")
+        unknown = self.numeric_fields - set(self.field_names)
+        if unknown:
+            raise ParseError(f"numeric flag on undeclared fields: {sorted(unknown)}")
+        self._ids = {n: i for i, n in enumerate(self.field_names)}
+
+    @property
+    def n_fields(self) -> int:
+        return len(self.field_names)
+
+    def field_id(self, name: str) -> int:
+        from .errors import ParseError
+        try:
+            return self._ids[name]
+        except KeyError:
+            raise ParseError(f"unknown field name: {name!r}") from None
+
+    @classmethod
+    def from_text(cls, text: str) -> "InputSchema":
+        from .errors import ParseError
+        names, numeric, hash_bits = [], set(), 18
+        for lineno, raw in enumerate(text.splitlines(), 1):
+            line = raw.split("#", 1)[0].strip()
+            if not line:
+                continue
+            parts = line.split()
+            if parts[0] == "field" and len(parts) in (2, 3):
+                if len(parts) == 3 and parts[2] != "numeric":
+                    raise ParseError(f"schema line {lineno}: unknown flag {parts[2]!r}")
+                names.append(parts[1])
+                if len(parts) == 3:
+                    numeric.add(parts[1])
+            elif parts[0] == "hash_bits" and len(parts) == 2:
+                try:
+                    hash_bits = int(parts[1])
+                except ValueError:
+                    raise ParseError(f"schema line {lineno}: hash_bits wants an integer") from None
+            else:
+                raise ParseError(f"schema line {lineno}: cannot parse {raw!r}")
+        return cls(tuple(names), frozenset(numeric), hash_bits)
+
+    def to_text(self) -> str:
+        lines = [f"hash_bits {self.hash_bits}"]
+        for name in self.field_names:
+            lines.append(f"field {name}{' numeric' if name in self.numeric_fields else ''}")
+        return "\n".join(lines) + "\n"
+
+
+class ParsedLines:
+    """K10 output on the device: a RaggedBatch of torch tensors plus labels,
+    per-line status, the largest per-field count, and optional f64 values."""
+
+    def __init__(self, batch, labels, status, val64=None):
+        self.batch, self.labels, self.status, self.val64 = batch, labels, status, val64
+
+    def first_error(self, skip_blank: bool = True):
+        """(line number, message) of the first line that failed, or None;
+        blank lines (status 11) count only with ``skip_blank=False``."""
+        import torch
+        bad = torch.nonzero((self.status != 0) & ((self.status != 11) | (not skip_blank)))
+        if bad.numel() == 0:
+            return None
+        i = int(bad[0, 0])
+        return i, PARSE_ERRORS.get(int(self.status[i]), "parse error")
+
+
+def split_lines(text) -> tuple[np.ndarray, np.ndarray]:
+    """Bytes of newline-separated lines -> (uint8 buffer, line offsets int64
+    [n+1]); line i = buf[off[i]:off[i+1]] keeps its '\n' (trailing whitespace
+    to the grammar, Fe:190/Fe:222).  A final line without '\n' counts; nothing
+    after the last '\n' does."""
+    buf = np.frombuffer(bytes(text), dtype=np.uint8) if not isinstance(text, np.ndarray) \
+        else np.ascontiguousarray(text, np.uint8)
+    nl = np.flatnonzero(buf == 10) + 1
+    ends = nl if (len(buf) == 0 or buf[-1] == 10) else np.append(nl, len(buf))
+    return buf, np.concatenate([[0], ends]).astype(np.int64)
+
+
+def parse_lines(text, schema: InputSchema, device, keep_f64: bool = False,
+                raise_on_error: bool = True, skip_blank: bool = True,
+                stream=None) -> ParsedLines:
+    """K10: parse example lines on the GPU (parse_example, Fe:221-235, for
+    every line at once).  ``text`` is bytes (newline-separated lines).  Lines
+    are the batch's examples in order; whitespace-only lines get status 11 and
+    no features (the stream loops skip them, T:176); with ``raise_on_error``
+    the first failed line raises ``ParseError`` like the reference's loop would."""
+    import torch
+
+    from . import _lib
+    from .errors import ParseError
+    dev = torch.device(device)
+    buf, off = split_lines(text)
+    n = len(off) - 1
+    packed = buf
+    F = schema.n_fields
+    names = b"".join(nm.encode("utf-8") for nm in schema.field_names)
+    noff = np.zeros(F + 1, np.int32)
+    np.cumsum([len(nm.encode("utf-8")) for nm in schema.field_names], out=noff[1:])
+    numeric = np.array([nm in schema.numeric_fields for nm in schema.field_names], np.uint8)
+    t_text = torch.from_numpy(packed.copy()).to(dev)
+    t_off = torch.from_numpy(off).to(dev)
+    t_names = torch.frombuffer(bytearray(names or b"\0"), dtype=torch.uint8).to(dev)
+    t_noff = torch.from_numpy(noff).to(dev)
+    t_num = torch.from_numpy(numeric).to(dev)
+    lib = _lib.lib()
+    nbytes = int(off[-1])
+    scratch = torch.empty(int(lib.fw_parse_scratch_bytes(n, nbytes)), dtype=torch.uint8,
+                          device=dev)
+    labels = torch.empty(n, dtype=torch.uint8, device=dev)
+    status = torch.empty(n, dtype=torch.int32, device=dev)
+    cnt = torch.empty((n, F), dtype=torch.uint8, device=dev)
+    ex_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    mx = torch.empty(1, dtype=torch.int32, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    _lib.check(lib.fw_parse_lines(t_text.data_ptr(), t_off.data_ptr(), n, nbytes,
+                                  t_names.data_ptr(), t_noff.data_ptr(), t_num.data_ptr(), F,
+                                  schema.hash_bits, scratch.data_ptr(), labels.data_ptr(),
+                                  status.data_ptr(), cnt.data_ptr(), ex_off.data_ptr(),
+                                  mx.data_ptr(), s.cuda_stream), "fw_parse_lines")
+    nnz = int(ex_off[n].item())  # synchronises: the emit pass needs the total
+    idx = torch.empty(nnz, dtype=torch.int32, device=dev)
+    val = torch.empty(nnz, dtype=torch.float32, device=dev)
+    val64 = torch.empty(nnz, dtype=torch.float64, device=dev) if keep_f64 else None
+    if nnz:
+        _lib.check(lib.fw_parse_emit(t_off.data_ptr(), n, nbytes, scratch.data_ptr(),
+                                     ex_off.data_ptr(), idx.data_ptr(), val.data_ptr(),
+                                     val64.data_ptr() if keep_f64 else None, s.cuda_stream),
+                   "fw_parse_emit")
+    out = ParsedLines(RaggedBatch(ex_off, cnt, idx, val, max(1, int(mx.item()))), labels,
+                      status, val64)
+    if raise_on_error:
+        err = out.first_error(skip_blank)
+        if err is not None:
+            raise ParseError(f"line {err[0] + 1}: {err[1]}")
+    return out

@@ -18,6 +18,9 @@ outputs of the unmodified reference package ``fieldwise``:
                        truth SPEC S:266 names for the context cache)
 * ``metrics.npz``   -- StreamingEvaluator / window_auc / logloss (Me:21-129)
 * ``serial.npz``    -- flat_weight_view bytes (M:640-660)
+* ``parse.npz``     -- features.parse_example (Fe:175-235) over seeded text
+                       lines with edge cases: which lines raise ParseError,
+                       labels, canonical (field, index, value) per line
 
 Nothing here runs on the GPU box; /root/reference does not exist there.
 """
@@ -247,6 +250,93 @@ def serial_fixture():
     print("serial", len(full), len(infer))
 
 
+def _value_text(rng):
+    r = rng.random()
+    if r < 0.25:
+        return str(int(rng.integers(-5, 100)))
+    if r < 0.45:
+        return f"{rng.random() * 10:.{int(rng.integers(1, 6))}f}"
+    if r < 0.6:
+        return repr(float(rng.standard_normal() * 10 ** int(rng.integers(-8, 9))))
+    if r < 0.7:
+        return f"{rng.integers(1, 999)}e{int(rng.integers(-30, 30))}"
+    if r < 0.75:
+        return "1_000.2_5"
+    if r < 0.8:
+        return f"+.{rng.integers(0, 99999)}"
+    if r < 0.85:
+        return f"{rng.integers(0, 9)}."
+    if r < 0.9:
+        return f"{rng.integers(1, 9)}E+0{rng.integers(0, 9)}"
+    return repr(float(rng.lognormal()))
+
+
+def parse_fixture():
+    from fieldwise.errors import ParseError
+    from fieldwise.features import parse_example
+    rng = np.random.default_rng(11)
+    names = ["user", "ad", "site", "hour", "price", "cnt", "q", "dev", "os", "geo"]
+    schema = InputSchema(tuple(names), frozenset({"price", "cnt"}), 20)
+    ws = [" ", "  ", "\t", " \t ", "\x1f", " \x0b"]
+    words = ["a", "b1", "u_42", "x.y", "tok-9", "Z", "ünï", "€", "@", "@12a", "@7", "@0042",
+             "@1048575", "@99", "-", "a:b"]
+    lines = []
+    for i in range(700):
+        label = ["0", "1", "-1", " 1 ", "1\t", " 0"][int(rng.integers(0, 6))]
+        parts = [label]
+        for _ in range(int(rng.integers(1, 7))):
+            f = names[int(rng.integers(0, len(names)))]
+            toks = []
+            for _ in range(int(rng.integers(0, 8))):
+                w = words[int(rng.integers(0, len(words)))] if rng.random() < 0.4 else \
+                    f"t{int(rng.integers(0, 40))}"
+                if rng.random() < 0.35:
+                    w = w + ":" + _value_text(rng)
+                toks.append(w)
+            sep = ws[int(rng.integers(0, len(ws)))]
+            parts.append("|" + f + (sep if toks else "") + sep.join(toks) +
+                         (sep if rng.random() < 0.2 else ""))
+        lines.append("".join(parts) if rng.random() < 0.5 else " ".join(parts))
+    lines += [  # errors and edges (Fe:191-231)
+        "2 |user a", "|user a", "1", "1 |", "1 | ", "1 |user a |", "1 |zzz a", "1 |user a:abc",
+        "1 |user a:inf", "1 |user a:nan", "1 |user a:-Infinity", "1 |user @1048576",
+        "1 |user @99999999999999999999", "1 |user a:1__0", "1 |user a:_1", "1 |user a:1_",
+        "1 |user a:1e", "1 |user a:e5", "1 |user a:.", "1 |user a:", "1 |user a:0x10",
+        "1 |user a:1e400", "1 |user a:1e-400", "1 |user a:-0.0", "1 |user a:1e1_0",
+        "1 |user a:1._5", "1 |user a:+-1", "0 |price 3:2.5 3:0.5 x:-1 @5:4", "1 |cnt a a a:2",
+        "-1 |user a |user a |ad a", "1 |user a:1:2", "1 |user\ta\x1fb\x1cc", "", "   ",
+        "1 |user " + " ".join(f"t{j}" for j in range(250)),
+        "1 |q " + " ".join(f"w:{j * 0.37:.3f}" for j in range(60)) + " |q w:1",
+        "1 |price 0.0000000000000000000000012345678901234567890123 1e-310:1 big:" + "9" * 30,
+        "1 |user 123456789012345678901234567890:1.7976931348623157e308",
+        "1 |user a:4.9e-324 b:2.2250738585072014e-308 c:0.1 d:0.3 e:12345678901234567e-10",
+    ]
+    ok, labels, off, fid, idx, val = [], [], [0], [], [], []
+    for ln in lines:
+        try:
+            ex = parse_example(ln, schema)
+        except ParseError:
+            ok.append(False)
+            labels.append(0)
+            off.append(off[-1])
+            continue
+        ok.append(True)
+        labels.append(ex.label)
+        for ff in sorted(ex.fields, key=lambda f: f.field_id):
+            fid += [ff.field_id] * len(ff.indices)
+            idx += ff.indices.tolist()
+            val += ff.values.tolist()
+        off.append(len(idx))
+    text = "\n".join(lines) + "\n"
+    np.savez_compressed(os.path.join(HERE, "parse.npz"),
+                        text=np.frombuffer(text.encode("utf-8"), np.uint8),
+                        schema=np.array(schema.to_text()), ok=np.array(ok),
+                        labels=np.array(labels, np.uint8), ex_off=np.array(off, np.int64),
+                        fid=np.array(fid, np.int64), idx=np.array(idx, np.int64),
+                        val=np.array(val, np.float64))
+    print("parse", len(lines), "lines,", sum(ok), "ok,", len(idx), "features")
+
+
 def main():
     hash_fixture()
     fwd_fixture("cfg1", configs.CFG1, 256, 10, 101, 0.1)
@@ -259,6 +349,7 @@ def main():
     ctx_fixture()
     metrics_fixture()
     serial_fixture()
+    parse_fixture()
 
 
 if __name__ == "__main__":
