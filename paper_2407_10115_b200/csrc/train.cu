@@ -352,15 +352,49 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       lrp[f] = lp;
     }
     // S[f][g][c] = sum_m x_m * ffm[j_m][g][c]  (M:339): warp per field,
-    // lanes along the row (coalesced)
-    for (int f = warp; f < F; f += TR_WARPS) {
-      for (int gk = lane; gk < Fk; gk += 32) {
-        double s = 0.0;
-        for (int m = 0; m < M; ++m) {
-          const int j = sidx[f * M + m];
-          if (j >= 0) s += sval[f * M + m] * (double)__ldcg(p.ffm + (int64_t)j * Fk + gk);
+    // lanes along the row (coalesced).  Rows of <= 256 floats and <= 4 slots:
+    // every load of the field is issued before the first sum (one memory
+    // latency per example instead of one per 32-wide column step), sums in
+    // slot order as before.
+    if (Fk <= 256 && M <= 4) {
+      for (int f = warp; f < F; f += TR_WARPS) {
+        int js[4];
+        double xs[4];
+        float v[4][8];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          js[m] = m < M ? sidx[f * M + m] : -1;
+          xs[m] = m < M ? sval[f * M + m] : 0.0;
         }
-        S[f * Fk + gk] = s;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int gk = lane + 32 * i;
+            v[m][i] = (js[m] >= 0 && gk < Fk) ? __ldcg(p.ffm + (int64_t)js[m] * Fk + gk) : 0.f;
+          }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int gk = lane + 32 * i;
+          if (gk < Fk) {
+            double s = 0.0;
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (js[m] >= 0) s += xs[m] * (double)v[m][i];
+            S[f * Fk + gk] = s;
+          }
+        }
+      }
+    } else {
+      for (int f = warp; f < F; f += TR_WARPS) {
+        for (int gk = lane; gk < Fk; gk += 32) {
+          double s = 0.0;
+          for (int m = 0; m < M; ++m) {
+            const int j = sidx[f * M + m];
+            if (j >= 0) s += sval[f * M + m] * (double)__ldcg(p.ffm + (int64_t)j * Fk + gk);
+          }
+          S[f * Fk + gk] = s;
+        }
       }
     }
     // sort-and-segment bookkeeping for the update (M:424-437): lead = first
@@ -841,6 +875,7 @@ extern "C" int dffm_train_sequential(const dffm_model* model, const dffm_train_s
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    note_launches(1);
     DFFM_CUDA_TRY(cudaLaunchKernelEx(&cfg, train_kernel<TR_CLUSTER>, p), "launch(train cluster)");
   }
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(train)");
