@@ -101,8 +101,10 @@ int dffm_forward(const dffm_model* model, const int32_t* idx, const float* val,
  *   0 row-coalesced, 1 warp-specialised (fused MLP on CUDA cores),
  *   2 CTA-synchronous, 3 TMA 1-D ring, 4 TMA gather4 ring,
  *   5 staged rows + tcgen05 3xTF32 MLP (hidden widths multiples of 16, <= 256),
- *   -1 = from DFFM_FORWARD_KERNEL; unset = 1, or 5 when the MLP has >= 64K
- *   multiply-adds per example (cfg5) and fits.
+ *   -1 = from DFFM_FORWARD_KERNEL; unset = 5 (staged rows through the
+ *   K1 v8 row ring + tcgen05 MLP) when the ring takes the shape (M <= 4,
+ *   F*M <= 128, k in {4, 8, 16}) and the hidden widths are multiples of 16,
+ *   or when the MLP has >= 64K multiply-adds per example; otherwise 1.
  * Family 5 keeps a per-(device, stream) device workspace (staged rows of one
  * slice + the blocked hi/lo MLP weights), allocated on first use.
  * Process-wide; for A/B measurements and tests.

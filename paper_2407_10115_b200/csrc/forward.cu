@@ -327,14 +327,21 @@ static bool try_rowstage_forward(const dffm_model* m, FwdParams& p, int smax, cu
   return false;
 }
 
-// K1 v8 staging gather: warp-specialised circular row ring (M <= 4)
-static bool try_rsw_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
-                            int* rc) {
-  if (!p.xout || p.M < 1 || p.M > 4 || p.P < 1 || p.F * p.M > RSW_MAXFM || p.F > 255) return false;
+// shapes the K1 v8 row-ring gather takes
+static bool rsw_shape_ok(const dffm_model* m, const FwdParams& p) {
+  if (p.M < 1 || p.M > 4 || p.P < 1 || p.F * p.M > RSW_MAXFM || p.F > 255) return false;
   const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
   const int k = p.k;
   if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
-  if (((uintptr_t)p.ffm & 15) || ((uintptr_t)p.lr & 3)) return false;
+  return !(((uintptr_t)p.ffm & 15) || ((uintptr_t)p.lr & 3));
+}
+
+// K1 v8 staging gather: warp-specialised circular row ring (M <= 4)
+static bool try_rsw_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
+                            int* rc) {
+  if (!p.xout || !rsw_shape_ok(m, p)) return false;
+  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
+  const int k = p.k;
   static int nx_env = -1;
   if (nx_env < 0) {
     const char* v = getenv("DFFM_RSW_NX");
@@ -441,7 +448,12 @@ int tc_mlp_slice(TcPlan& plan, int64_t rows, int64_t status_base, float* prob, f
 static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
                            int* rc) {
   const int fam = forward_family();
-  if (fam != FAM_TC && !(fam == FAM_WS && !g_family_explicit && tc_auto(p))) return false;
+  // default (family unset): the row-ring gather + tensor-core MLP wherever the
+  // ring takes the shape (cfg2: 135 vs 111 M preds/s for the fused ws kernel),
+  // or whenever the MLP is too heavy for CUDA cores (cfg5)
+  if (fam != FAM_TC &&
+      !(fam == FAM_WS && !g_family_explicit && (tc_auto(p) || rsw_shape_ok(m, p))))
+    return false;
   if (!tc_eligible(p, smax)) return false;
   FwdParams pg = p;
   pg.hmax = 0;  // staging mode: the gather kernels keep no hidden-layer buffers

@@ -6,13 +6,14 @@
 // barrier / mbarrier waits -- three CTA barriers per example -- while DRAM
 // is 31% busy.  Here no CTA barrier is left on the per-example path:
 //
-//   NPROD producer warps  read example i's padded slots (streamed IDXD
-//       examples ahead into shared memory by cp.async), allocate its present rows in a circular ring of R
-//       row slots (allocation and release in example order), write the slot
-//       metadata and issue one 1-D bulk (TMA) copy per present row; the
-//       ring is shared by all in-flight examples, so multi-slot data (cfg2:
-//       ~47 of 72 slots present) packs densely and ~4-6 examples are
-//       resident or in flight per SM.
+//   1 allocator warp  reads example i's padded slots (streamed IDXD examples
+//       ahead into shared memory by cp.async), allocates its present rows in
+//       a circular ring of R row slots (allocation and release in example
+//       order) and publishes the slot metadata on meta[i]; the ring is shared
+//       by all in-flight examples, so multi-slot data (cfg2: ~47 of 72 slots
+//       present) packs densely and ~4-6 examples are resident or in flight.
+//   NISS issue warps    one 1-D bulk (TMA) copy per present row, slot s by
+//       warp s % NISS (full[i] counts their bytes).
 //   NPW pair warps      process 32-pair chunks; chunk c of example i goes to
 //       warp (i*nch + c) % npw (npw = min(NPW, nch)), so the warps drift
 //       across examples and stay balanced however P divides.  Each chunk writes its raw pair values,
@@ -37,17 +38,21 @@ namespace dffm {
 #ifndef DFFM_RSW_NPW
 #define DFFM_RSW_NPW 12
 #endif
-#ifndef DFFM_RSW_NPROD
-#define DFFM_RSW_NPROD 2
+#ifndef DFFM_RSW_NISS
+#define DFFM_RSW_NISS 4
 #endif
 #ifndef DFFM_RSW_IDXD
 #define DFFM_RSW_IDXD 4
+#endif
+#ifndef DFFM_RSW_PAD
+#define DFFM_RSW_PAD 16
 #endif
 #ifndef DFFM_RSW_NMW
 #define DFFM_RSW_NMW 3
 #endif
 constexpr int RSW_NPW = DFFM_RSW_NPW;
-constexpr int RSW_NPROD = DFFM_RSW_NPROD;
+constexpr int RSW_NISS = DFFM_RSW_NISS;  // TMA issue warps (plus one allocator warp)
+constexpr int RSW_NPROD = 1 + RSW_NISS;
 constexpr int RSW_NMW = DFFM_RSW_NMW;
 constexpr int RSW_IDXD = DFFM_RSW_IDXD;  // examples of idx/val in flight per producer (power of 2)
 static_assert((RSW_IDXD & (RSW_IDXD - 1)) == 0, "RSW_IDXD must be a power of two");
@@ -69,7 +74,7 @@ __host__ __device__ inline RswSmem rsw_smem_layout(int F, int M, int P, int row_
   const int FM = F * M;
   s.NX = NX;
   s.nch = (P + 31) / 32;
-  s.row_stride = row_bytes + 16;  // rotates banks row to row
+  s.row_stride = row_bytes + DFFM_RSW_PAD;  // +16 rotates banks row to row
   int q = 0;
   s.off_sidx = q; q = align16(q + FM * 4);
   s.off_sval = q; q = align16(q + FM * 4);
@@ -77,10 +82,10 @@ __host__ __device__ inline RswSmem rsw_smem_layout(int F, int M, int P, int row_
   s.off_xv = q; q = align16(q + (P + 1) * 4);
   s.slot_bytes = q;
   int o = 0;
-  s.off_bar = o; o = align16(o + 3 * RSW_MAXX * 8);
+  s.off_bar = o; o = align16(o + 4 * RSW_MAXX * 8);
   s.off_pair = o; o = align16(o + P * 2);
-  s.off_cnt = o; o = align16(o + RSW_NPROD * RSW_MAXX * 4);
-  s.off_pidx = o; o = align16(o + RSW_NPROD * RSW_IDXD * 2 * FM * 4);
+  s.off_cnt = o; o = align16(o + RSW_MAXX * 4);
+  s.off_pidx = o; o = align16(o + RSW_IDXD * 2 * FM * 4);
   s.off_slot = o; o = align16(o + NX * s.slot_bytes);
   s.off_ring = o;
   s.R = (smem_max - o) / s.row_stride;
@@ -101,8 +106,9 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
   uint64_t* full = (uint64_t*)(smem + L.off_bar);  // [NX] producers -> pair/merge warps
   uint64_t* pdone = full + RSW_MAXX;               // [NX] pair chunks -> producers/merge
   uint64_t* mfree = pdone + RSW_MAXX;              // [NX] merge warp -> producers
+  uint64_t* meta = mfree + RSW_MAXX;               // [NX] allocator -> issue warps
   uint16_t* pairtab = (uint16_t*)(smem + L.off_pair);
-  int* cnt_all = (int*)(smem + L.off_cnt);  // [NPROD][MAXX] rows per slot (producer-private)
+  int* my_cnt = (int*)(smem + L.off_cnt);  // [MAXX] rows per slot (allocator-private)
   unsigned char* slots = smem + L.off_slot;
   unsigned char* ring = smem + L.off_ring;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,7 +120,8 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
   }
   if (threadIdx.x == 0) {
     for (int b = 0; b < NX; ++b) {
-      mbar_init(&full[b], RSW_NPROD);
+      mbar_init(&full[b], RSW_NISS);
+      mbar_init(&meta[b], 1);
       mbar_init(&pdone[b], nch);
       mbar_init(&mfree[b], 1);
     }
@@ -197,15 +204,52 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       xs += RSW_NMW;
       while (xs >= NX) { xs -= NX; par ^= 1u; }
     }
-  } else if (warp >= RSW_NPW) {
-    // ================================================================ producer warps
-    const int pw = warp - RSW_NPW;
-    int* my_cnt = cnt_all + pw * RSW_MAXX;
+  } else if (warp > RSW_NPW) {
+    // ================================================================ TMA issue warps
+    // Slot s of example i is issued by warp s % NISS, lane s / NISS, from the
+    // metadata the allocator published on meta[i]; each warp arrives on
+    // full[i] once with the bytes of its rows.  Issuing is spread over several
+    // warps because a 1-D bulk copy per row is the step that limits how fast
+    // the ring refills (measured: 2 -> 4 issuing warps, cfg5 +5%, cfg2 +20%).
+    const int iw = warp - RSW_NPW - 1;
+    int xs = 0;
+    uint32_t par = 0;
+    for (int64_t i = 0; i < my_n; ++i) {
+      mbar_wait(&meta[xs], par);
+      const unsigned char* sb = slot(xs);
+      const int* sidx = (const int*)(sb + L.off_sidx);
+      const uint16_t* rpos = (const uint16_t*)(sb + L.off_rpos);
+      constexpr int SPW = (RSW_MAXFM + 32 * RSW_NISS - 1) / (32 * RSW_NISS);  // slots per lane
+      int rr[SPW];
+      int mine = 0;
+#pragma unroll
+      for (int t = 0; t < SPW; ++t) {
+        const int s = iw + RSW_NISS * (lane + 32 * t);
+        rr[t] = s < FM ? (int)rpos[s] : 0xFFFF;
+        mine += __popc(__ballot_sync(0xffffffffu, rr[t] != 0xFFFF));
+      }
+      if (lane == 0) {
+        if (mine) mbar_arrive_expect_tx(&full[xs], (uint32_t)(mine * row_bytes));
+        else mbar_arrive(&full[xs]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < SPW; ++t) {
+        const int s = iw + RSW_NISS * (lane + 32 * t);
+        if (rr[t] != 0xFFFF)
+          tma_load_1d(ring + (size_t)rr[t] * RSB,
+                      (const unsigned char*)p.ffm + (int64_t)sidx[s] * row_bytes,
+                      (uint32_t)row_bytes, &full[xs]);
+      }
+      if (++xs == NX) { xs = 0; par ^= 1u; }
+    }
+  } else if (warp == RSW_NPW) {
+    // ================================================================ allocator warp
     constexpr int SPL = RSW_MAXFM / 32;
-    // idx / val of examples i+1 .. i+IDXD-1 stream into a private shared ring
-    // by 4-byte cp.async (one commit group per example), so the producer never
+    // idx / val of examples i+1 .. i+IDXD-1 stream into a shared ring by
+    // 4-byte cp.async (one commit group per example), so the allocator never
     // waits a global-load latency per example
-    int* pidx = (int*)(smem + L.off_pidx) + pw * RSW_IDXD * 2 * FM;  // [IDXD][idx FM | val FM]
+    int* pidx = (int*)(smem + L.off_pidx);  // [IDXD][idx FM | val FM]
     auto issue_ex = [&](int64_t i) {
       if (i < my_n) {
         const int64_t e = blockIdx.x + i * gridDim.x;
@@ -247,7 +291,7 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
         }
       }
       issue_ex(i + RSW_IDXD);
-      if (pw == 0 && __any_sync(0xffffffffu, bad) && lane == 0)
+      if (__any_sync(0xffffffffu, bad) && lane == 0)
         atomicMin((unsigned long long*)p.status,
                   (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
                                                  DFFM_CONTRACT));
@@ -282,41 +326,27 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
         ++tail_ex;
         if (++ts == NX) { ts = 0; tpar ^= 1u; }
       }
-      // slot metadata (this warp writes the slots it issues) + one bulk copy per row
+      // slot metadata -> meta[xs] (release): the issue warps copy the rows
       unsigned char* sb = slot(xs);
       int* sidx = (int*)(sb + L.off_sidx);
       float* sval = (float*)(sb + L.off_sval);
       uint16_t* rpos = (uint16_t*)(sb + L.off_rpos);
-      int before = 0, mine = 0;
-      int rp[SPL];
+      int before = 0;
 #pragma unroll
       for (int c = 0; c < SPL; ++c) {
         const int s = lane + 32 * c;
         int r = head + before + __popc(mask[c] & lt);
         if (r >= R) r -= R;
-        rp[c] = cj[c] >= 0 ? r : -1;
         before += __popc(mask[c]);
-        const bool own = ((lane + c) % RSW_NPROD) == pw;
-        if (own && s < FM) {
+        if (s < FM) {
           sidx[s] = cj[c];
           sval[s] = cx[c];
           rpos[s] = (uint16_t)(cj[c] >= 0 ? r : 0xFFFF);
         }
-        mine += __popc(__ballot_sync(0xffffffffu, own && cj[c] >= 0));
       }
-      if (lane == 0) {
-        my_cnt[xs] = cnt;
-        if (mine) mbar_arrive_expect_tx(&full[xs], (uint32_t)(mine * row_bytes));
-        else mbar_arrive(&full[xs]);
-      }
+      if (lane == 0) my_cnt[xs] = cnt;
       __syncwarp();
-#pragma unroll
-      for (int c = 0; c < SPL; ++c) {
-        if (rp[c] >= 0 && ((lane + c) % RSW_NPROD) == pw)
-          tma_load_1d(ring + (size_t)rp[c] * RSB,
-                      (const unsigned char*)p.ffm + (int64_t)cj[c] * row_bytes,
-                      (uint32_t)row_bytes, &full[xs]);
-      }
+      if (lane == 0) mbar_arrive(&meta[xs]);
       head += cnt;
       if (head >= R) head -= R;
       used += cnt;
