@@ -399,7 +399,11 @@ def run_ours(args, wl):
                    "parallelism": f"batch-sharded x{world}, replicated tables, no collective"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(wl.name),
-                     "algorithmic_bytes_per_step": alg, "peak_source": peak_src},
+                     "algorithmic_bytes_per_step": alg, "peak_source": peak_src,
+                     "scope": "whole step: algorithmic bytes / step time over every kernel "
+                              "of the call (per slice: K1 v8 row-ring gather + tcgen05 MLP "
+                              "when staged, else the fused kernel); traffic = DRAM bytes of "
+                              "one step (profiles/ncu_traffic.json)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": rb.nbytes() if ragged_wins else pad_bytes,
                 "d2h_bytes_per_step": n * 4 + 8, "matches_device_run": e2e_ok,

@@ -1,0 +1,27 @@
+"""One bench-shaped forward step inside an NVTX range "step" (after warm-up), for
+ncu captures that must cover exactly one step:
+    ncu --nvtx --nvtx-include "step/" ... python tools/one_forward.py cfg2 [n]"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_2407_10115_b200 import configs  # noqa: E402
+from paper_2407_10115_b200.model import predict_batch  # noqa: E402
+
+wl = {"cfg1": configs.CFG1, "cfg2": configs.CFG2, "cfg5": configs.CFG5}[sys.argv[1]]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else wl.n_examples
+dev = torch.device("cuda", 0)
+st = bench.build_store(wl, dev)
+idx, val = bench.build_inputs(wl, n, dev, 0)
+prob = torch.empty(n, device=dev)
+for _ in range(3):
+    predict_batch(idx, val, st, out=prob, check=False)
+torch.cuda.synchronize()
+torch.empty(64 << 20, device=dev).zero_()  # L2 flush, as in bench.py
+torch.cuda.nvtx.range_push("step")
+predict_batch(idx, val, st, out=prob, check=False)
+torch.cuda.nvtx.range_pop()
+torch.cuda.synchronize()
+print("one step done", n)
