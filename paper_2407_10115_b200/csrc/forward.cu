@@ -345,7 +345,7 @@ static bool try_rsw_forward(const dffm_model* m, FwdParams& p, int smax, cudaStr
   static int nx_env = -1;
   if (nx_env < 0) {
     const char* v = getenv("DFFM_RSW_NX");
-    nx_env = v ? std::min(RSW_MAXX, std::max(2, atoi(v))) : 6;
+    nx_env = v ? std::min(RSW_MAXX, std::max(2, atoi(v))) : 8;
   }
 
   const int row_bytes = p.F * k * esz;

@@ -36,7 +36,7 @@
 namespace dffm {
 
 #ifndef DFFM_RSW_NPW
-#define DFFM_RSW_NPW 12
+#define DFFM_RSW_NPW 16
 #endif
 #ifndef DFFM_RSW_NISS
 #define DFFM_RSW_NISS 4
@@ -48,7 +48,7 @@ namespace dffm {
 #define DFFM_RSW_PAD 16
 #endif
 #ifndef DFFM_RSW_NMW
-#define DFFM_RSW_NMW 3
+#define DFFM_RSW_NMW 6
 #endif
 constexpr int RSW_NPW = DFFM_RSW_NPW;
 constexpr int RSW_NISS = DFFM_RSW_NISS;  // TMA issue warps (plus one allocator warp)
