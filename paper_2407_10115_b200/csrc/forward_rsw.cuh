@@ -143,8 +143,12 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       unsigned char* sb = slot(xs);
       const int* sidx = (const int*)(sb + L.off_sidx);
       const float* sval = (const float*)(sb + L.off_sval);
-      mbar_wait(&full[xs], par);
-      // LR terms (M:338) in flight while the pairs are formed
+      // metadata published (meta[i]; before the rows are even requested): the
+      // LR loads start a whole row-copy latency before the pairs are formed.
+      // Phase-safe like the pair warps: pdone(i - NMW) complete means every
+      // pair warp -- hence every full/meta phase up to i - NMW -- is done.
+      mbar_wait(&meta[xs], par);
+      // LR terms (M:338) in flight while the rows land and the pairs are formed
       float lw[RSW_MAXFM / 32], lx[RSW_MAXFM / 32];
 #pragma unroll
       for (int c = 0; c < RSW_MAXFM / 32; ++c) {
