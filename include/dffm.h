@@ -224,6 +224,19 @@ int fw_parse_emit(const int64_t* line_off, int64_t n_lines, int64_t text_bytes,
                   const void* scratch, const int64_t* ex_off, int32_t* idx, float* val,
                   double* val64_opt, void* stream);
 
+/*
+ * K9b packed wire format -> padded layout: as dffm_unpack_ragged, but each
+ * index is idx_width (3 or 4) little-endian bytes and values equal to 1.0 are
+ * elided: bit (bit_base + t) of vbits (LSB first) is set iff feature t of this
+ * call carries an explicit f32, stored in vals[voff[e] - val_base + rank].
+ * n_fields * max_per_field <= 128.
+ */
+int dffm_unpack_packed(const int64_t* ex_off, const uint8_t* cnt, const uint8_t* idx_bytes,
+                       int32_t idx_width, const uint8_t* vbits, const float* vals,
+                       const int64_t* voff, int64_t n, int32_t n_fields, int32_t max_per_field,
+                       int64_t nnz_base, int64_t bit_base, int64_t val_base, int32_t* out_idx,
+                       float* out_val, int64_t status_base, uint64_t* status, void* stream);
+
 /* Kernels launched by this library so far (all devices and threads). */
 int64_t dffm_launch_count(void);
 

@@ -74,6 +74,9 @@ SIGNATURES = {
                                      c_int32, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
                                      c_void_p]),
     "dffm_launch_count": (c_int64, []),
+    "dffm_unpack_packed": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
+                                     c_void_p, c_int64, c_int32, c_int32, c_int64, c_int64,
+                                     c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "fw_parse_scratch_bytes": (c_int64, [c_int64, c_int64]),
     "fw_parse_lines": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
                                  c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p,

@@ -133,6 +133,44 @@ class RaggedBatch:
         return idx, val
 
 
+class PackedBatch:
+    """Wire format for host-resident batches (K9b unpacks it on the device): the
+    ragged batch with each bucket index in ``idx_width`` little-endian bytes (3
+    when every index < 2^24 -- exact) and the values equal to 1.0 (categorical
+    indicators, Fe:202) elided: bit t of ``vbits`` (LSB first) says feature t
+    carries an explicit f32 in ``vals``; ``voff`` int64 [n+1] indexes ``vals``
+    per example.  cfg2: ~215 B per example vs 411 B ragged, 576 B padded."""
+
+    def __init__(self, ex_off, cnt, idx_bytes, idx_width, vbits, vals, voff, max_per_field):
+        self.ex_off, self.cnt, self.idx_bytes, self.vbits = ex_off, cnt, idx_bytes, vbits
+        self.vals, self.voff = vals, voff
+        self.idx_width, self.max_per_field = int(idx_width), int(max_per_field)
+
+    @property
+    def n(self) -> int:
+        return int(self.cnt.shape[0])
+
+    def nbytes(self) -> int:
+        return sum(int(a.nbytes if hasattr(a, "nbytes") else a.numel() * a.element_size())
+                   for a in (self.ex_off, self.cnt, self.idx_bytes, self.vbits, self.vals,
+                             self.voff))
+
+    @classmethod
+    def from_ragged(cls, rb: "RaggedBatch") -> "PackedBatch":
+        idx = np.asarray(rb.idx, np.int64)
+        val = np.asarray(rb.val, np.float32)
+        width = 3 if (len(idx) == 0 or idx.max() < (1 << 24)) else 4
+        if len(idx) and idx.min() < 0:
+            raise ContractError("negative bucket index in a ragged batch")
+        ib = idx.astype("<u4").view(np.uint8).reshape(-1, 4)[:, :width]
+        explicit = ~(val.view(np.uint32) == np.float32(1.0).view(np.uint32))  # bit-exact 1.0
+        vbits = np.packbits(explicit, bitorder="little")
+        ex_off = np.asarray(rb.ex_off, np.int64)
+        cs = np.concatenate([[0], np.cumsum(explicit, dtype=np.int64)])
+        return cls(ex_off, np.asarray(rb.cnt, np.uint8), np.ascontiguousarray(ib).ravel(), width,
+                   vbits, np.ascontiguousarray(val[explicit]), cs[ex_off], rb.max_per_field)
+
+
 # --------------------------------------------------------------------------- text input (K10)
 
 MIN_HASH_BITS, MAX_HASH_BITS = 10, 29  # H:24-25

@@ -563,6 +563,78 @@ class HostPredictor:
         return out_host
 
 
+    def predict_packed(self, batch, out_host: torch.Tensor, check: bool = True) -> torch.Tensor:
+        """Host-buffer entry point for ``features.PackedBatch`` (pinned torch
+        tensors): per chunk the packed slices are copied, K9b
+        (``dffm_unpack_packed``) expands them to the padded layout, K1 scores."""
+        n, F = int(batch.cnt.shape[0]), int(batch.cnt.shape[1])
+        M = batch.max_per_field
+        W = batch.idx_width
+        lib = _lib.lib()
+        cm = self.store.c_model_ref()
+        cs, ks = self.copy_stream, self.compute_stream
+        dev = self.store.device
+        bounds = _chunk_bounds(n, self.chunk)
+        off_h, voff_h = batch.ex_off, batch.voff
+        zs = [(int(off_h[c0]), int(off_h[c1]), int(voff_h[c0]), int(voff_h[c1])) for c0, c1 in bounds]
+        need = (max((z1 - z0 for z0, z1, _, _ in zs), default=0),
+                max((v1 - v0 for _, _, v0, v1 in zs), default=0))
+        if getattr(self, "pk_cap", None) != need:
+            self.pk_off = [torch.empty(self.chunk + 1, dtype=torch.int64, device=dev) for _ in range(2)]
+            self.pk_voff = [torch.empty(self.chunk + 1, dtype=torch.int64, device=dev) for _ in range(2)]
+            self.pk_cnt = [torch.empty((self.chunk, F), dtype=torch.uint8, device=dev) for _ in range(2)]
+            self.pk_idx = [torch.empty(need[0] * 4 + 8, dtype=torch.uint8, device=dev) for _ in range(2)]
+            self.pk_bits = [torch.empty(need[0] // 8 + 16, dtype=torch.uint8, device=dev) for _ in range(2)]
+            self.pk_vals = [torch.empty(need[1] + 1, dtype=torch.float32, device=dev) for _ in range(2)]
+            self.pk_cap = need
+        h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        with torch.cuda.stream(ks):
+            self.status.clear()
+        cs.wait_stream(ks)
+        for i, ((c0, c1), (z0, z1, v0, v1)) in enumerate(zip(bounds, zs)):
+            b = i & 1
+            y0, y1 = z0 // 8, (z1 + 7) // 8
+            ob, vob = self.pk_off[b][: c1 - c0 + 1], self.pk_voff[b][: c1 - c0 + 1]
+            cb = self.pk_cnt[b][: c1 - c0]
+            ib = self.pk_idx[b][: (z1 - z0) * W]
+            bb = self.pk_bits[b][: y1 - y0]
+            vb = self.pk_vals[b][: v1 - v0]
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(free[b])
+                ob.copy_(off_h[c0:c1 + 1], non_blocking=True)
+                vob.copy_(voff_h[c0:c1 + 1], non_blocking=True)
+                cb.copy_(batch.cnt[c0:c1], non_blocking=True)
+                ib.copy_(batch.idx_bytes[z0 * W:z1 * W], non_blocking=True)
+                bb.copy_(batch.vbits[y0:y1], non_blocking=True)
+                vb.copy_(batch.vals[v0:v1], non_blocking=True)
+                h2d_done[b].record(cs)
+            pi = self.idx_buf[b][: c1 - c0]
+            pv = self.val_buf[b][: c1 - c0]
+            pb = self.prob_buf[b][: c1 - c0]
+            with torch.cuda.stream(ks):
+                ks.wait_event(h2d_done[b])
+                _lib.check(lib.dffm_unpack_packed(ob.data_ptr(), cb.data_ptr(), ib.data_ptr(), W,
+                                                  bb.data_ptr(), vb.data_ptr(), vob.data_ptr(),
+                                                  c1 - c0, F, M, z0, z0 - 8 * y0, v0,
+                                                  pi.data_ptr(), pv.data_ptr(), c0,
+                                                  self.status.ptr(), ks.cuda_stream),
+                           "dffm_unpack_packed")
+                rc = lib.dffm_forward(cm, pi.data_ptr(), pv.data_ptr(), M, c1 - c0,
+                                      pb.data_ptr(), None, c0, self.status.ptr(), ks.cuda_stream)
+                _lib.check(rc, "dffm_forward")
+                self.launches += 1
+                out_host[c0:c1].copy_(pb, non_blocking=True)
+                free[b].record(ks)
+        with torch.cuda.stream(ks):
+            self.status.fetch_async()
+        ks.synchronize()
+        if check:
+            self.status.raise_if_set("forward: ")
+        return out_host
+
+
 def forward(example, store: WeightStore, mac_counter=None) -> ForwardState:
     """One example through the fused kernel (API of M:321)."""
     from .features import pack_examples

@@ -9,7 +9,7 @@ import torch
 from oracle import fieldwise_oracle as fo
 from paper_2407_10115_b200 import _lib, configs, synth
 from paper_2407_10115_b200.errors import ContractError
-from paper_2407_10115_b200.features import RaggedBatch
+from paper_2407_10115_b200.features import PackedBatch, RaggedBatch
 from paper_2407_10115_b200.model import HostPredictor, ModelConfig, StatusWord, WeightStore, \
     predict_batch
 
@@ -91,3 +91,28 @@ def test_host_predictor_ragged_equals_padded(wl_name):
     out2 = torch.empty(n, dtype=torch.float32).pin_memory()
     hp(idx.pin_memory(), val.pin_memory(), out2)
     assert torch.equal(out2, ref)
+
+
+@pytest.mark.parametrize("wl_name", ["CFG2", "CFG5"])
+def test_host_predictor_packed_equals_padded(wl_name):
+    """The packed wire format (3-byte indices, 1.0 values elided; K9b) returns
+    the bits of the padded device run, several chunks with a ragged tail."""
+    wl = getattr(configs, wl_name)
+    bits = 20
+    ost = fo.random_store(wl.n_fields, wl.k, wl.hidden, bits, seed=8, scale=0.05)
+    cfg = ModelConfig(n_fields=wl.n_fields, k=wl.k, hidden_sizes=wl.hidden, hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, "bf16" if wl_name == "CFG5" else "f32",
+                               False)
+    n = 3 * 4096 + 77
+    idx, val = synth.make_examples(wl, n, seed=10, hash_bits=bits)
+    ref = predict_batch(idx, val, st).cpu()
+    pk = PackedBatch.from_ragged(RaggedBatch.from_padded(idx.numpy(), val.numpy()))
+    assert pk.idx_width == 3
+    pkh = PackedBatch(*(torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                        for a in (pk.ex_off, pk.cnt, pk.idx_bytes)), 3,
+                      *(torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                        for a in (pk.vbits, pk.vals, pk.voff)), pk.max_per_field)
+    hp = HostPredictor(st, n, idx.shape[2], chunk=4096)
+    out = torch.empty(n, dtype=torch.float32).pin_memory()
+    hp.predict_packed(pkh, out)
+    assert torch.equal(out, ref)

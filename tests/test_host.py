@@ -113,6 +113,33 @@ def test_ragged_batch_round_trip():
     assert np.array_equal(i2, idx) and np.array_equal(v2, val)
 
 
+def test_packed_batch_round_trip():
+    """PackedBatch (3-byte indices, 1.0 values elided) decodes back to the
+    ragged batch bit for bit (host decoder restating K9b)."""
+    rng = np.random.default_rng(4)
+    n, F, M = 257, 6, 3
+    cnt = rng.integers(0, M + 1, size=(n, F))
+    idx = np.full((n, F, M), -1, np.int32)
+    val = np.zeros((n, F, M), np.float32)
+    live = np.arange(M)[None, None, :] < cnt[:, :, None]
+    idx[live] = rng.integers(0, 1 << 24, size=int(live.sum()))
+    v = np.where(rng.random(int(live.sum())) < 0.3, rng.lognormal(size=int(live.sum())), 1.0)
+    v[:5] = [-0.0, 1.0, np.float32(1.0000001), 0.0, 1.0]
+    val[live] = v.astype(np.float32)
+    rb = features.RaggedBatch.from_padded(idx, val)
+    pb = features.PackedBatch.from_ragged(rb)
+    assert pb.idx_width == 3 and pb.nbytes() < rb.nbytes()
+    nnz = int(rb.ex_off[-1])
+    b = pb.idx_bytes.reshape(nnz, 3).astype(np.int64)
+    dec_idx = b[:, 0] | (b[:, 1] << 8) | (b[:, 2] << 16)
+    bits = np.unpackbits(pb.vbits, bitorder="little")[:nnz].astype(bool)
+    dec_val = np.ones(nnz, np.float32)
+    dec_val[bits] = pb.vals
+    assert np.array_equal(dec_idx, rb.idx) and np.array_equal(dec_val.view(np.uint32),
+                                                              rb.val.view(np.uint32))
+    assert np.array_equal(np.cumsum(np.r_[0, bits])[rb.ex_off], pb.voff)
+
+
 def test_metrics_match_reference():
     g = load("metrics")
     ev = metrics.StreamingEvaluator(30000)
