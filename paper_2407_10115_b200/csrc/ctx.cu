@@ -216,6 +216,30 @@ ctx_kernel(CtxParams q) {
   }
 }
 
+}  // namespace dffm
+
+#include "ctx_ring.cuh"
+
+namespace dffm {
+
+using CtxRingKernel = void (*)(CtxParams, CrSmem);
+
+template <typename T>
+static CtxRingKernel select_ctx_ring(int K, int MD) {
+#define DFFM_SEL(KK)                                        \
+  if (K == KK) {                                            \
+    if (MD == 1) return ctx_ring_kernel<KK, T, 1>;          \
+    if (MD == 2) return ctx_ring_kernel<KK, T, 2>;          \
+    if (MD == 3) return ctx_ring_kernel<KK, T, 3>;          \
+    if (MD == 4) return ctx_ring_kernel<KK, T, 4>;          \
+  }
+  if constexpr (sizeof(T) == 4) { DFFM_SEL(4) }
+  DFFM_SEL(8)
+  DFFM_SEL(16)
+#undef DFFM_SEL
+  return nullptr;
+}
+
 using CtxKernel = void (*)(CtxParams);
 
 template <typename T>
@@ -332,6 +356,72 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
     default: kern = select_ctx<uint16_t>(K, MU); break;
   }
   if (!kern) { set_error("no context kernel for k=%d", p.k); return DFFM_SIZING; }
+  // K3 v2 (default when it takes the shape): candidates through the K1 v8 row
+  // ring with the context cache in shared memory, MLP on the tensor cores
+  {
+    static int ring_env = -1;
+    if (ring_env < 0) {
+      const char* v = getenv("DFFM_CTX_RING");
+      ring_env = v ? atoi(v) : 1;
+    }
+    const int esz = model->wdtype == DFFM_W_F32 ? 4 : 2;
+    const int k = p.k;
+    const int NX = CR_MAXX;
+    const int64_t per_cta = ((n_requests + 147) / 148 + 1) * (int64_t)n_cand;
+    bool ok = ring_env && ctx_mlp == nullptr && tc_eligible(p, smax) && n_ctx_fields >= 1 &&
+              per_cta < (1ll << 30) &&
+              q.Fd >= 1 && cand_m <= 4 && q.Fd * cand_m <= CR_MAXFM && n_cand >= NX &&
+              (k == 4 || k == 8 || k == 16) && (k * esz) % 16 == 0 && ctx_idx && ctx_val &&
+              !((uintptr_t)p.ffm & 15) && !((uintptr_t)p.lr & 3);
+    CrSmem CL{};
+    if (ok) {
+      CL = cr_smem_layout(p.F, q.Fc, q.Mc, q.Fd, cand_m, k, esz, NX, smax);
+      ok = CL.R >= 2 * q.Fd * cand_m;
+    }
+    CtxRingKernel rk = nullptr;
+    if (ok) {
+      switch (model->wdtype) {
+        case DFFM_W_F32: rk = select_ctx_ring<float>(k, cand_m); break;
+        case DFFM_W_BF16: rk = select_ctx_ring<__nv_bfloat16>(k, cand_m); break;
+        default: rk = select_ctx_ring<uint16_t>(k, cand_m); break;
+      }
+    }
+    if (rk) {
+      const cudaStream_t s = (cudaStream_t)stream;
+      p.hmax = 0;
+      const int64_t rows_all = n_requests * (int64_t)n_cand;
+      const int64_t cap = std::max<int64_t>(n_cand, std::min<int64_t>(rows_all, 1 << 22));
+      const int64_t req_per = std::max<int64_t>(1, cap / n_cand);
+      const int64_t rows_max = std::min<int64_t>(req_per, n_requests) * n_cand;
+      TcPlan plan;
+      if ((rc = tc_plan(p, smax, (rows_max + TC_M - 1) / TC_M * TC_M, s, &plan))) return rc;
+      int occ = 0;
+      if ((rc = kernel_occupancy((const void*)rk, CR_THREADS, CL.total, &occ))) return rc;
+      const int DM = q.Fd * q.Md;
+      for (int64_t r0 = 0; r0 < n_requests; r0 += req_per) {
+        const int64_t nr = std::min<int64_t>(req_per, n_requests - r0);
+        CtxParams a = q;
+        a.cidx = ctx_idx + r0 * q.Fc * q.Mc;
+        a.cval = ctx_val + r0 * q.Fc * q.Mc;
+        a.didx = cand_idx + r0 * n_cand * DM;
+        a.dval = cand_val + r0 * n_cand * DM;
+        a.R = nr;
+        a.f.n = nr * n_cand;
+        a.f.status_base = r0 * n_cand;
+        a.f.prob = prob + r0 * n_cand;
+        a.f.xout = plan.X;
+        a.f.rout = plan.resid;
+        a.f.fout = plan.flags;
+        a.f.Kp = plan.Kp;
+        const int64_t grid = std::min<int64_t>(nr, (int64_t)sm_count_current());
+        note_launches(1), rk<<<(unsigned)grid, CR_THREADS, CL.total, s>>>(a, CL);
+        DFFM_CUDA_TRY(cudaGetLastError(), "launch(ctx_ring)");
+        if ((rc = tc_mlp_slice(plan, nr * n_cand, r0 * n_cand, prob + r0 * n_cand, nullptr, s)))
+          return rc;
+      }
+      return DFFM_OK;
+    }
+  }
   if (!use_tc) return launch_ctx(kern, q, L.total, (cudaStream_t)stream);
   // requests in slices: K3 stages each candidate's MergeNorm row, mlp_tc scores them
   const cudaStream_t s = (cudaStream_t)stream;

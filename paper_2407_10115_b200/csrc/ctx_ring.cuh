@@ -1,0 +1,478 @@
+// K3 v2: context-cached candidate scorer on the K1 v8 row ring (staging mode:
+// the candidates' MergeNorm rows go to the tcgen05 MLP, mlp_tc.cu).
+//
+// SPEC S:239-296 (no reference code; truth = model.forward on the merged
+// example).  Context fields are 0..Fc-1, candidate fields Fc..F-1
+// (disjoint).  The examples of the ring are the candidates of this
+// CTA's requests, in order (request r = blockIdx.x + t*gridDim.x):
+//   allocator warp   streams candidate slots (cp.async, IDXD ahead), allocates
+//                    their present rows in the ring, publishes meta[i]
+//   issue warps      one 1-D bulk copy per candidate row (full[i])
+//   pair warps       per request, first build the context cache together
+//                    (double-buffered by request parity, behind a
+//                    named barrier): Sctx[x][g][:] = sum_m x_m w_m[g] (f32 fma
+//                    over the context slots, as K3 v1), the ctx x ctx pair
+//                    values and the context lr partial; then per candidate
+//                    the pairs that involve a candidate field:
+//                    <S[c][x], Sctx[x][c]> and <S[c1][c2], S[c2][c1]>, in
+//                    32-pair chunks (chunk c of candidate i on warp
+//                    (i*nch + c) % npw, npw = min(NPW, nch): phase-safe waits)
+//   merge warps      lr_out = bias + ctx lr partial + candidate lr terms;
+//                    MergeNorm over [lr_out, all P pairs] (ctx x ctx from the
+//                    cache: never cached past MergeNorm) in f64 ->
+//                    staged row, residual, stage bits.
+// The cache of request t is built (buffer t & 1) only after every pair warp
+// is done with request t-1, and a pair warp starts candidate i only after the
+// merge of candidate i-NX (the allocator waits mfree before publishing i), so
+// with C >= NX no merge warp still reads a buffer that is being rebuilt.
+#pragma once
+
+#include "forward_kernel.cuh"
+#include "forward_rsw.cuh"
+
+namespace dffm {
+
+constexpr int CR_NPW = 8, CR_NISS = 2, CR_NMW = 12;
+constexpr int CR_THREADS = (CR_NPW + 1 + CR_NISS + CR_NMW) * 32;
+constexpr int CR_MAXX = 64;   // candidate slots in flight
+constexpr int CR_MAXFM = 32;  // candidate slots per candidate (Fd * Md)
+constexpr int CR_CHUNK = 32;  // pairs per chunk (lane per pair)
+constexpr int CR_IDXD = 8;    // candidates of slot data streamed ahead
+
+struct CrSmem {
+  int off_bar, off_ptab, off_cnt, off_pidx, off_cache, off_slot, off_ring, total;
+  int cache_bytes, c_S, c_cpx, c_lr, c_pres, c_sidx, c_sval;  // within a cache buffer
+  int slot_bytes, s_sidx, s_sval, s_rpos, s_xv;                // within a slot
+  int row_stride, R, NX, nch, Pc;
+};
+
+__host__ __device__ inline CrSmem cr_smem_layout(int F, int Fc, int Mc, int Fd, int Md, int k,
+                                                 int esz, int NX, int smem_max) {
+  CrSmem s;
+  const int P = F * (F - 1) / 2;
+  s.Pc = Fc * Fd + Fd * (Fd - 1) / 2;
+  s.nch = (s.Pc + CR_CHUNK - 1) / CR_CHUNK;
+  s.NX = NX;
+  const int FM = Fd * Md;
+  s.row_stride = F * k * esz + 16;
+  int q = 0;
+  s.c_S = q; q = align16(q + Fc * F * k * 4);
+  s.c_cpx = q; q = align16(q + P * 4);
+  s.c_lr = q; q = align16(q + 32);  // lr partial, sum and sum of squares of ctx pairs, bad flag
+  s.c_pres = q; q = align16(q + Fc);
+  s.c_sidx = q; q = align16(q + Fc * Mc * 4);
+  s.c_sval = q; q = align16(q + Fc * Mc * 4);
+  s.cache_bytes = q;
+  q = 0;
+  s.s_sidx = q; q = align16(q + FM * 4);
+  s.s_sval = q; q = align16(q + FM * 4);
+  s.s_rpos = q; q = align16(q + FM * 2);
+  s.s_xv = q; q = align16(q + s.Pc * 4);
+  s.slot_bytes = q;
+  int o = 0;
+  s.off_bar = o; o = align16(o + 4 * CR_MAXX * 8);
+  s.off_ptab = o; o = align16(o + s.Pc * 4);
+  s.off_cnt = o; o = align16(o + CR_MAXX * 4);
+  s.off_pidx = o; o = align16(o + CR_IDXD * 2 * FM * 4);
+  s.off_cache = o; o = align16(o + 2 * s.cache_bytes);
+  s.off_slot = o; o = align16(o + NX * s.slot_bytes);
+  s.off_ring = o;
+  s.R = (smem_max - o) / s.row_stride;
+  if (s.R > 65535) s.R = 65535;
+  s.total = o + (s.R > 0 ? s.R : 0) * s.row_stride;
+  return s;
+}
+
+template <int K, typename T, int MD>
+__global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, CrSmem L) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const FwdParams& p = q.f;
+  const int F = p.F, P = p.P, D = p.D, Fc = q.Fc, Mc = q.Mc, Fd = q.Fd;
+  constexpr int M = MD;
+  const int FM = Fd * M;
+  const int C = q.C;
+  constexpr int SEGB = K * (int)sizeof(T);
+  const int row_bytes = F * SEGB;
+  const int RSB = L.row_stride, R = L.R, NX = L.NX, nch = L.nch, Pc = L.Pc;
+  uint64_t* full = (uint64_t*)(smem + L.off_bar);
+  uint64_t* pdone = full + CR_MAXX;
+  uint64_t* mfree = pdone + CR_MAXX;
+  uint64_t* meta = mfree + CR_MAXX;
+  uint32_t* ptab = (uint32_t*)(smem + L.off_ptab);  // candidate pairs: f1 | f2 << 8 | pos << 16
+  int* my_cnt = (int*)(smem + L.off_cnt);
+  unsigned char* slots = smem + L.off_slot;
+  unsigned char* ring = smem + L.off_ring;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const T* lrt = (const T*)p.lr;
+  const T* ffm = (const T*)p.ffm;
+
+  // candidate-pair table in global pair order (position = index into pairs)
+  if (threadIdx.x == 0) {
+    int n = 0, pos = 0;
+    for (int f1 = 0; f1 < F; ++f1)
+      for (int f2 = f1 + 1; f2 < F; ++f2, ++pos)
+        if (f2 >= Fc) ptab[n++] = (uint32_t)f1 | ((uint32_t)f2 << 8) | ((uint32_t)pos << 16);
+    for (int b = 0; b < NX; ++b) {
+      mbar_init(&full[b], CR_NISS);
+      mbar_init(&meta[b], 1);
+      mbar_init(&pdone[b], nch);
+      mbar_init(&mfree[b], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int64_t my_req = q.R > blockIdx.x ? (q.R - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_n = my_req * C;
+  auto slot = [&](int xs) { return slots + (size_t)xs * L.slot_bytes; };
+  auto cache = [&](int64_t t) { return smem + L.off_cache + (size_t)(t & 1) * L.cache_bytes; };
+  auto cand_e = [&](int64_t i) {  // global candidate number of local candidate i
+    const int t = (int)((uint32_t)i / (uint32_t)C);  // i < 2^31 (host check): 32-bit divide
+    return ((int64_t)blockIdx.x + (int64_t)t * gridDim.x) * C + (i - (int64_t)t * C);
+  };
+
+  if (warp >= CR_NPW + 1 + CR_NISS) {
+    // ================================================================ merge warps
+    const int mw = warp - CR_NPW - 1 - CR_NISS;
+    const float bias = load_elem<T>(lrt + p.n_buckets, p.dlr);
+    int xs = mw % NX;
+    uint32_t par = (uint32_t)((mw / NX) & 1);
+    for (int64_t i = mw; i < my_n; i += CR_NMW) {
+      const int64_t e = cand_e(i);
+      unsigned char* sb = slot(xs);
+      const int* sidx = (const int*)(sb + L.s_sidx);
+      const float* sval = (const float*)(sb + L.s_sval);
+      mbar_wait(&meta[xs], par);
+      float lw = 0.f, lx = 0.f;
+      if (lane < FM) {
+        const int j = sidx[lane];
+        lx = j >= 0 ? sval[lane] : 0.f;
+        lw = j >= 0 ? load_elem<T>(lrt + j, p.dlr) : 0.f;
+      }
+      mbar_wait(&pdone[xs], par);
+      const unsigned char* cb = cache((uint32_t)i / (uint32_t)C);
+      const float* cpx = (const float*)(cb + L.c_cpx);
+      const float* xv = (const float*)(sb + L.s_xv);
+      // candidate pairs land in xv in ptab order; the ctx x ctx pairs' sum and
+      // sum of squares come from the cache (f64, computed once per request)
+      const double* cst = (const double*)(cb + L.c_lr);  // lr partial, sum v, sum v^2, bad
+      double ps = 0.0;
+      int pbad = 0;
+      for (int t = lane; t < Pc; t += 32) {
+        const float v = xv[t];
+        ps += (double)v;
+        pbad |= !isfinite(v);
+      }
+      const double psum = warp_sum(ps) + cst[1];
+      pbad = __any_sync(0xffffffffu, pbad) | (cst[3] != 0.0);
+      const double lr_out = (double)bias + cst[0] + warp_sum((double)lx * (double)lw);  // M:327
+      const double mu = (psum + lr_out) / D;
+      // population variance (M:359): candidate deviations two-pass, the ctx x ctx
+      // block through its cached moments: sum (v-mu)^2 = S2 - 2 mu S1 + n mu^2
+      double s2 = 0.0;
+      for (int t = lane; t < Pc; t += 32) {
+        const double d = (double)xv[t] - mu;
+        s2 += d * d;
+      }
+      const int nctx = P - Pc;
+      s2 = warp_sum(s2) + (cst[2] - 2.0 * mu * cst[1] + (double)nctx * mu * mu) +
+           (lr_out - mu) * (lr_out - mu);
+      const double rden = 1.0 / (sqrt(s2 / D) + 1e-6);
+      const float m0 = (float)((lr_out - mu) * rden);
+      int mbad = !isfinite(m0);
+      float* row = p.xout + e * p.Kp;
+      // ctx positions and padding first, then the candidate positions overwrite theirs
+      for (int c = lane; c < p.Kp; c += 32) {
+        float m = 0.f;
+        if (c == 0) m = m0;
+        else if (c < D) m = (float)(((double)cpx[c - 1] - mu) * rden);
+        mbad |= !isfinite(m);
+        row[c] = m;
+      }
+      __syncwarp();
+      for (int t = lane; t < Pc; t += 32) {
+        const int pos = (int)(ptab[t] >> 16);
+        const float m = (float)(((double)xv[t] - mu) * rden);
+        mbad |= !isfinite(m);
+        row[1 + pos] = m;
+      }
+      mbad = __any_sync(0xffffffffu, mbad);
+      if (lane == 0) {
+        p.rout[e] = lr_out + psum;
+        p.fout[e] = (!isfinite(lr_out) ? 1 : 0) | (pbad ? 2 : 0) | (mbad ? 4 : 0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mfree[xs]);
+      xs += CR_NMW;
+      while (xs >= NX) { xs -= NX; par ^= 1u; }
+    }
+  } else if (warp > CR_NPW) {
+    // ================================================================ TMA issue warps
+    const int iw = warp - CR_NPW - 1;
+    int xs = 0;
+    uint32_t par = 0;
+    for (int64_t i = 0; i < my_n; ++i) {
+      mbar_wait(&meta[xs], par);
+      const unsigned char* sb = slot(xs);
+      const int* sidx = (const int*)(sb + L.s_sidx);
+      const uint16_t* rpos = (const uint16_t*)(sb + L.s_rpos);
+      const int s = iw + CR_NISS * lane;
+      const int r = s < FM ? (int)rpos[s] : 0xFFFF;
+      const int mine = __popc(__ballot_sync(0xffffffffu, r != 0xFFFF));
+      if (lane == 0) {
+        if (mine) mbar_arrive_expect_tx(&full[xs], (uint32_t)(mine * row_bytes));
+        else mbar_arrive(&full[xs]);
+      }
+      __syncwarp();
+      if (r != 0xFFFF)
+        tma_load_1d(ring + (size_t)r * RSB, (const unsigned char*)p.ffm + (int64_t)sidx[s] * row_bytes,
+                    (uint32_t)row_bytes, &full[xs]);
+      if (++xs == NX) { xs = 0; par ^= 1u; }
+    }
+  } else if (warp == CR_NPW) {
+    // ================================================================ allocator warp
+    int* pidx = (int*)(smem + L.off_pidx);  // [IDXD][idx FM | val FM]
+    auto issue_ex = [&](int64_t i) {
+      if (i < my_n && lane < FM) {
+        const int64_t e = cand_e(i);
+        int* d = pidx + (int)(i & (CR_IDXD - 1)) * 2 * FM;
+        cp_async4(d + lane, q.didx + e * FM + lane);
+        cp_async4(d + FM + lane, q.dval + e * FM + lane);
+      }
+      cp_async_commit();
+    };
+#pragma unroll 1
+    for (int d = 0; d < CR_IDXD; ++d) issue_ex(d);
+    int head = 0, tail = 0, used = 0;
+    int64_t tail_ex = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    int xs = 0, ts = 0;
+    uint32_t fpar = 1, tpar = 0;
+    for (int64_t i = 0; i < my_n; ++i) {
+      const int64_t e = cand_e(i);
+      cp_async_wait<CR_IDXD - 1>();
+      const int* d = pidx + (int)(i & (CR_IDXD - 1)) * 2 * FM;
+      int j = lane < FM ? d[lane] : -1;
+      const float x = lane < FM ? __int_as_float(d[FM + lane]) : 0.f;
+      int bad = 0;
+      if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
+      issue_ex(i + CR_IDXD);
+      if (__any_sync(0xffffffffu, bad) && lane == 0)
+        atomicMin((unsigned long long*)p.status,
+                  (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
+                                                 DFFM_CONTRACT));
+      const uint32_t mask = __ballot_sync(0xffffffffu, j >= 0);
+      const int cnt = __popc(mask);
+      if (i >= NX) {
+        mbar_wait(&mfree[xs], fpar);
+        if (tail_ex == i - NX) {
+          const int tc = my_cnt[xs];
+          tail += tc;
+          if (tail >= R) tail -= R;
+          used -= tc;
+          ++tail_ex;
+          if (++ts == NX) { ts = 0; tpar ^= 1u; }
+        }
+      }
+      while (used + cnt > R) {
+        mbar_wait(&pdone[ts], tpar);
+        const int tc = my_cnt[ts];
+        tail += tc;
+        if (tail >= R) tail -= R;
+        used -= tc;
+        ++tail_ex;
+        if (++ts == NX) { ts = 0; tpar ^= 1u; }
+      }
+      unsigned char* sb = slot(xs);
+      if (lane < FM) {
+        int r = head + __popc(mask & lt);
+        if (r >= R) r -= R;
+        ((int*)(sb + L.s_sidx))[lane] = j;
+        ((float*)(sb + L.s_sval))[lane] = x;
+        ((uint16_t*)(sb + L.s_rpos))[lane] = (uint16_t)(j >= 0 ? r : 0xFFFF);
+      }
+      if (lane == 0) my_cnt[xs] = cnt;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&meta[xs]);
+      head += cnt;
+      if (head >= R) head -= R;
+      used += cnt;
+      if (++xs == NX) { xs = 0; fpar ^= 1u; }
+    }
+    cp_async_wait<0>();
+  } else {
+    // ================================================================ pair warps
+    const int npw = CR_NPW < nch ? CR_NPW : nch;
+    if (warp >= npw) return;
+    int64_t i = 0;
+    int c = warp, xs = 0;
+    uint32_t par = 0;
+    int64_t cur = -1, cur_req = -1;
+    const unsigned char* sb = nullptr;
+    const unsigned char* cb = nullptr;
+    const int tid = warp * 32 + lane, nthr = npw * 32;
+    for (; i < my_n;) {
+      if (i != cur) {
+        const int64_t t = (uint32_t)i / (uint32_t)C;
+        if (t != cur_req) {
+          // ---- build_context_cache for request t, buffer t & 1
+          cur_req = t;
+          const int64_t r = (int64_t)blockIdx.x + t * gridDim.x;
+          unsigned char* wb = cache(t);
+          float* S = (float*)(wb + L.c_S);
+          float* cpx = (float*)(wb + L.c_cpx);
+          unsigned char* cpres = wb + L.c_pres;
+          int* csidx = (int*)(wb + L.c_sidx);
+          float* csval = (float*)(wb + L.c_sval);
+          named_bar_sync(1, nthr);  // every pair warp is past request t-1
+          for (int s = tid; s < Fc * Mc; s += nthr) {
+            int j = __ldg(q.cidx + r * Fc * Mc + s);
+            if (j >= p.n_buckets || j < -1) {
+              atomicMin((unsigned long long*)p.status,
+                        (unsigned long long)status_key(p.status_base + r * C, DFFM_BLOCK_NONE,
+                                                       DFFM_CONTRACT));
+              j = -1;
+            }
+            csidx[s] = j;
+            csval[s] = __ldg(q.cval + r * Fc * Mc + s);
+          }
+          named_bar_sync(1, nthr);
+          if (warp == 0) {
+            double lrs = 0.0;
+            for (int s = lane; s < Fc * Mc; s += 32)
+              if (csidx[s] >= 0) lrs += (double)csval[s] * (double)load_elem<T>(lrt + csidx[s], p.dlr);
+            lrs = warp_sum(lrs);
+            if (lane == 0) *(double*)(wb + L.c_lr) = lrs;
+          }
+          for (int x = tid; x < Fc; x += nthr) {
+            unsigned char pr = 0;
+            for (int m = 0; m < Mc; ++m) pr |= (csidx[x * Mc + m] >= 0);
+            cpres[x] = pr;
+          }
+          const int Fk = F * p.k;
+          for (int t2 = tid; t2 < Fc * Fk; t2 += nthr) {
+            const int x = t2 / Fk, gk = t2 - x * Fk;
+            float acc = 0.f;
+            for (int m = 0; m < Mc; ++m) {
+              const int j = csidx[x * Mc + m];
+              if (j >= 0) acc = fmaf(csval[x * Mc + m], load_elem<T>(ffm + (int64_t)j * Fk + gk, p.dffm), acc);
+            }
+            S[t2] = acc;
+          }
+          named_bar_sync(1, nthr);
+          for (int pp = tid; pp < P; pp += nthr) cpx[pp] = 0.f;
+          named_bar_sync(1, nthr);
+          for (int x1 = 0; x1 < Fc; ++x1)
+            for (int x2 = x1 + 1 + tid; x2 < Fc; x2 += nthr) {
+              float pv = 0.f;
+              if (cpres[x1] & cpres[x2]) {
+                const float* a = S + (x1 * F + x2) * p.k;
+                const float* b = S + (x2 * F + x1) * p.k;
+                for (int kk = 0; kk < p.k; ++kk) pv = fmaf(a[kk], b[kk], pv);
+              }
+              cpx[x1 * F - x1 * (x1 + 1) / 2 + x2 - x1 - 1] = pv;
+            }
+          named_bar_sync(1, nthr);
+          if (warp == 0) {  // moments of the ctx x ctx block (fixed order: deterministic)
+            double s1 = 0.0, sq = 0.0;
+            int bad = 0;
+            for (int pp = lane; pp < P; pp += 32) {
+              const double v = cpx[pp];
+              s1 += v;
+              sq += v * v;
+              bad |= !isfinite(cpx[pp]);
+            }
+            s1 = warp_sum(s1);
+            sq = warp_sum(sq);
+            bad = __any_sync(0xffffffffu, bad);
+            if (lane == 0) {
+              double* cm = (double*)(wb + L.c_lr);
+              cm[1] = s1;
+              cm[2] = sq;
+              cm[3] = bad ? 1.0 : 0.0;
+            }
+          }
+          named_bar_sync(1, nthr);
+          cb = wb;
+        }
+        mbar_wait(&full[xs], par);
+        cur = i;
+        sb = slot(xs);
+      }
+      const float* S = (const float*)(cb + L.c_S);
+      const unsigned char* cpres = cb + L.c_pres;
+      const int* sidx = (const int*)(sb + L.s_sidx);
+      const float* sval = (const float*)(sb + L.s_sval);
+      const uint16_t* rpos = (const uint16_t*)(sb + L.s_rpos);
+      float* xv = (float*)(sb + L.s_xv);
+      const int t = c * CR_CHUNK + lane;
+      if (t < Pc) {
+        const uint32_t pr = ptab[t];
+        const int f1 = pr & 0xFF, f2 = (pr >> 8) & 0xFF;
+        constexpr int PER = 16 / (int)sizeof(T);
+        float a[K], bb[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) { a[u] = 0.f; bb[u] = 0.f; }
+        bool p1 = false, p2 = false;
+        const int c2 = f2 - Fc;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {  // candidate field f2: its slots' segment f1
+          const int r2 = rpos[c2 * M + m];
+          if (r2 != 0xFFFF) {
+            p2 = true;
+            const float x2 = sval[c2 * M + m];
+            const unsigned char* q2 = ring + (size_t)r2 * RSB + f1 * SEGB;
+#pragma unroll
+            for (int u = 0; u < SEGB / 16; ++u) {
+              float w[PER];
+              unpack16<T>(*(const uint4*)(q2 + u * 16), w, p.dffm);
+#pragma unroll
+              for (int v = 0; v < PER; ++v) bb[u * PER + v] = fmaf(x2, w[v], bb[u * PER + v]);
+            }
+          }
+        }
+        if (f1 < Fc) {  // context field: the cached S[x][c]
+          p1 = cpres[f1] != 0;
+          const float* sc = S + (f1 * F + f2) * K;
+#pragma unroll
+          for (int u = 0; u < K; ++u) a[u] = sc[u];
+        } else {
+          const int c1 = f1 - Fc;
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            const int r1 = rpos[c1 * M + m];
+            if (r1 != 0xFFFF) {
+              p1 = true;
+              const float x1 = sval[c1 * M + m];
+              const unsigned char* q1 = ring + (size_t)r1 * RSB + f2 * SEGB;
+#pragma unroll
+              for (int u = 0; u < SEGB / 16; ++u) {
+                float w[PER];
+                unpack16<T>(*(const uint4*)(q1 + u * 16), w, p.dffm);
+#pragma unroll
+                for (int v = 0; v < PER; ++v) a[u * PER + v] = fmaf(x1, w[v], a[u * PER + v]);
+              }
+            }
+          }
+        }
+        float pv = 0.f;
+        if (p1 && p2) {  // inactive pairs stay exactly 0 (M:346-351)
+#pragma unroll
+          for (int u = 0; u < K; ++u) pv = fmaf(a[u], bb[u], pv);
+        }
+        xv[t] = pv;
+      }
+      (void)sidx;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pdone[xs]);
+      c += npw;
+      while (c >= nch) {
+        c -= nch;
+        ++i;
+        if (++xs == NX) { xs = 0; par ^= 1u; }
+      }
+    }
+  }
+}
+
+}  // namespace dffm

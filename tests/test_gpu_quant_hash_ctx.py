@@ -111,9 +111,16 @@ def test_hash_synthetic_ranks_large_batch():
 # ------------------------------------------------------------------ K3
 
 
-@pytest.mark.parametrize("ctx_mlp", ["simt", "tc"])
+def _ctx_mode(ctx_mlp, monkeypatch):
+    if ctx_mlp == "ring":  # default: K3 v2 (row ring + tcgen05 MLP) where it applies
+        monkeypatch.delenv("DFFM_CTX_MLP", raising=False)
+    else:
+        monkeypatch.setenv("DFFM_CTX_MLP", ctx_mlp)
+
+
+@pytest.mark.parametrize("ctx_mlp", ["simt", "tc", "ring"])
 def test_context_cache_matches_reference_merged_forward(ctx_mlp, monkeypatch):
-    monkeypatch.setenv("DFFM_CTX_MLP", ctx_mlp)
+    _ctx_mode(ctx_mlp, monkeypatch)
     g = load("ctx")
     F, k, hidden, bits, flat = fixture_flat(g)
     cfg = ModelConfig(n_fields=F, k=k, hidden_sizes=hidden, hash_bits=bits)
@@ -129,10 +136,11 @@ def test_context_cache_matches_reference_merged_forward(ctx_mlp, monkeypatch):
         inference.predict_batch(cache, g["cand_idx"][3], g["cand_val"][3], st)
 
 
-@pytest.mark.parametrize("ctx_mlp", ["simt", "tc"])
+@pytest.mark.parametrize("ctx_mlp", ["simt", "tc", "ring"])
 def test_context_cache_equals_uncached_forward_u16(ctx_mlp, monkeypatch):
-    """K3 (SIMT or staged tensor-core MLP) == K1 on the merged examples == oracle."""
-    monkeypatch.setenv("DFFM_CTX_MLP", ctx_mlp)
+    """K3 (SIMT, staged tensor-core MLP, or the row-ring K3 v2) == K1 on the
+    merged examples == oracle."""
+    _ctx_mode(ctx_mlp, monkeypatch)
     wl = configs.CFG4
     bits = 14
     ost = fo.random_store(24, 8, (64, 32), bits, seed=44)
@@ -150,4 +158,52 @@ def test_context_cache_equals_uncached_forward_u16(ctx_mlp, monkeypatch):
     assert np.abs(p - p_unc).max() <= 1e-6
     cst, ridx, _ = compact_oracle(sq, merged_i.numpy())
     _, ref = fo.forward_batch(ridx, merged_v.numpy(), cst)
+    assert np.abs(p.reshape(-1) - ref).max() <= 1e-6
+
+
+@pytest.mark.parametrize("wdtype,Mc,Md,C", [("f32", 2, 2, 40), ("bf16", 1, 3, 33), ("u16", 3, 1, 64)])
+def test_context_ring_edge_cases_match_oracle(wdtype, Mc, Md, C, monkeypatch):
+    """K3 v2 with multi-slot context and candidate fields, absent context and
+    candidate fields, empty candidates; every table dtype; vs the oracle."""
+    monkeypatch.delenv("DFFM_CTX_MLP", raising=False)
+    bits = 12
+    Fc, Fd = 10, 6
+    F = Fc + Fd
+    ost = fo.random_store(F, 8, (32, 16), bits, seed=Mc * 10 + Md)
+    cfg = ModelConfig(n_fields=F, k=8, hidden_sizes=(32, 16), hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, with_optimizer=False)
+    if wdtype == "bf16":
+        st = WeightStore.from_flat(cfg, ost.flat(False), DEV, "bf16", False)
+    elif wdtype == "u16":
+        st, _ = quant.quantize_store(st)
+    rng = np.random.default_rng(Mc + 7 * Md)
+    R = 21
+
+    def slots(shape, M):
+        idx = rng.integers(-1, 1 << bits, size=shape + (M,)).astype(np.int32)
+        idx = np.sort(np.where(idx < 0, np.iinfo(np.int32).max, idx), axis=-1)
+        idx = np.where(idx == np.iinfo(np.int32).max, -1, idx)
+        flat = idx.reshape(-1, M)
+        for r in range(len(flat)):
+            live = np.unique(flat[r][flat[r] >= 0])
+            flat[r] = -1
+            flat[r][:len(live)] = live
+        return flat.reshape(idx.shape)
+
+    ci = slots((R, Fc), Mc)
+    ci[2] = -1  # a request without context features
+    di = slots((R, C, Fd), Md)
+    di[:, ::7] = -1  # empty candidates
+    cv = np.where(ci >= 0, rng.lognormal(size=ci.shape), 0).astype(np.float32)
+    dv = np.where(di >= 0, rng.lognormal(size=di.shape), 0).astype(np.float32)
+    p = inference.score_requests(ci, cv, di, dv, st).cpu().numpy()
+    M = max(Mc, Md)
+    mi = np.full((R, C, F, M), -1, np.int32)
+    mv = np.zeros((R, C, F, M), np.float32)
+    mi[:, :, :Fc, :Mc] = ci[:, None]
+    mv[:, :, :Fc, :Mc] = cv[:, None]
+    mi[:, :, Fc:, :Md] = di
+    mv[:, :, Fc:, :Md] = dv
+    cst, ridx, _ = compact_oracle(st, mi.reshape(R * C, F, M))
+    _, ref = fo.forward_batch(ridx, mv.reshape(R * C, F, M), cst)
     assert np.abs(p.reshape(-1) - ref).max() <= 1e-6
