@@ -15,8 +15,8 @@
 //                    values and the context lr partial; then per candidate
 //                    the pairs that involve a candidate field:
 //                    <S[c][x], Sctx[x][c]> and <S[c1][c2], S[c2][c1]>, in
-//                    32-pair chunks (chunk c of candidate i on warp
-//                    (i*nch + c) % npw, npw = min(NPW, nch): phase-safe waits)
+//                    32-pair chunks; G groups of min(NPW, nch) warps take
+//                    alternate candidates (phase-safe waits: G divides NX)
 //   merge warps      lr_out = bias + ctx lr partial + candidate lr terms;
 //                    MergeNorm over [lr_out, all P pairs] (ctx x ctx from the
 //                    cache: never cached past MergeNorm) in f64 ->
@@ -32,7 +32,17 @@
 
 namespace dffm {
 
-constexpr int CR_NPW = 8, CR_NISS = 2, CR_NMW = 12;
+#ifndef DFFM_CR_GT
+#define DFFM_CR_GT 2
+#endif
+#ifndef DFFM_CR_NPW
+#define DFFM_CR_NPW 10
+#endif
+#ifndef DFFM_CR_NMW
+#define DFFM_CR_NMW 6
+#endif
+constexpr int CR_NPW = DFFM_CR_NPW, CR_NISS = 2, CR_NMW = DFFM_CR_NMW;
+constexpr int CR_GT = DFFM_CR_GT;  // candidate groups of pair warps (power of 2)
 constexpr int CR_THREADS = (CR_NPW + 1 + CR_NISS + CR_NMW) * 32;
 constexpr int CR_MAXX = 64;   // candidate slots in flight
 constexpr int CR_MAXFM = 32;  // candidate slots per candidate (Fd * Md)
@@ -302,15 +312,22 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
     cp_async_wait<0>();
   } else {
     // ================================================================ pair warps
-    const int npw = CR_NPW < nch ? CR_NPW : nch;
-    if (warp >= npw) return;
-    int64_t i = 0;
-    int c = warp, xs = 0;
+    // G groups of npg warps; group g takes candidates g, g+G, ... (chunk c of
+    // a candidate on warp c % npg of the group).  Phase-safe: G divides NX, so
+    // a group revisits a slot only through its own candidates, and every warp
+    // of a group has a chunk in each of the group's candidates.
+    int G = 1;
+    while (2 * G <= CR_GT && NX % (2 * G) == 0 && 2 * G <= C) G *= 2;
+    const int npg = CR_NPW / G < nch ? CR_NPW / G : nch;
+    const int gw = warp / npg, wi = warp - gw * npg;
+    if (gw >= G) return;
+    int64_t i = gw;
+    int c = wi, xs = gw;
     uint32_t par = 0;
     int64_t cur = -1, cur_req = -1;
     const unsigned char* sb = nullptr;
     const unsigned char* cb = nullptr;
-    const int tid = warp * 32 + lane, nthr = npw * 32;
+    const int tid = warp * 32 + lane, nthr = G * npg * 32;
     for (; i < my_n;) {
       if (i != cur) {
         const int64_t t = (uint32_t)i / (uint32_t)C;
@@ -465,11 +482,12 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
       (void)sidx;
       __syncwarp();
       if (lane == 0) mbar_arrive(&pdone[xs]);
-      c += npw;
-      while (c >= nch) {
-        c -= nch;
-        ++i;
-        if (++xs == NX) { xs = 0; par ^= 1u; }
+      c += npg;
+      if (c >= nch) {
+        c = wi;
+        i += G;
+        xs += G;
+        if (xs >= NX) { xs -= NX; par ^= 1u; }
       }
     }
   }
