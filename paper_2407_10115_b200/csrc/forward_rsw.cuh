@@ -14,11 +14,13 @@
 //       present) packs densely and ~4-6 examples are resident or in flight.
 //   NISS issue warps    one 1-D bulk (TMA) copy per present row, slot s by
 //       warp s % NISS (full[i] counts their bytes).
-//   NPW pair warps      process 32-pair chunks; chunk c of example i goes to
-//       warp (i*nch + c) % npw (npw = min(NPW, nch)), so the warps drift
-//       across examples and stay balanced however P divides.  Each chunk writes its raw pair values,
-//       an f64 partial sum and a non-finite bit, then arrives on pdone[i].
-//       The last chunk of an example frees its ring rows.
+//   NPW pair warps      process 32-pair chunks: npg = min(NPW, nch) warps,
+//       warp w takes chunks w, w+npg, ... of every example (a group of G
+//       warp sets could take alternate examples -- RSW_GT -- but one group
+//       measured best).  Each chunk writes its raw pair values
+//       and arrives on pdone[i]; the last chunk of an example frees its ring
+//       rows.  With one slot per field a pair is x1*x2*<w1, w2>: bf16 rows
+//       are dotted with the mixed-precision FMA (FHFMA.BF16, no unpacking).
 //   NMW merge warps     (example i on warp i % NMW) load the LR weights
 //       while the pairs are formed, then: sum(pairs) and the non-finite
 //       check, lr_out (M:327, M:338), f64 mean /
@@ -47,6 +49,9 @@ namespace dffm {
 #ifndef DFFM_RSW_PAD
 #define DFFM_RSW_PAD 16
 #endif
+#ifndef DFFM_RSW_GT
+#define DFFM_RSW_GT 1
+#endif
 #ifndef DFFM_RSW_NMW
 #define DFFM_RSW_NMW 6
 #endif
@@ -54,6 +59,7 @@ constexpr int RSW_NPW = DFFM_RSW_NPW;
 constexpr int RSW_NISS = DFFM_RSW_NISS;  // TMA issue warps (plus one allocator warp)
 constexpr int RSW_NPROD = 1 + RSW_NISS;
 constexpr int RSW_NMW = DFFM_RSW_NMW;
+constexpr int RSW_GT = DFFM_RSW_GT;  // example groups of pair warps (power of 2)
 constexpr int RSW_IDXD = DFFM_RSW_IDXD;  // examples of idx/val in flight per producer (power of 2)
 static_assert((RSW_IDXD & (RSW_IDXD - 1)) == 0, "RSW_IDXD must be a power of two");
 constexpr int RSW_THREADS = (RSW_NPW + RSW_NPROD + RSW_NMW) * 32;
@@ -359,18 +365,20 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
     cp_async_wait<0>();
   } else {
     // ================================================================ pair warps
-    // Only min(NPW, nch) pair warps take chunks, so every active warp has a
-    // chunk in every example and walks the examples in order: when it waits
-    // on full[] for example i it has seen example i-NX's phase complete, and
-    // the slot cannot be reissued before its own chunk of i is done -- the
-    // mbarrier parity waits never alias across phases (same argument for the
-    // merge warps: pdone(i-NMW) complete => every pair warp is past i-NMW).
-    const int npw = RSW_NPW < nch ? RSW_NPW : nch;
-    // chunk counter g = warp + t*npw walked incrementally: example i, chunk c,
-    // slot xs, phase parity (no 64-bit divisions on the per-chunk path)
-    int64_t i = warp < npw ? 0 : my_n;
-    int c = warp;
-    int xs = 0;
+    // G groups of npg = min(NPW / G, nch) pair warps; group g takes examples
+    // g, g+G, ... and chunk c of an example goes to warp c % npg of the group,
+    // so every active warp has a chunk in each of its group's examples.
+    // Phase-safe waits: G divides NX, so a group revisits a slot only through
+    // its own examples (it saw example i-NX complete before waiting on i), and
+    // slot i is not reissued before the group's chunks of i are done.  (The
+    // merge warps wait on meta[i], published only after the merge of i-NX.)
+    int G = 1;
+    while (2 * G <= RSW_GT && NX % (2 * G) == 0) G *= 2;
+    const int npg = RSW_NPW / G < nch ? RSW_NPW / G : nch;
+    const int gw = warp / npg, wi = warp - gw * npg;
+    int64_t i = gw < G ? gw : my_n;
+    int c = wi;
+    int xs = gw < G ? gw : 0;
     uint32_t par = 0;
     int64_t cur = -1;
     const unsigned char* sb = nullptr;
@@ -455,11 +463,12 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&pdone[xs]);
-      c += npw;
-      while (c >= nch) {
-        c -= nch;
-        ++i;
-        if (++xs == NX) { xs = 0; par ^= 1u; }
+      c += npg;
+      if (c >= nch) {
+        c = wi;
+        i += G;
+        xs += G;
+        if (xs >= NX) { xs -= NX; par ^= 1u; }
       }
     }
   }
