@@ -540,7 +540,11 @@ def run_ours_ctx(args, wl):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(wl.name),
                      "algorithmic_bytes_per_step": alg, "peak_source": peak_src,
-                     "mlp_tflops": mlp_flops * R * C / (ms_step / 1e3) / 1e12},
+                     "mlp_tflops": mlp_flops * R * C / (ms_step / 1e3) / 1e12,
+                     "scope": "whole step (K3 v2 row-ring candidate kernel + tcgen05 MLP); "
+                              "algorithmic bytes are only 3.2 KB per candidate (the context "
+                              "rows are read once per request), so the step is bound by the "
+                              "per-candidate pair / MergeNorm work, not by HBM"},
         "e2e": {"value": e2e, "unit": "candidates/s",
                 "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in host),
                 "d2h_bytes_per_step": R * C * 4},
