@@ -418,7 +418,6 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
       }
       const float* S = (const float*)(cb + L.c_S);
       const unsigned char* cpres = cb + L.c_pres;
-      const int* sidx = (const int*)(sb + L.s_sidx);
       const float* sval = (const float*)(sb + L.s_sval);
       const uint16_t* rpos = (const uint16_t*)(sb + L.s_rpos);
       float* xv = (float*)(sb + L.s_xv);
@@ -479,7 +478,6 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
         }
         xv[t] = pv;
       }
-      (void)sidx;
       __syncwarp();
       if (lane == 0) mbar_arrive(&pdone[xs]);
       c += npg;

@@ -317,18 +317,24 @@ __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
 // B: per line, sort the raw entries by (field, index, position), sum
 // duplicates in occurrence order, count per field; canonical entries are
 // written back to the line's scratch window
-__global__ void __launch_bounds__(PB_WARPS * 32) parse_canon_kernel(ParseParams p, uint8_t* cnt,
-                                                                    int32_t* max_cnt) {
-  __shared__ uint64_t key[PB_WARPS][PB_CAP];
-  __shared__ double sval[PB_WARPS][PB_CAP];
-  __shared__ int fcnt[PB_WARPS][256];
+// Two tiers: <CAP_S, 8 warps> takes every line with <= CAP_S raw entries (the
+// common case, many warps per SM), <PB_CAP, 2 warps> then takes the rest (a
+// line is processed by the tier whose range holds its raw count LO < ne <= CAP;
+// processed lines hold their canonical count <= their raw count afterwards).
+template <int CAP, int WARPS, int LO>
+__global__ void __launch_bounds__(WARPS * 32) parse_canon_kernel(ParseParams p, uint8_t* cnt,
+                                                                 int32_t* max_cnt) {
+  __shared__ uint64_t key[WARPS][CAP];
+  __shared__ double sval[WARPS][CAP];
+  __shared__ int fcnt[WARPS][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* k = key[warp];
   double* sv = sval[warp];
   int* fc = fcnt[warp];
-  for (int64_t i = (int64_t)blockIdx.x * PB_WARPS + warp; i < p.n;
-       i += (int64_t)gridDim.x * PB_WARPS) {
+  for (int64_t i = (int64_t)blockIdx.x * WARPS + warp; i < p.n;
+       i += (int64_t)gridDim.x * WARPS) {
     const int ne = p.ent_n[i];
+    if (ne > CAP || (LO > 0 && ne <= LO)) continue;  // the other tier's line
     const int64_t eb = ent_base(p, i);
     for (int f = lane; f < p.F; f += 32) fc[f] = 0;
     int np2 = 1;
@@ -394,15 +400,33 @@ __global__ void __launch_bounds__(PB_WARPS * 32) parse_canon_kernel(ParseParams 
   }
 }
 
-// C: ex_off = exclusive scan of the canonical counts (one CTA; a few µs per 1M lines)
-__global__ void __launch_bounds__(1024) parse_scan_kernel(const int32_t* ent_n, int64_t n,
-                                                          int64_t* ex_off) {
+// C: ex_off = exclusive scan of the canonical counts: per-tile sums, a scan of
+// the tile sums in one CTA, then each tile's local scan plus its offset
+constexpr int SC_TILE = 4096;
+__global__ void __launch_bounds__(256) parse_tile_sum_kernel(const int32_t* ent_n, int64_t n,
+                                                             int64_t* tsum) {
+  __shared__ int64_t red[8];
+  const int64_t b = (int64_t)blockIdx.x * SC_TILE;
+  int64_t s = 0;
+  for (int64_t i = b + threadIdx.x; i < min(n, b + SC_TILE); i += 256) s += ent_n[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    tsum[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) parse_tile_scan_kernel(int64_t* tsum, int64_t ntiles,
+                                                               int64_t* total) {
   __shared__ int64_t part[1024];
   const int t = threadIdx.x;
-  const int64_t per = (n + 1023) / 1024;
-  const int64_t b = t * per, e = min(n, b + per);
+  const int64_t per = (ntiles + 1023) / 1024;
+  const int64_t b = t * per, e = min(ntiles, b + per);
   int64_t s = 0;
-  for (int64_t i = b; i < e; ++i) s += ent_n[i];
+  for (int64_t i = b; i < e; ++i) s += tsum[i];
   part[t] = s;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
@@ -412,8 +436,37 @@ __global__ void __launch_bounds__(1024) parse_scan_kernel(const int32_t* ent_n, 
     __syncthreads();
   }
   int64_t run = t ? part[t - 1] : 0;
-  for (int64_t i = b; i < e; ++i) { ex_off[i] = run; run += ent_n[i]; }
-  if (t == 1023) ex_off[n] = part[1023];
+  for (int64_t i = b; i < e; ++i) { const int64_t v = tsum[i]; tsum[i] = run; run += v; }
+  if (t == 1023) *total = part[1023];
+}
+
+__global__ void __launch_bounds__(256) parse_tile_apply_kernel(const int32_t* ent_n, int64_t n,
+                                                               const int64_t* tsum,
+                                                               int64_t* ex_off) {
+  __shared__ int64_t wsum[8];
+  const int64_t b = (int64_t)blockIdx.x * SC_TILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t run = tsum[blockIdx.x];
+  for (int64_t c0 = b; c0 < min(n, b + SC_TILE); c0 += 256) {
+    const int64_t i = c0 + threadIdx.x;
+    const int64_t v = i < n ? ent_n[i] : 0;
+    int64_t x = v;  // inclusive scan within the warp, then across the 8 warps
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int64_t before = 0, all = 0;
+    for (int w = 0; w < 8; ++w) {
+      if (w < warp) before += wsum[w];
+      all += wsum[w];
+    }
+    if (i < n) ex_off[i] = run + before + x - v;
+    run += all;
+    __syncthreads();
+  }
 }
 
 // D: canonical entries -> ragged batch arrays
@@ -451,7 +504,7 @@ static ParseParams parse_params(const int64_t* line_off, int64_t n, int64_t text
 
 extern "C" int64_t fw_parse_scratch_bytes(int64_t n_lines, int64_t text_bytes) {
   const int64_t cap = text_bytes / 2 + n_lines + 1;
-  return cap * 16 + n_lines * 4 + 256;
+  return cap * 16 + n_lines * 4 + 256 + ((n_lines + SC_TILE - 1) / SC_TILE) * 8 + 16;
 }
 
 extern "C" int fw_parse_lines(const uint8_t* text, const int64_t* line_off, int64_t n_lines,
@@ -486,10 +539,21 @@ extern "C" int fw_parse_lines(const uint8_t* text, const int64_t* line_off, int6
   note_launches(1), parse_lines_kernel<<<(unsigned)((n_lines + 127) / 128), 128, 0, s>>>(p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_lines)");
   const int64_t sms = sm_count_current();
-  const unsigned gb = (unsigned)std::min<int64_t>((n_lines + PB_WARPS - 1) / PB_WARPS, sms * 16);
-  note_launches(1), parse_canon_kernel<<<gb, PB_WARPS * 32, 0, s>>>(p, cnt, max_cnt);
+  constexpr int CAP_S = 128;
+  const unsigned g1 = (unsigned)std::min<int64_t>((n_lines + 7) / 8, sms * 8);
+  note_launches(1), parse_canon_kernel<CAP_S, 8, 0><<<g1, 256, 0, s>>>(p, cnt, max_cnt);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_canon)");
-  note_launches(1), parse_scan_kernel<<<1, 1024, 0, s>>>(p.ent_n, n_lines, ex_off);
+  const unsigned gb = (unsigned)std::min<int64_t>((n_lines + PB_WARPS - 1) / PB_WARPS, sms * 16);
+  note_launches(1), parse_canon_kernel<PB_CAP, PB_WARPS, CAP_S><<<gb, PB_WARPS * 32, 0, s>>>(
+      p, cnt, max_cnt);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_canon long lines)");
+  // ex_off via tile sums: the tile-sum array lives past the ent_n array in scratch
+  const int64_t ntiles = (n_lines + SC_TILE - 1) / SC_TILE;
+  int64_t* tsum = (int64_t*)(((uintptr_t)(p.ent_n + n_lines) + 15) & ~(uintptr_t)15);
+  note_launches(1), parse_tile_sum_kernel<<<(unsigned)ntiles, 256, 0, s>>>(p.ent_n, n_lines, tsum);
+  note_launches(1), parse_tile_scan_kernel<<<1, 1024, 0, s>>>(tsum, ntiles, ex_off + n_lines);
+  note_launches(1), parse_tile_apply_kernel<<<(unsigned)ntiles, 256, 0, s>>>(p.ent_n, n_lines, tsum,
+                                                                          ex_off);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(parse_scan)");
   return DFFM_OK;
 }
