@@ -12,6 +12,11 @@ for W in cfg5 cfg4 cfg1; do
   timeout 600 python bench.py --workload $W --steps 10 --warmup 3 --train-examples 0 > $OUT/bench_$W.json 2> $OUT/bench_$W.err
 done
 timeout 600 python bench.py --workload parse --steps 5 --warmup 3 > $OUT/bench_parse.json 2> $OUT/bench_parse.err
+# launch list of the bench command itself (every kernel of the run; per-launch times are
+# cold-cache and serialised: compare shares, not absolutes)
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --train-examples 0"
+$CMD > $OUT/plain1.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
+  -k regex:"dffm|fwd_|mlp_tc|tc_prep|unpack" --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none"
 for W in cfg2 cfg5; do
   python tools/one_forward.py $W > $OUT/plain_$W.log 2>&1 && timeout 900 ncu $M --nvtx --nvtx-include "step/" \
