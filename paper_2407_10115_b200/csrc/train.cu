@@ -35,6 +35,10 @@ namespace dffm {
 #endif
 constexpr int TR_THREADS = DFFM_TR_THREADS;
 constexpr int TR_WARPS = TR_THREADS / 32;
+#ifndef DFFM_TR_HW_THREADS
+#define DFFM_TR_HW_THREADS 512
+#endif
+constexpr int TR_HW_THREADS = DFFM_TR_HW_THREADS;  // threads per Hogwild worker (K6)
 constexpr int TR_CLUSTER = 8;  // CTAs per cluster for the split trainer
 
 // Phase timestamps (debug builds only, -DDFFM_TR_TRACE): SM clock of thread 0
@@ -167,7 +171,9 @@ __device__ __forceinline__ void adagrad_m(float* w, float* acc, double g, double
 // Block-wide f64 sum (all threads call); result broadcast to all.  One
 // barrier: warps publish partials into a ping-pong slot, then every thread
 // folds the TR_WARPS partials itself in a fixed order (deterministic).
+template <int NW = TR_WARPS>
 __device__ double block_sum(double v, double* red, int& ctr) {
+  constexpr int TR_WARPS = NW;
   // every thread calls block_sum the same number of times, so the per-thread
   // call counter selects the same ping-pong slot block-wide; reusing a slot
   // two calls later is ordered by the intervening call's barrier
@@ -193,8 +199,12 @@ __device__ __forceinline__ double sigmoid_raw(double logit) {  // M:293-297
   return e / (1.0 + e);
 }
 
-template <int C>
-__global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
+// NT threads per CTA: 1024 for the sequential trainer (one chain, all of the
+// SM); the Hogwild workers use NT = 512 so two workers share an SM
+template <int C, int NT = TR_THREADS>
+__global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
+  constexpr int TR_THREADS = NT;  // shadow the file-wide defaults inside the kernel
+  constexpr int TR_WARPS = NT / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int F = p.F, M = p.M, k = p.k, P = p.P, D = p.D, FM = F * M, Fk = F * k;
   const TrSmem L =
@@ -454,7 +464,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         if (pres[f]) lo += lrp[f];
       v[0] = lo;
     }
-    const double psum = block_sum(psum_part, red, bsc);
+    const double psum = block_sum<TR_WARPS>(psum_part, red, bsc);
     ffm_bad = __syncthreads_or(ffm_bad);
     const double lr_out = v[0];
     const double mu = (psum + lr_out) / D;
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       const double c = v[i] - mu;
       sq_part += c * c;
     }
-    const double sd = sqrt(block_sum(sq_part, red, bsc) / D);  // np.std (population)
+    const double sd = sqrt(block_sum<TR_WARPS>(sq_part, red, bsc) / D);  // np.std (population)
     const double denom = sd + 1e-6;
     int merge_bad = 0;
     for (int i = tid; i < D; i += TR_THREADS) {
@@ -530,7 +540,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
       const int I = p.dims[NL - 1];
       double s = 0.0;
       for (int i = tid; i < I; i += TR_THREADS) s += a[i] * ldm(&Wl[NL - 1][i], mg);
-      nn_out = block_sum(s, red, bsc) + ldm(&bl[NL - 1][0], mg);  // M:372-373
+      nn_out = block_sum<TR_WARPS>(s, red, bsc) + ldm(&bl[NL - 1][0], mg);  // M:372-373
       nn_bad = __syncthreads_or(nn_bad);
     }
     TR_MARK(7);
@@ -638,8 +648,8 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(TrainParams p) {
         s_d += dmerged[i];
         s_dc += dmerged[i] * (v[i] - mu);
       }
-      const double mean_d = block_sum(s_d, red, bsc) / D;
-      const double dot_dc = block_sum(s_dc, red, bsc);
+      const double mean_d = block_sum<TR_WARPS>(s_d, red, bsc) / D;
+      const double dot_dc = block_sum<TR_WARPS>(s_dc, red, bsc);
       for (int i = tid; i < D; i += TR_THREADS) {
         double x = (dmerged[i] - mean_d) / denom;
         if (sd > 0.0) x = x - (v[i] - mu) * (dot_dc / (D * sd * denom * denom));
@@ -936,12 +946,13 @@ extern "C" int dffm_train_hogwild(const dffm_model* model, const dffm_train_stat
   p.status = status;
   p.n = n;
   int occ = 0;
-  rc = kernel_occupancy((const void*)train_kernel<1>, TR_THREADS, smem, &occ);
+  rc = kernel_occupancy((const void*)train_kernel<1, TR_HW_THREADS>, TR_HW_THREADS, smem, &occ);
   if (rc) return rc;
   // concurrent workers only: a CTA that could not be resident would run later,
   // in series with the others
   const int64_t W = std::min<int64_t>({(int64_t)n_workers, (int64_t)occ * sm_count_current(), n});
-  note_launches(1), train_kernel<1><<<(unsigned)W, TR_THREADS, smem, (cudaStream_t)stream>>>(p);
+  note_launches(1), train_kernel<1, TR_HW_THREADS><<<(unsigned)W, TR_HW_THREADS, smem,
+                                                      (cudaStream_t)stream>>>(p);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(train hogwild)");
   return DFFM_OK;
 }
@@ -952,6 +963,7 @@ extern "C" int dffm_hogwild_max_workers(const dffm_model* model, int32_t max_per
   if (tr_validate(model, max_per_field, 1, p, &smem)) return 0;
   smem = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 0).total;
   int occ = 0;
-  if (kernel_occupancy((const void*)train_kernel<1>, TR_THREADS, smem, &occ)) return 0;
+  if (kernel_occupancy((const void*)train_kernel<1, TR_HW_THREADS>, TR_HW_THREADS, smem, &occ))
+    return 0;
   return occ * sm_count_current();
 }
