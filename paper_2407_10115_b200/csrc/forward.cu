@@ -378,7 +378,7 @@ int64_t tc_default_slice_rows() {
   static int64_t slice_env = -1;
   if (slice_env < 0) {
     const char* v = getenv("DFFM_TC_SLICE");
-    slice_env = v ? atoll(v) : (int64_t)4 * 148 * TC_M;
+    slice_env = v ? atoll(v) : (int64_t)32 * 148 * TC_M;  // 606,208 rows: fewer pipeline fills (cfg2 +4%)
     slice_env = std::max<int64_t>(TC_M, slice_env / TC_M * TC_M);
   }
   return slice_env;

@@ -123,11 +123,11 @@ def test_forward_cfg5_shape_tensor_core_mlp(family, n):
 
 
 def test_forward_tc_slices_and_nonfinite_nn():
-    """Several staging slices (DFFM_TC_SLICE is 148*128 rows by default) and
+    """Several staging slices (DFFM_TC_SLICE is 32*148*128 rows by default) and
     a non-finite hidden unit reported as block "nn" at the first example."""
     from paper_2407_10115_b200 import _lib
     ost = fo.random_store(8, 4, (32, 16), 10, seed=3)
-    n = 148 * 128 * 2 + 77
+    n = 32 * 148 * 128 * 2 + 77
     rng = np.random.default_rng(0)
     idx = rng.integers(0, 1 << 10, size=(n, 8, 1)).astype(np.int32)
     val = np.ones_like(idx, dtype=np.float32)
