@@ -25,7 +25,7 @@ constexpr int TC_THREADS = 64 + 32 * (TC_EPI_WARPS + TC_SPLIT_WARPS);
 constexpr int TC_PART_MAX = 256 / TC_PARTS;  // accumulator columns per epilogue thread
 constexpr int TC_WIDTH_MULT = 16;            // hidden widths: multiples of this, <= 256
 #ifndef DFFM_TC_GROUP
-#define DFFM_TC_GROUP 8
+#define DFFM_TC_GROUP 16
 #endif
 constexpr int TC_GROUP = DFFM_TC_GROUP;  // K chunks per TMEM accumulation group
 constexpr int TC_MAX_STAGES = 8;

@@ -24,7 +24,7 @@ pin = lambda a: torch.from_numpy(a.copy()).pin_memory()  # noqa: E731
 pkh = PackedBatch(pin(pk.ex_off), pin(pk.cnt), pin(pk.idx_bytes), pk.idx_width, pin(pk.vbits),
                   pin(pk.vals), pin(pk.voff), pk.max_per_field)
 out = torch.empty(n, dtype=torch.float32).pin_memory()
-for ch in [1 << 17, 75776 * 2, 75776 * 3, 75776 * 4]:
+for ch in [1 << 17, 1 << 18, 1 << 19]:
     hp = HostPredictor(st, n, idx.shape[2], chunk=ch)
     for name, fn in [("ragged", lambda: hp.predict_ragged(rbh, out)),
                      ("packed", lambda: hp.predict_packed(pkh, out))]:
