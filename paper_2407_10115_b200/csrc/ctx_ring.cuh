@@ -41,7 +41,10 @@ namespace dffm {
 #ifndef DFFM_CR_NMW
 #define DFFM_CR_NMW 6
 #endif
-constexpr int CR_NPW = DFFM_CR_NPW, CR_NISS = 2, CR_NMW = DFFM_CR_NMW;
+#ifndef DFFM_CR_NISS
+#define DFFM_CR_NISS 2
+#endif
+constexpr int CR_NPW = DFFM_CR_NPW, CR_NISS = DFFM_CR_NISS, CR_NMW = DFFM_CR_NMW;
 constexpr int CR_GT = DFFM_CR_GT;  // candidate groups of pair warps (power of 2)
 constexpr int CR_THREADS = (CR_NPW + 1 + CR_NISS + CR_NMW) * 32;
 constexpr int CR_MAXX = 64;   // candidate slots in flight

@@ -207,3 +207,21 @@ def test_context_ring_edge_cases_match_oracle(wdtype, Mc, Md, C, monkeypatch):
     cst, ridx, _ = compact_oracle(st, mi.reshape(R * C, F, M))
     _, ref = fo.forward_batch(ridx, mv.reshape(R * C, F, M), cst)
     assert np.abs(p.reshape(-1) - ref).max() <= 1e-6
+
+
+def test_context_ring_bad_context_index_is_contract_error(monkeypatch):
+    """K3 v2: an out-of-range context bucket raises ContractError (reported at
+    the request's first candidate)."""
+    monkeypatch.delenv("DFFM_CTX_MLP", raising=False)
+    bits = 10
+    ost = fo.random_store(12, 8, (16,), bits, seed=3)
+    cfg = ModelConfig(n_fields=12, k=8, hidden_sizes=(16,), hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, with_optimizer=False)
+    R, C = 5, 64
+    rng = np.random.default_rng(0)
+    ci = rng.integers(0, 1 << bits, size=(R, 8, 1)).astype(np.int32)
+    di = rng.integers(0, 1 << bits, size=(R, C, 4, 1)).astype(np.int32)
+    ci[3, 2, 0] = 1 << bits  # out of range
+    with pytest.raises(ContractError):
+        inference.score_requests(ci, np.ones_like(ci, np.float32), di,
+                                 np.ones_like(di, np.float32), st)

@@ -116,3 +116,32 @@ def test_host_predictor_packed_equals_padded(wl_name):
     out = torch.empty(n, dtype=torch.float32).pin_memory()
     hp.predict_packed(pkh, out)
     assert torch.equal(out, ref)
+
+
+def test_host_predictor_packed_reports_global_example_index():
+    """A non-finite row hit only by an example in a later chunk is reported at
+    that example's batch-global index (status_base per chunk), as M:392-396."""
+    from paper_2407_10115_b200.errors import NumericError
+    wl = configs.CFG2
+    bits = 12
+    ost = fo.random_store(wl.n_fields, wl.k, wl.hidden, bits, seed=12)
+    n = 10_000
+    idx, val = synth.make_examples(wl, n, seed=13, hash_bits=bits)
+    bad_e = 7_777
+    j = int(idx[bad_e, 3, 0])
+    ix = idx.numpy().copy()
+    ix[:, :, :][ix == j] = -1  # only example bad_e keeps bucket j
+    ix[bad_e, 3, 0] = j
+    vv = np.where(ix >= 0, val.numpy(), 0).astype(np.float32)
+    ost.ffm[j, 5, 0] = np.inf
+    cfg = ModelConfig(n_fields=wl.n_fields, k=wl.k, hidden_sizes=wl.hidden, hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, "f32", False)
+    pk = PackedBatch.from_ragged(RaggedBatch.from_padded(ix, vv))
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    pkh = PackedBatch(pin(pk.ex_off), pin(pk.cnt), pin(pk.idx_bytes), pk.idx_width,
+                      pin(pk.vbits), pin(pk.vals), pin(pk.voff), pk.max_per_field)
+    hp = HostPredictor(st, n, ix.shape[2], chunk=2048)
+    out = torch.empty(n, dtype=torch.float32).pin_memory()
+    with pytest.raises(NumericError) as ei:
+        hp.predict_packed(pkh, out)
+    assert ei.value.example == bad_e and ei.value.block == "ffm"
