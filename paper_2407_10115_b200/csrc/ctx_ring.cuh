@@ -369,15 +369,30 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
             for (int m = 0; m < Mc; ++m) pr |= (csidx[x * Mc + m] >= 0);
             cpres[x] = pr;
           }
+          // 16-byte vectors of the context rows (one load per slot per vector,
+          // all in flight together); same f32 fma over the slots in slot order
           const int Fk = F * p.k;
-          for (int t2 = tid; t2 < Fc * Fk; t2 += nthr) {
-            const int x = t2 / Fk, gk = t2 - x * Fk;
-            float acc = 0.f;
+          constexpr int PER = 16 / (int)sizeof(T);
+          const int nvec = Fk / PER;  // rows are whole 16-byte vectors (k * esz % 16 == 0)
+          for (int t2 = tid; t2 < Fc * nvec; t2 += nthr) {
+            const int x = t2 / nvec, v = t2 - x * nvec;
+            float acc[PER];
+#pragma unroll
+            for (int u = 0; u < PER; ++u) acc[u] = 0.f;
             for (int m = 0; m < Mc; ++m) {
               const int j = csidx[x * Mc + m];
-              if (j >= 0) acc = fmaf(csval[x * Mc + m], load_elem<T>(ffm + (int64_t)j * Fk + gk, p.dffm), acc);
+              if (j >= 0) {
+                float w[PER];
+                unpack16<T>(*(const uint4*)((const unsigned char*)p.ffm +
+                                            ((int64_t)j * Fk + v * PER) * (int64_t)sizeof(T)),
+                            w, p.dffm);
+                const float xv = csval[x * Mc + m];
+#pragma unroll
+                for (int u = 0; u < PER; ++u) acc[u] = fmaf(xv, w[u], acc[u]);
+              }
             }
-            S[t2] = acc;
+#pragma unroll
+            for (int u = 0; u < PER; ++u) S[x * Fk + v * PER + u] = acc[u];
           }
           named_bar_sync(1, nthr);
           for (int pp = tid; pp < P; pp += nthr) cpx[pp] = 0.f;
