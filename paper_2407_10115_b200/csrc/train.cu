@@ -366,7 +366,38 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
     // every load of the field is issued before the first sum (one memory
     // latency per example instead of one per 32-wide column step), sums in
     // slot order as before.
-    if (Fk <= 256 && M <= 4) {
+    // Spare warps (warp >= F) build the duplicate lists meanwhile (below).
+    const bool dup_split = Fk <= 256 && M <= 4 && TR_WARPS - F >= 4;
+    if (dup_split && warp >= F) {
+      const int dt = tid - F * 32, dn = (TR_WARPS - F) * 32;
+      for (int s = dt; s < FM; s += dn) {
+        lead[s] = sidx[s] >= 0 ? s : -1;
+        nxt[s] = 0x7fffffff;
+      }
+      named_bar_sync(2, dn);
+      for (int t = dt; t < FM * FM; t += dn) {
+        const int s = t / FM, s2 = t - s * FM;
+        if (s2 != s && sidx[s] >= 0 && sidx[s2] == sidx[s]) {
+          if (s2 < s) atomicMin(&lead[s], s2);
+          else atomicMin(&nxt[s], s2);
+        }
+      }
+      named_bar_sync(2, dn);
+      for (int s = dt; s < FM; s += dn)
+        if (nxt[s] == 0x7fffffff) nxt[s] = -1;
+      named_bar_sync(2, dn);
+      if (warp == F) {
+        int cnt = 0;
+        for (int s0 = 0; s0 < FM; s0 += 32) {
+          const int s = s0 + lane;
+          const bool isl = s < FM && lead[s] == s;
+          const unsigned bm = __ballot_sync(0xffffffffu, isl);
+          if (isl) ulist[cnt + __popc(bm & ((1u << lane) - 1u))] = s;
+          cnt += __popc(bm);
+        }
+        if (lane == 0) *nuniq = cnt;
+      }
+    } else if (Fk <= 256 && M <= 4) {
       for (int f = warp; f < F; f += TR_WARPS) {
         int js[4];
         double xs[4];
@@ -411,35 +442,37 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
     // slot holding the bucket, nxt = next slot of the same bucket; the
     // leaders (one per unique bucket, occurrence order) are compacted into
     // ulist by warp 0
-    for (int s = tid; s < FM; s += TR_THREADS) {
-      lead[s] = sidx[s] >= 0 ? s : -1;
-      nxt[s] = 0x7fffffff;
-    }
-    __syncthreads();
-    TR_MARK(2);
-    // all (s, s2) slot pairs in parallel: lead = smallest equal slot, nxt =
-    // smallest equal slot after s
-    for (int t = tid; t < FM * FM; t += TR_THREADS) {
-      const int s = t / FM, s2 = t - s * FM;
-      if (s2 != s && sidx[s] >= 0 && sidx[s2] == sidx[s]) {
-        if (s2 < s) atomicMin(&lead[s], s2);
-        else atomicMin(&nxt[s], s2);
+    if (!dup_split) {
+      for (int s = tid; s < FM; s += TR_THREADS) {
+        lead[s] = sidx[s] >= 0 ? s : -1;
+        nxt[s] = 0x7fffffff;
       }
-    }
-    __syncthreads();
-    for (int s = tid; s < FM; s += TR_THREADS)
-      if (nxt[s] == 0x7fffffff) nxt[s] = -1;
-    __syncthreads();
-    if (warp == 0) {
-      int cnt = 0;
-      for (int s0 = 0; s0 < FM; s0 += 32) {
-        const int s = s0 + lane;
-        const bool isl = s < FM && lead[s] == s;
-        const unsigned bm = __ballot_sync(0xffffffffu, isl);
-        if (isl) ulist[cnt + __popc(bm & ((1u << lane) - 1u))] = s;
-        cnt += __popc(bm);
+      __syncthreads();
+      TR_MARK(2);
+      // all (s, s2) slot pairs in parallel: lead = smallest equal slot, nxt =
+      // smallest equal slot after s
+      for (int t = tid; t < FM * FM; t += TR_THREADS) {
+        const int s = t / FM, s2 = t - s * FM;
+        if (s2 != s && sidx[s] >= 0 && sidx[s2] == sidx[s]) {
+          if (s2 < s) atomicMin(&lead[s], s2);
+          else atomicMin(&nxt[s], s2);
+        }
       }
-      if (lane == 0) *nuniq = cnt;
+      __syncthreads();
+      for (int s = tid; s < FM; s += TR_THREADS)
+        if (nxt[s] == 0x7fffffff) nxt[s] = -1;
+      __syncthreads();
+      if (warp == 0) {
+        int cnt = 0;
+        for (int s0 = 0; s0 < FM; s0 += 32) {
+          const int s = s0 + lane;
+          const bool isl = s < FM && lead[s] == s;
+          const unsigned bm = __ballot_sync(0xffffffffu, isl);
+          if (isl) ulist[cnt + __popc(bm & ((1u << lane) - 1u))] = s;
+          cnt += __popc(bm);
+        }
+        if (lane == 0) *nuniq = cnt;
+      }
     }
     __syncthreads();
     TR_MARK(3);
