@@ -340,3 +340,120 @@ def parse_lines(text, schema: InputSchema, device, keep_f64: bool = False,
         if err is not None:
             raise ParseError(f"line {err[0] + 1}: {err[1]}")
     return out
+
+
+class HostTextParser:
+    """K10 from pinned host text, pipelined: the batch's lines are cut into
+    chunks; chunk j+1's text and line offsets travel host->device on a copy
+    stream while K10 parses chunk j on the compute stream, so the link and the
+    parse overlap (``parse_lines`` copies the whole text, then parses).
+
+    Each chunk is one ``fw_parse_lines`` + ``fw_parse_emit`` call on global
+    pointers: the text window base is relative to the chunk's first line
+    (line_off[0]), so chunk-sized scratch suffices and labels/status/cnt land
+    at the chunk's global rows.  idx/val of chunk j start at element
+    (off[c0] // 2 + c0) of one buffer -- every chunk's capacity (bytes/2 +
+    lines) fits below the next chunk's base -- so no host read of a chunk's
+    total is needed between chunks.  ``__call__`` returns a ParsedLines per
+    chunk (RaggedBatch views) after one synchronise at the end."""
+
+    def __init__(self, schema: InputSchema, device, max_lines: int, max_bytes: int,
+                 chunk_lines: int = 1 << 17):
+        import torch
+
+        from . import _lib
+        self.schema, self.dev = schema, torch.device(device)
+        self.chunk = max(1, int(min(chunk_lines, max(1, max_lines))))
+        self.max_lines, self.max_bytes = int(max_lines), int(max_bytes)
+        F = schema.n_fields
+        names = b"".join(nm.encode("utf-8") for nm in schema.field_names)
+        noff = np.zeros(F + 1, np.int32)
+        np.cumsum([len(nm.encode("utf-8")) for nm in schema.field_names], out=noff[1:])
+        numeric = np.array([nm in schema.numeric_fields for nm in schema.field_names], np.uint8)
+        dev = self.dev
+        self.t_names = torch.frombuffer(bytearray(names or b"\0"), dtype=torch.uint8).to(dev)
+        self.t_noff = torch.from_numpy(noff).to(dev)
+        self.t_num = torch.from_numpy(numeric).to(dev)
+        self.d_text = torch.empty(max(1, self.max_bytes), dtype=torch.uint8, device=dev)
+        self.d_off = torch.empty(self.max_lines + 1, dtype=torch.int64, device=dev)
+        nchunks_max = (self.max_lines + self.chunk - 1) // self.chunk + 1
+        cap = self.max_bytes // 2 + self.max_lines + 1
+        self.idx = torch.empty(cap, dtype=torch.int32, device=dev)
+        self.val = torch.empty(cap, dtype=torch.float32, device=dev)
+        self.labels = torch.empty(max(1, self.max_lines), dtype=torch.uint8, device=dev)
+        self.status = torch.empty(max(1, self.max_lines), dtype=torch.int32, device=dev)
+        self.cnt = torch.empty((max(1, self.max_lines), F), dtype=torch.uint8, device=dev)
+        self.ex_off = torch.empty(self.max_lines + nchunks_max, dtype=torch.int64, device=dev)
+        self.mx = torch.empty(nchunks_max, dtype=torch.int32, device=dev)
+        self.scratch_cap = 0
+        self.scratch = None
+        self.copy_stream = torch.cuda.Stream(dev)
+        self.compute_stream = torch.cuda.Stream(dev)
+        self._lib = _lib
+
+    def _bounds(self, off: np.ndarray):
+        n = len(off) - 1
+        return [(c0, min(n, c0 + self.chunk)) for c0 in range(0, n, self.chunk)]
+
+    def __call__(self, h_text, h_off, status_host=None):
+        """``h_text``: pinned uint8 tensor of the text, ``h_off``: pinned int64
+        tensor of line offsets [n+1] (``split_lines``); optional pinned int32
+        ``status_host`` [n] receives the per-line status (D2H inside the
+        pipeline).  Returns a list of (c0, c1, ParsedLines) per chunk."""
+        import torch
+        lib = self._lib.lib()
+        off = h_off.numpy()
+        n = len(off) - 1
+        if n > self.max_lines or int(off[-1]) > self.max_bytes:
+            raise ContractError(f"{n} lines / {int(off[-1])} bytes exceed the parser's "
+                                f"{self.max_lines} / {self.max_bytes}")
+        bounds = self._bounds(off)
+        need = max((int(lib.fw_parse_scratch_bytes(c1 - c0, int(off[c1] - off[c0])))
+                    for c0, c1 in bounds), default=0)
+        if need > self.scratch_cap:
+            self.scratch = torch.empty(need, dtype=torch.uint8, device=self.dev)
+            self.scratch_cap = need
+        cs, ks = self.copy_stream, self.compute_stream
+        cs.wait_stream(torch.cuda.current_stream(self.dev))
+        ks.wait_stream(cs)
+        F = self.schema.n_fields
+        evs = []
+        for j, (c0, c1) in enumerate(bounds):
+            b0, b1 = int(off[c0]), int(off[c1])
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(cs):
+                self.d_text[b0:b1].copy_(h_text[b0:b1], non_blocking=True)
+                self.d_off[c0:c1 + 1].copy_(h_off[c0:c1 + 1], non_blocking=True)
+                ev.record(cs)
+            evs.append(ev)
+            base = b0 // 2 + c0
+            eo = self.ex_off[c0 + j:c1 + j + 1]
+            with torch.cuda.stream(ks):
+                ks.wait_event(ev)
+                self._lib.check(lib.fw_parse_lines(
+                    self.d_text.data_ptr(), self.d_off[c0:].data_ptr(), c1 - c0, b1 - b0,
+                    self.t_names.data_ptr(), self.t_noff.data_ptr(), self.t_num.data_ptr(), F,
+                    self.schema.hash_bits, self.scratch.data_ptr(),
+                    self.labels[c0:].data_ptr(), self.status[c0:].data_ptr(),
+                    self.cnt[c0:].data_ptr(), eo.data_ptr(), self.mx[j:].data_ptr(),
+                    ks.cuda_stream), "fw_parse_lines")
+                self._lib.check(lib.fw_parse_emit(
+                    self.d_off[c0:].data_ptr(), c1 - c0, b1 - b0, self.scratch.data_ptr(),
+                    eo.data_ptr(), self.idx[base:].data_ptr(), self.val[base:].data_ptr(),
+                    None, ks.cuda_stream), "fw_parse_emit")
+                if status_host is not None:
+                    status_host[c0:c1].copy_(self.status[c0:c1], non_blocking=True)
+        with torch.cuda.stream(ks):
+            ends = torch.tensor([c1 + j for j, (_, c1) in enumerate(bounds)], dtype=torch.int64,
+                                device=self.dev) if bounds else None
+            tail = (torch.stack([self.ex_off[ends], self.mx[:len(bounds)].to(torch.int64)])
+                    .cpu() if bounds else None)
+        ks.synchronize()
+        out = []
+        for j, (c0, c1) in enumerate(bounds):
+            nnz, mxc = int(tail[0, j]), int(tail[1, j])
+            base = int(off[c0]) // 2 + c0
+            rb = RaggedBatch(self.ex_off[c0 + j:c1 + j + 1], self.cnt[c0:c1],
+                             self.idx[base:base + nnz], self.val[base:base + nnz], max(1, mxc))
+            out.append((c0, c1, ParsedLines(rb, self.labels[c0:c1], self.status[c0:c1])))
+        return out

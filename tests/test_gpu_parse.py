@@ -112,3 +112,38 @@ def test_parsed_lines_feed_the_forward():
     prob = predict_batch(pi, pv, store).double().cpu().numpy()
     _, ref = fo.forward_batch(pi.cpu().numpy(), pv.cpu().numpy(), ost)
     assert (np.abs(prob - ref) / ref).max() < 1e-5
+
+
+@pytest.mark.parametrize("chunk", [1, 7, 4096, 1 << 17])
+def test_host_text_parser_chunks_match_parse_lines(chunk):
+    """HostTextParser (pinned host text, chunked H2D overlapped with K10) gives,
+    chunk by chunk, exactly the rows of one parse_lines call: status, labels,
+    counts, ragged offsets, indices and values; failed and blank lines included."""
+    from paper_2407_10115_b200.features import HostTextParser
+    names, lines = _random_lines(9000 if chunk > 1 else 300, 13)
+    lines[5] = "7 |f1 x"            # bad label
+    lines[17] = "   "                # blank
+    lines[-1] = "1 |nofield t"       # unknown field, last line
+    sc = InputSchema(tuple(names), frozenset(names[20:]), 20)
+    text = ("\n".join(lines) + "\n").encode()
+    ref = parse_lines(text, sc, DEV, raise_on_error=False)
+    buf, off = split_lines(text)
+    h_text = torch.from_numpy(buf.copy()).pin_memory()
+    h_off = torch.from_numpy(off).pin_memory()
+    st_h = torch.full((len(lines),), -1, dtype=torch.int32).pin_memory()
+    p = HostTextParser(sc, DEV, len(lines), len(buf), chunk_lines=chunk)
+    for _ in range(2):  # second call reuses every buffer
+        parts = p(h_text, h_off, st_h)
+        assert [c0 for c0, _, _ in parts] == list(range(0, len(lines), min(chunk, len(lines))))
+        assert torch.equal(st_h, ref.status.cpu())
+        r_off = ref.batch.ex_off.cpu()
+        for c0, c1, pl in parts:
+            assert torch.equal(pl.status.cpu(), ref.status[c0:c1].cpu())
+            assert torch.equal(pl.labels.cpu(), ref.labels[c0:c1].cpu())
+            assert torch.equal(pl.batch.cnt.cpu(), ref.batch.cnt[c0:c1].cpu())
+            assert torch.equal(pl.batch.ex_off.cpu(), r_off[c0:c1 + 1] - r_off[c0])
+            z0, z1 = int(r_off[c0]), int(r_off[c1])
+            assert torch.equal(pl.batch.idx.cpu(), ref.batch.idx[z0:z1].cpu())
+            assert torch.equal(pl.batch.val.cpu(), ref.batch.val[z0:z1].cpu())
+    with pytest.raises(Exception, match="exceed"):
+        HostTextParser(sc, DEV, 10, 100)(h_text, h_off)
