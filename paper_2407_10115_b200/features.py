@@ -345,8 +345,9 @@ def parse_lines(text, schema: InputSchema, device, keep_f64: bool = False,
 class HostTextParser:
     """K10 from pinned host text, pipelined: the batch's lines are cut into
     chunks; chunk j+1's text and line offsets travel host->device on a copy
-    stream while K10 parses chunk j on the compute stream, so the link and the
-    parse overlap (``parse_lines`` copies the whole text, then parses).
+    stream while K10 parses chunk j on one of two compute streams (consecutive
+    chunks' parses overlap too), so the link and the parse overlap
+    (``parse_lines`` copies the whole text, then parses).
 
     Each chunk is one ``fw_parse_lines`` + ``fw_parse_emit`` call on global
     pointers: the text window base is relative to the chunk's first line
@@ -386,9 +387,11 @@ class HostTextParser:
         self.ex_off = torch.empty(self.max_lines + nchunks_max, dtype=torch.int64, device=dev)
         self.mx = torch.empty(nchunks_max, dtype=torch.int32, device=dev)
         self.scratch_cap = 0
-        self.scratch = None
+        self.scratch = [None, None]
         self.copy_stream = torch.cuda.Stream(dev)
-        self.compute_stream = torch.cuda.Stream(dev)
+        # two compute streams, alternate chunks: K10 is one thread per line, so one
+        # chunk's launches leave most of the machine idle; consecutive chunks overlap
+        self.compute_streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
         self._lib = _lib
 
     def _bounds(self, off: np.ndarray):
@@ -411,11 +414,13 @@ class HostTextParser:
         need = max((int(lib.fw_parse_scratch_bytes(c1 - c0, int(off[c1] - off[c0])))
                     for c0, c1 in bounds), default=0)
         if need > self.scratch_cap:
-            self.scratch = torch.empty(need, dtype=torch.uint8, device=self.dev)
+            self.scratch = [torch.empty(need, dtype=torch.uint8, device=self.dev)
+                            for _ in range(2)]
             self.scratch_cap = need
-        cs, ks = self.copy_stream, self.compute_stream
+        cs = self.copy_stream
         cs.wait_stream(torch.cuda.current_stream(self.dev))
-        ks.wait_stream(cs)
+        for ks in self.compute_streams:
+            ks.wait_stream(cs)
         F = self.schema.n_fields
         evs = []
         for j, (c0, c1) in enumerate(bounds):
@@ -428,21 +433,24 @@ class HostTextParser:
             evs.append(ev)
             base = b0 // 2 + c0
             eo = self.ex_off[c0 + j:c1 + j + 1]
+            ks, scr = self.compute_streams[j & 1], self.scratch[j & 1]
             with torch.cuda.stream(ks):
                 ks.wait_event(ev)
                 self._lib.check(lib.fw_parse_lines(
                     self.d_text.data_ptr(), self.d_off[c0:].data_ptr(), c1 - c0, b1 - b0,
                     self.t_names.data_ptr(), self.t_noff.data_ptr(), self.t_num.data_ptr(), F,
-                    self.schema.hash_bits, self.scratch.data_ptr(),
+                    self.schema.hash_bits, scr.data_ptr(),
                     self.labels[c0:].data_ptr(), self.status[c0:].data_ptr(),
                     self.cnt[c0:].data_ptr(), eo.data_ptr(), self.mx[j:].data_ptr(),
                     ks.cuda_stream), "fw_parse_lines")
                 self._lib.check(lib.fw_parse_emit(
-                    self.d_off[c0:].data_ptr(), c1 - c0, b1 - b0, self.scratch.data_ptr(),
+                    self.d_off[c0:].data_ptr(), c1 - c0, b1 - b0, scr.data_ptr(),
                     eo.data_ptr(), self.idx[base:].data_ptr(), self.val[base:].data_ptr(),
                     None, ks.cuda_stream), "fw_parse_emit")
                 if status_host is not None:
                     status_host[c0:c1].copy_(self.status[c0:c1], non_blocking=True)
+        ks = self.compute_streams[0]
+        ks.wait_stream(self.compute_streams[1])
         with torch.cuda.stream(ks):
             ends = torch.tensor([c1 + j for j, (_, c1) in enumerate(bounds)], dtype=torch.int64,
                                 device=self.dev) if bounds else None
