@@ -221,10 +221,32 @@ __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
   uint8_t label = 0;
   // unsupported (non-ASCII whitespace) anywhere in the line; whitespace-only
   // lines are "blank" (skipped by the stream loops, T:176)
+  // (8-byte words where aligned: an all-ASCII word needs no per-byte reload)
   bool blank = true;
-  for (int64_t q = b; q < e; ++q) {
-    blank &= is_ws(s[q]);
-    if (s[q] >= 0xC2 && unicode_ws_at(s, q, e)) { st = PS_UNSUPPORTED; break; }
+  {
+    const int64_t head = (int64_t)((8 - ((uintptr_t)(s + b) & 7)) & 7);
+    const int64_t qa = b + head < e ? b + head : e;
+    int64_t q = b;
+    for (; q < qa && st == PS_OK; ++q) {
+      blank &= is_ws(s[q]);
+      if (s[q] >= 0xC2 && unicode_ws_at(s, q, e)) st = PS_UNSUPPORTED;
+    }
+    for (; q + 8 <= e && st == PS_OK; q += 8) {
+      const uint64_t w = *reinterpret_cast<const uint64_t*>(s + q);
+      if (w & 0x8080808080808080ull) {
+        for (int k = 0; k < 8 && st == PS_OK; ++k) {
+          blank &= is_ws(s[q + k]);
+          if (s[q + k] >= 0xC2 && unicode_ws_at(s, q + k, e)) st = PS_UNSUPPORTED;
+        }
+      } else if (blank) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) blank &= is_ws((uint32_t)(w >> (8 * k)) & 0xffu);
+      }
+    }
+    for (; q < e && st == PS_OK; ++q) {
+      blank &= is_ws(s[q]);
+      if (s[q] >= 0xC2 && unicode_ws_at(s, q, e)) st = PS_UNSUPPORTED;
+    }
   }
   if (st == PS_OK && blank) st = PS_BLANK;
   // label (Fe:223-229)
