@@ -211,6 +211,28 @@ __device__ __forceinline__ int64_t ent_base(const ParseParams& p, int64_t i) {
   return (p.line_off[i] - p.line_off[0]) / 2 + i;
 }
 
+// first q in [from, e) with s[q] == c, else e; aligned 8-byte words, bytes only
+// in a word that may hold c (the zero-byte test has no false negatives)
+__device__ __forceinline__ int64_t find_byte(const uint8_t* s, int64_t from, int64_t e,
+                                             uint32_t c) {
+  int64_t q = from;
+  const int64_t head = (int64_t)((8 - ((uintptr_t)(s + q) & 7)) & 7);
+  for (const int64_t qa = q + head < e ? q + head : e; q < qa; ++q)
+    if (s[q] == c) return q;
+  const uint64_t pat = 0x0101010101010101ull * c;
+  for (; q + 8 <= e; q += 8) {
+    const uint64_t x = *reinterpret_cast<const uint64_t*>(s + q) ^ pat;
+    if ((x - 0x0101010101010101ull) & ~x & 0x8080808080808080ull) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (((x >> (8 * k)) & 0xffu) == 0) return q + k;
+    }
+  }
+  for (; q < e; ++q)
+    if (s[q] == c) return q;
+  return e;
+}
+
 __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
@@ -250,8 +272,7 @@ __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
   }
   if (st == PS_OK && blank) st = PS_BLANK;
   // label (Fe:223-229)
-  int64_t bar = b;
-  while (bar < e && s[bar] != '|') ++bar;
+  const int64_t bar = find_byte(s, b, e, '|');
   if (st == PS_OK) {
     int64_t h0 = b, h1 = bar;
     while (h0 < h1 && is_ws(s[h0])) ++h0;
@@ -266,8 +287,7 @@ __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
   const int64_t max_index = 1ll << p.hash_bits;
   int64_t q = bar;
   while (st == PS_OK && q < e) {  // one '|' block per iteration; q at its '|'
-    int64_t se = q + 1;
-    while (se < e && s[se] != '|') ++se;
+    const int64_t se = find_byte(s, q + 1, e, '|');
     int64_t a = q + 1;
     while (a < se && is_ws(s[a])) ++a;
     if (a >= se) { st = PS_EMPTY_BLOCK; break; }
