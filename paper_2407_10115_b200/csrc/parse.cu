@@ -312,10 +312,19 @@ __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
     while (st == PS_OK) {  // atoms after the name
       while (t < se && is_ws(s[t])) ++t;
       if (t >= se) break;
-      int64_t te = t;
-      while (te < se && !is_ws(s[te])) ++te;
-      int64_t colon = t;
-      while (colon < te && s[colon] != ':') ++colon;
+      // one pass over the atom: its end, its first ':' and the FNV-1a of the
+      // bytes before it (used when the atom is not a raw @index)
+      int64_t te = t, colon = -1;
+      uint32_t htok = hname;
+      for (; te < se; ++te) {
+        const uint32_t c = s[te];
+        if (is_ws(c)) break;
+        if (colon < 0) {
+          if (c == ':') colon = te;
+          else htok = (htok ^ c) * 0x01000193u;
+        }
+      }
+      if (colon < 0) colon = te;
       double value = 1.0;
       if (colon < te) {
         const int r = parse_float(s, colon + 1, te, &value);
@@ -338,9 +347,7 @@ __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
         if (big) { st = PS_RAW_RANGE; break; }
         index = v;
       } else {  // H:43-50 (+ Fe:215-218 numeric transform)
-        uint32_t h = hname;
-        for (int64_t k = t; k < colon; ++k) h = (h ^ s[k]) * 0x01000193u;
-        index = h & mask;
+        index = htok & mask;
         if (numeric && value > 0) value = log1p(value);
       }
       p.ent_key[eb + ne] = ((uint64_t)fid << 40) | ((uint64_t)index << 11) | (uint64_t)ne;
