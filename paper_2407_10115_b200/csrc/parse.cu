@@ -234,6 +234,15 @@ __device__ __forceinline__ int64_t find_byte(const uint8_t* s, int64_t from, int
 }
 
 __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
+  // schema lookup table: (name length << 32) | FNV-1a of the name, per field
+  __shared__ uint64_t ftab[256];
+  for (int f = threadIdx.x; f < p.F; f += blockDim.x) {
+    const int32_t o0 = p.name_off[f], o1 = p.name_off[f + 1];
+    uint32_t h = 0x811C9DC5u;
+    for (int32_t k = o0; k < o1; ++k) h = (h ^ p.names[k]) * 0x01000193u;
+    ftab[f] = ((uint64_t)(uint32_t)(o1 - o0) << 32) | h;
+  }
+  __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   const uint8_t* s = p.text;
@@ -292,20 +301,25 @@ __global__ void __launch_bounds__(128) parse_lines_kernel(ParseParams p) {
     while (a < se && is_ws(s[a])) ++a;
     if (a >= se) { st = PS_EMPTY_BLOCK; break; }
     int64_t ae = a;
-    while (ae < se && !is_ws(s[ae])) ++ae;
-    // field name lookup (InputSchema.field_id)
+    uint32_t hname = 0x811C9DC5u;
+    for (; ae < se; ++ae) {
+      const uint32_t c = s[ae];
+      if (is_ws(c)) break;
+      hname = (hname ^ c) * 0x01000193u;
+    }
+    // field name lookup (InputSchema.field_id): the first field whose name equals
+    // the atom; fields whose (length, hash) differ cannot, the rest are compared
     int fid = -1;
     const int64_t nl = ae - a;
+    const uint64_t key = nl <= 0xFFFFFFFFll ? ((uint64_t)nl << 32) | hname : ~0ull;
     for (int f = 0; f < p.F && fid < 0; ++f) {
-      const int32_t o0 = p.name_off[f], o1 = p.name_off[f + 1];
-      if (o1 - o0 != nl) continue;
+      if (ftab[f] != key) continue;
+      const int32_t o0 = p.name_off[f];
       bool eq = true;
       for (int64_t k = 0; k < nl && eq; ++k) eq = p.names[o0 + k] == s[a + k];
       if (eq) fid = f;
     }
     if (fid < 0) { st = PS_UNKNOWN_FIELD; break; }
-    uint32_t hname = 0x811C9DC5u;
-    for (int64_t k = a; k < ae; ++k) hname = (hname ^ s[k]) * 0x01000193u;
     hname = (hname ^ 0x1Fu) * 0x01000193u;
     const bool numeric = p.numeric[fid] != 0;
     int64_t t = ae;
