@@ -394,10 +394,7 @@ __global__ void __launch_bounds__(WARPS * 32) parse_canon_kernel(ParseParams p, 
   uint64_t* k = key[warp];
   double* sv = sval[warp];
   int* fc = fcnt[warp];
-  for (int64_t i = (int64_t)blockIdx.x * WARPS + warp; i < p.n;
-       i += (int64_t)gridDim.x * WARPS) {
-    const int ne = p.ent_n[i];
-    if (ne > CAP || (LO > 0 && ne <= LO)) continue;  // the other tier's line
+  auto line = [&](int64_t i, int ne) {
     const int64_t eb = ent_base(p, i);
     for (int f = lane; f < p.F; f += 32) fc[f] = 0;
     int np2 = 1;
@@ -460,6 +457,26 @@ __global__ void __launch_bounds__(WARPS * 32) parse_canon_kernel(ParseParams p, 
     if (big)
       for (int f = lane; f < p.F; f += 32) cnt[i * p.F + f] = 0;
     __syncwarp();
+  };
+  const int64_t w0 = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
+  if (LO == 0) {
+    for (int64_t i = w0; i < p.n; i += nw) {
+      const int ne = p.ent_n[i];
+      if (ne <= CAP) line(i, ne);  // longer lines: the other tier's
+    }
+  } else {
+    // the long-line tier sees few lines: 32 counts per coalesced load, a ballot
+    // picks this tier's lines
+    for (int64_t g = w0 * 32; g < p.n; g += nw * 32) {
+      const int64_t il = g + lane;
+      const int nel = il < p.n ? p.ent_n[il] : 0;
+      uint32_t pend = __ballot_sync(0xffffffffu, nel > LO && nel <= CAP);
+      while (pend) {
+        const int b = __ffs(pend) - 1;
+        pend &= pend - 1;
+        line(g + b, __shfl_sync(0xffffffffu, nel, b));
+      }
+    }
   }
 }
 
