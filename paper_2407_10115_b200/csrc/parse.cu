@@ -399,11 +399,41 @@ __global__ void __launch_bounds__(WARPS * 32) parse_canon_kernel(ParseParams p, 
     for (int f = lane; f < p.F; f += 32) fc[f] = 0;
     int np2 = 1;
     while (np2 < ne) np2 <<= 1;
-    for (int t = lane; t < np2; t += 32) {
-      k[t] = t < ne ? p.ent_key[eb + t] : ~0ull;
-      if (t < ne) sv[t] = p.ent_val[eb + t];
+    if (np2 <= 64) {
+      // keys unique (position in the low bits): bitonic sort of 64 in registers,
+      // element t = lane + 32 j in slot j, partners by shuffle (stride < 32)
+      uint64_t r0 = lane < ne ? p.ent_key[eb + lane] : ~0ull;
+      uint64_t r1 = lane + 32 < ne ? p.ent_key[eb + lane + 32] : ~0ull;
+      if (lane < ne) sv[lane] = p.ent_val[eb + lane];
+      if (lane + 32 < ne) sv[lane + 32] = p.ent_val[eb + lane + 32];
+#pragma unroll
+      for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          if (stride == 32) {  // size 64: slot 0 (t < 32) keeps the min
+            const uint64_t lo = r0 < r1 ? r0 : r1, hi = r0 < r1 ? r1 : r0;
+            r0 = lo, r1 = hi;
+          } else {
+            const bool lower = (lane & stride) == 0;
+            const uint64_t y0 = __shfl_xor_sync(0xffffffffu, r0, stride);
+            const uint64_t y1 = __shfl_xor_sync(0xffffffffu, r1, stride);
+            const bool up0 = (lane & size) == 0, up1 = ((lane + 32) & size) == 0;
+            r0 = (lower == up0) ? (r0 < y0 ? r0 : y0) : (r0 < y0 ? y0 : r0);
+            r1 = (lower == up1) ? (r1 < y1 ? r1 : y1) : (r1 < y1 ? y1 : r1);
+          }
+        }
+      }
+      k[lane] = r0;
+      k[lane + 32] = r1;
+      __syncwarp();
+      np2 = 0;  // sorted: skip the shared-memory network below
+    } else {
+      for (int t = lane; t < np2; t += 32) {
+        k[t] = t < ne ? p.ent_key[eb + t] : ~0ull;
+        if (t < ne) sv[t] = p.ent_val[eb + t];
+      }
+      __syncwarp();
     }
-    __syncwarp();
     for (int size = 2; size <= np2; size <<= 1) {  // bitonic sort, ascending
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
         for (int t = lane; t < np2; t += 32) {
