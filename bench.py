@@ -278,9 +278,13 @@ def run_reference(args, wl):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if wl.name == "cfg5_large_bf16" else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; reference CPU port on host cores)",
         "config": {"workload": wl.name, "sample_examples_per_step": sample,
+                   "same_config": "same workload recipe; each step scores a bounded sample of "
+                                  "its examples against a compact table of the rows they touch "
+                                  "(the per-example CPU rate does not depend on batch size)",
                    "n_fields": wl.n_fields, "k": wl.k, "hidden": list(wl.hidden),
                    "hash_bits": wl.hash_bits, "parallelism": f"{cores} forked processes"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -290,21 +294,104 @@ def run_reference(args, wl):
     }), flush=True)
 
 
-def run_ours(args, wl):
+def so_sha16() -> str:
+    import hashlib
+    p = os.path.join(REPO, "paper_2407_10115_b200", "libdffm.so")
+    try:
+        with open(p, "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()[:16]
+    except OSError:
+        return ""
+
+
+def ncu_traffic_for(workload: str):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    dominant kernel from the committed ncu capture, only if it was taken on the
+    libdffm.so that is loaded now (same sha); else None."""
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None, "no capture"
+    with open(p) as fh:
+        d = json.load(fh)
+    ent = d.get("captures", {}).get(workload)
+    if not ent:
+        return None, "no capture for this workload"
+    if ent.get("so_sha16") != so_sha16():
+        return None, f"capture taken on libdffm.so {ent.get('so_sha16')}, loaded {so_sha16()}"
+    return float(ent["dram_bytes_per_launch"]), ent.get("source", "")
+
+
+class LaunchTrace:
+    """Per-kernel device time of dffm_forward's launches inside the timed region:
+    the library records a caller-created CUDA event after every kernel it launches
+    on the launch stream and tags its role (dffm_set_event_trace), so the interval
+    ending at each event is that kernel's device time (kernels of one stream run
+    back to back)."""
+
+    TAGS = {0: "weight_blocking", 1: "gather", 2: "mlp", 3: "fused"}
+
+    def __init__(self, per_step: int, steps: int):
+        import ctypes
+
+        import torch
+        self.cap = per_step * steps
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(self.cap)]
+        for e in self.events:
+            e.record()  # creates the underlying cudaEvent_t
+        torch.cuda.synchronize()
+        self.handles = (ctypes.c_void_p * self.cap)(*[e.cuda_event for e in self.events])
+        self.tags = (ctypes.c_int32 * self.cap)()
+        self.count = ctypes.c_int32(0)
+        self.starts = []  # (step start event, first trace index of the step)
+
+    def __enter__(self):
+        import ctypes
+
+        from paper_2407_10115_b200 import _lib
+        _lib.check(_lib.lib().dffm_set_event_trace(self.handles, self.tags, self.cap,
+                                                   ctypes.byref(self.count)))
+        return self
+
+    def __exit__(self, *a):
+        from paper_2407_10115_b200 import _lib
+        _lib.lib().dffm_set_event_trace(None, None, 0, None)
+
+    def mark_step(self, start_event):
+        self.starts.append((start_event, int(self.count.value)))
+
+    def split(self):
+        """{role: (total ms, launches)} over every traced step."""
+        out = {}
+        bounds = [i for _, i in self.starts] + [int(self.count.value)]
+        for (s_ev, i0), i1 in zip(self.starts, bounds[1:]):
+            prev = s_ev
+            for i in range(i0, i1):
+                ms = prev.elapsed_time(self.events[i])
+                tag = self.TAGS.get(int(self.tags[i]), str(self.tags[i]))
+                t, c = out.get(tag, (0.0, 0))
+                out[tag] = (t + ms, c + 1)
+                prev = self.events[i]
+        return out
+
+
+def run_ours(args, wl, world, rank, local, dev, nested=False):
+    """Forward bench of one workload on this rank -> the JSON line's dict (rank 0
+    prints it).  cfg5 (the metric's "1/2/4/8 B200" config) divides its fixed
+    8,388,608-example batch across the ranks (strong scaling); cfg1/cfg2 give every
+    rank its own full batch (weak scaling)."""
     import torch
     import torch.distributed as dist
 
     from paper_2407_10115_b200 import _lib
     from paper_2407_10115_b200.model import HostPredictor, predict_batch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    n = wl.n_examples if wl.name != "cfg5_large_bf16" else wl.n_examples // max(world, 1)
-    if args.examples:
+    from paper_2407_10115_b200.parallel import shard_range
+    strong = wl.name == "cfg5_large_bf16"
+    if strong:
+        sh = shard_range(wl.n_examples, world, rank)
+        n = sh.size
+    else:
+        n = wl.n_examples
+    if args.examples and not nested:
         n = args.examples
     st = build_store(wl, dev)
     idx, val = build_inputs(wl, n, dev, rank)
@@ -325,20 +412,21 @@ def run_ours(args, wl):
         dist.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    trace = LaunchTrace(per_step=2 + 2 * (-(-n // (32 * 148 * 128))) + 4, steps=args.steps)
     lc0 = _lib.lib().dffm_launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, trace:
         torch.cuda.synchronize()
         for s, e in evs:
             flush.zero_()
             s.record()
+            trace.mark_step(s)
             step()
             e.record()
         torch.cuda.synchronize()
     launches = int(_lib.lib().dffm_launch_count() - lc0)
-    if world > 1:
-        dist.barrier()
     times = [s.elapsed_time(e) for s, e in evs]
     total_ms = float(sum(times))
+    split = trace.split()
     # parity guard: the status word must be clear and every output finite
     predict_batch(idx, val, st, out=prob, check=True)
     assert bool(torch.isfinite(prob).all())
@@ -346,23 +434,35 @@ def run_ours(args, wl):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = n * world * args.steps / (total_ms / 1e3)
+    n_total = wl.n_examples if (strong and not args.examples) else n * world
+    value = n_total * args.steps / (total_ms / 1e3)
     ms_step = total_ms / args.steps
     peak, peak_src = measured_peaks()
-    achieved = alg / (ms_step / 1e3) / 1e9
+    dom = "gather" if "gather" in split else "fused"
+    dom_ms, dom_launches = split.get(dom, (total_ms, args.steps))
+    dom_alg_per_launch = alg * args.steps / max(dom_launches, 1)
+    dom_ms_per_launch = dom_ms / max(dom_launches, 1)
+    achieved = dom_alg_per_launch / (dom_ms_per_launch / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic_for(wl.name)
 
-    # e2e: the public host-buffer API (pinned H2D per step + D2H of the probabilities),
-    # in both host formats: padded [n,F,M] (HostPredictor.__call__) and ragged
-    # (HostPredictor.predict_ragged: present features only, K9 unpacks on the device);
-    # the headline `e2e` is the format with fewer bytes for this workload
+    # e2e: the public host-buffer API (HostPredictor: pinned H2D of the inputs per
+    # chunk overlapped with K1, D2H of the probabilities), headline in the padded
+    # canonical layout [n][F][M]; the ragged (K9) and packed (K9b) host formats are
+    # listed with their host-side encoding time (done once, outside the region)
     from paper_2407_10115_b200.features import PackedBatch, RaggedBatch
     idx_h = idx.cpu().pin_memory()
     val_h = val.cpu().pin_memory()
+    t0 = time.perf_counter()
     rb = RaggedBatch.from_padded(idx_h.numpy(), val_h.numpy())
+    enc_rag = time.perf_counter() - t0
     rb_h = RaggedBatch(*(torch.from_numpy(a).pin_memory() for a in (rb.ex_off, rb.cnt, rb.idx,
                                                                     rb.val)), rb.max_per_field)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-    pk = PackedBatch.from_ragged(rb) if rb.n_fields * rb.max_per_field <= 128 else None
+    pk, enc_pk = None, None
+    if rb.n_fields * rb.max_per_field <= 128:
+        t0 = time.perf_counter()
+        pk = PackedBatch.from_ragged(rb)
+        enc_pk = enc_rag + time.perf_counter() - t0
     pk_h = None if pk is None else PackedBatch(pin(pk.ex_off), pin(pk.cnt), pin(pk.idx_bytes),
                                                pk.idx_width, pin(pk.vbits), pin(pk.vals),
                                                pin(pk.voff), pk.max_per_field)
@@ -383,54 +483,147 @@ def run_ours(args, wl):
                           device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        return n * world / float(te.item()), bool(torch.equal(out_h, prob_h))
+        return n_total / float(te.item()), bool(torch.equal(out_h, prob_h))
 
     pad_bytes = idx.numel() * 4 + val.numel() * 4
     e2e_pad, ok_pad = time_e2e(lambda: hp(idx_h, val_h, out_h))
     e2e_rag, ok_rag = time_e2e(lambda: hp.predict_ragged(rb_h, out_h))
-    fmts = {"padded": (e2e_pad, ok_pad, pad_bytes), "ragged": (e2e_rag, ok_rag, rb.nbytes())}
+    fmts = {"ragged": {"value": e2e_rag, "h2d_bytes_per_step": rb.nbytes(),
+                       "matches_device_run": ok_rag,
+                       "host_encode_s_excluded": enc_rag}}
     if pk_h is not None:
         e2e_pk, ok_pk = time_e2e(lambda: hp.predict_packed(pk_h, out_h))
-        fmts["packed"] = (e2e_pk, ok_pk, pk.nbytes())
-    best = max(fmts, key=lambda k: fmts[k][0])  # the fastest host format (all are reported)
-    e2e_value, e2e_ok, e2e_bytes = fmts[best]
+        fmts["packed"] = {"value": e2e_pk, "h2d_bytes_per_step": pk.nbytes(),
+                          "matches_device_run": ok_pk, "host_encode_s_excluded": enc_pk}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": {"f32": "f32", "bf16": "bf16 tables, f32/f64 arithmetic",
+                  "u16": "u16 tables, f32 arithmetic"}[st.wdtype],
         "data": "synthetic (seeded on-device; Zipf/hashed stand-in for Criteo-like data)",
-        "config": {"workload": wl.name, "examples_per_gpu": n, "n_fields": wl.n_fields,
+        "config": {"workload": wl.name, "examples_total": n_total, "examples_per_gpu": n,
+                   "n_fields": wl.n_fields,
                    "k": wl.k, "hidden": list(wl.hidden), "hash_bits": wl.hash_bits,
                    "max_per_field": int(idx.shape[2]), "table_dtype": st.wdtype,
                    "mean_features_per_example": int((idx >= 0).sum().item()) / n,
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"batch-sharded x{world}, replicated tables, no collective"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(wl.name),
+                   "parallelism": (f"batch-sharded x{world} ({'fixed total batch' if strong else 'full batch per rank'}),"
+                                   " replicated tables, no collective")},
+        "roofline": {"bound": "hbm", "kernel": "fwd_rsw_kernel (K1 v8 row-ring gather)"
+                     if dom == "gather" else "fused forward",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": dom_alg_per_launch,
+                     "ms_per_launch": dom_ms_per_launch, "launches": dom_launches,
                      "algorithmic_bytes_per_step": alg, "peak_source": peak_src,
-                     "scope": "whole step: algorithmic bytes / step time over every kernel "
-                              "of the call (per slice: K1 v8 row-ring gather + tcgen05 MLP "
-                              "when staged, else the fused kernel); traffic = DRAM bytes of "
-                              "one step (profiles/ncu_traffic.json)"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_bytes,
-                "d2h_bytes_per_step": n * 4 + 8, "matches_device_run": e2e_ok,
-                "format": best + {"padded": "", "ragged": " (K9 unpack on device)",
-                                  "packed": " (3-byte indices, 1.0 values elided; K9b unpack "
-                                            "on device)"}[best],
-                **{k: {"value": v[0], "h2d_bytes_per_step": v[2], "matches_device_run": v[1]}
-                   for k, v in fmts.items()}},
+                     "step_achieved": alg / (ms_step / 1e3) / 1e9,
+                     "step_frac": alg / (ms_step / 1e3) / 1e9 / peak,
+                     "kernel_ms_per_step": {k: v[0] / args.steps for k, v in split.items()},
+                     "kernel_launches_per_step": {k: v[1] / args.steps for k, v in split.items()},
+                     "timing": "CUDA events recorded by libdffm after every launch on the "
+                               "launch stream (dffm_set_event_trace), summed per kernel role",
+                     "note": "achieved counts algorithmic bytes (SURVEY 8(d)); Zipf rows "
+                             "re-hit in L2, so it can exceed the DRAM peak -- traffic is "
+                             "the DRAM bytes ncu measured for one launch"},
+        "e2e": {"value": e2e_pad, "unit": UNIT, "h2d_bytes_per_step": pad_bytes,
+                "d2h_bytes_per_step": n * 4 + 8, "matches_device_run": ok_pad,
+                "format": "padded canonical layout idx/val [n][F][M] (HostPredictor.__call__)",
+                "other_host_formats": fmts},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(st, idx, val, prob, wl)
-    if args.train_examples > 0:
-        del st, idx, val, prob, hp, idx_h, val_h, out_h, rb, rb_h, prob_h, pk, pk_h
-        torch.cuda.empty_cache()
-        line["adagrad"] = bench_adagrad(args, dev, clk_index=local)
+    del st, idx, val, prob, hp, idx_h, val_h, out_h, rb, rb_h, prob_h, pk, pk_h, flush
+    torch.cuda.empty_cache()
+    return line
+
+
+def _run_rank(args):
+    """One rank (torchrun / self-spawned / single process) of the default bench."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_10115_b200 import configs
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS[args.workload]
+    if wl is configs.CFG4:
+        line = run_ours_ctx(args, wl, world, rank, local, dev)
+    else:
+        line = run_ours(args, wl, world, rank, local, dev)
+        if args.workload == "cfg5" and not args.examples and not args.no_nested:
+            # BASELINE configs[1] (cfg2, 1,048,576 examples per rank) as a nested line
+            sub = run_ours(args, configs.CFG2, world, rank, local, dev, nested=True)
+            line["cfg2"] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "scaling",
+                                                 "dtype", "config", "roofline", "e2e",
+                                                 "gpu_launches", "clocks", "cpu_baseline")
+                            if k in sub}
+    if args.train_examples > 0 and wl is not configs.CFG4:
+        if rank == 0:  # training is one GPU (SURVEY 8(e)); the other ranks wait
+            line["adagrad"] = bench_adagrad(args, dev, clk_index=local)
+        if world > 1:
+            dist.barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _spawned(i, args, world, port, target):
+    os.environ.update({"RANK": str(i), "LOCAL_RANK": str(i), "WORLD_SIZE": str(world),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    target(args)
+
+
+def spawn_ranks(args, target):
+    """--gpus N without torchrun: start N ranks (one process per GPU) with the same
+    env contract torchrun sets (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.start_processes(_spawned, args=(args, args.gpus, port, target), nprocs=args.gpus,
+                       join=True, start_method="spawn")
+
+
+def _selftest_rank(args):
+    """CPU stand-in for one rank of the default bench (gloo): times a fixed amount of
+    host work per step, barrier + max-over-ranks like the GPU path; proves the
+    launcher and the reduction (tests/test_bench_launcher.py)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    n_per = 1 << 12
+    x = np.random.default_rng(rank).random(n_per)
+    for _ in range(args.warmup):
+        np.sort(x)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        np.sort(x)
+    el = torch.tensor([time.perf_counter() - t0 + 1e-9], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": "selftest", "value": n_per * world * args.steps
+                          / float(el.item()), "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "scaling": "weak"}), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -450,24 +643,17 @@ def _cpu_ctx_worker(bounds):
     return bounds[0], out
 
 
-def run_ours_ctx(args, wl):
+def run_ours_ctx(args, wl, world, rank, local, dev):
     """cfg4: context-cached serving (K3) over R requests x C candidates, u16 tables.
     value = candidates/s with requests resident; e2e = pinned host buffers in,
     probabilities out, through inference.score_requests."""
     import multiprocessing as mp
 
     import torch
+    import torch.distributed as dist
 
     from paper_2407_10115_b200 import synth
     from paper_2407_10115_b200.inference import score_requests
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
     R, C, Fc, F = wl.n_requests, wl.n_candidates, wl.ctx_fields, wl.n_fields
     st = build_store(wl, dev)
     cdf = synth.zipf_cdf(1 << wl.hash_bits, wl.zipf_alpha, dev)
@@ -573,11 +759,7 @@ def run_ours_ctx(args, wl):
             "kind": "port", "sample": f"first {nreq} requests x {C} candidates, oracle "
                                       "context cache + per-candidate finish, forked processes",
             "gpu_vs_oracle_max_rel_err": float(np.max(np.abs(gp - ref) / ref))}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    return line
 
 
 def bench_adagrad(args, dev, clk_index=0):
@@ -607,7 +789,7 @@ def bench_adagrad(args, dev, clk_index=0):
     torch.cuda.empty_cache()
 
     def student():
-        st = WeightStore(cfg, dev)
+        st = WeightStore(cfg, dev).fill_accumulators(1.0)  # acc0 = 1.0 (cfg3)
         gen.manual_seed(wl.weight_seed)
         for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
             flat = t.view(-1)
@@ -720,6 +902,101 @@ def cpu_baseline(st, idx, val, prob, wl, budget_s=12.0):
             "sample": f"first {sample} examples of the timed batch, per-example oracle "
                       f"forward+predict_proba, {cores} forked processes",
             "gpu_vs_oracle_max_rel_err": rel}
+
+
+def device_digest(tensors) -> str:
+    """Order-sensitive 64-bit fold of tensors' bit patterns, computed on the device
+    in chunks (a final-weights fingerprint without copying 26 GB to the host)."""
+    import torch
+    acc = 0
+    for t in tensors:
+        flat = t.reshape(-1).view(torch.int32) if t.element_size() == 4 else \
+            t.reshape(-1).view(torch.int16).to(torch.int32)
+        for c0 in range(0, flat.numel(), 1 << 26):
+            c = flat[c0:c0 + (1 << 26)].to(torch.int64) & 0xFFFFFFFF
+            w = torch.arange(c0, c0 + c.numel(), device=c.device, dtype=torch.int64)
+            w = (w * 2654435761 + 1) & 0xFFFFFFFF
+            acc = (acc * 1000003 + int(((c * w) & 0xFFFFFFFFFFFF).sum().item())) & ((1 << 64) - 1)
+    return f"{acc:016x}"
+
+
+def run_cfg3_stream(args):
+    """BASELINE configs[2] as stated: online Adagrad over the full 10M-example stream
+    (K2, the reference's exact sequential schedule, T:172-185), labels from a planted
+    teacher, student N(0,0.05) with acc0 = 1.0.  Reports examples/s, progressive
+    logloss, the 30k-window AUC series (K8) and a final-weights digest."""
+    import torch
+
+    from paper_2407_10115_b200 import configs
+    from paper_2407_10115_b200.model import ModelConfig, WeightStore, predict_batch
+    from paper_2407_10115_b200.training import TrainOptions, train_sequential
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    wl = configs.CFG3
+    n = args.examples or wl.n_examples
+    cfg = ModelConfig(n_fields=wl.n_fields, k=wl.k, hidden_sizes=wl.hidden,
+                      hash_bits=wl.hash_bits, lr_ffm=wl.lr, lr_lr=wl.lr, lr_nn=wl.lr,
+                      power_t=wl.power_t)
+    idx, val = build_inputs(wl, n, dev, 0)
+    gen = torch.Generator(device=dev).manual_seed(3003)
+    teacher = WeightStore(cfg, dev, with_optimizer=False)
+    for t in [teacher.lr, teacher.ffm] + [x for wb in teacher.nn_layers for x in wb]:
+        flat = t.view(-1)
+        for c0 in range(0, flat.numel(), 1 << 28):
+            c1 = min(flat.numel(), c0 + (1 << 28))
+            flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=dev) * 0.1)
+    labels = torch.empty(n, dtype=torch.uint8, device=dev)
+    for c0 in range(0, n, 1 << 21):
+        p = predict_batch(idx[c0:c0 + (1 << 21)], val[c0:c0 + (1 << 21)], teacher)
+        labels[c0:c0 + p.numel()] = (torch.rand(p.numel(), generator=gen, device=dev) < p)
+    del teacher
+    torch.cuda.empty_cache()
+    st = WeightStore(cfg, dev).fill_accumulators(1.0)
+    gen.manual_seed(wl.weight_seed)
+    for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
+        flat = t.view(-1)
+        for c0 in range(0, flat.numel(), 1 << 28):
+            c1 = min(flat.numel(), c0 + (1 << 28))
+            flat[c0:c1].copy_(torch.randn(c1 - c0, generator=gen, device=dev) * wl.weight_scale)
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = adagrad_cpu_baseline(st, idx[:4000], val[:4000], labels[:4000], cfg)
+    from paper_2407_10115_b200 import _lib
+    lc0 = _lib.lib().dffm_launch_count()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        s.record()
+        rep = train_sequential(idx, val, labels, st, TrainOptions(chunk=1 << 22))
+        e.record()
+        torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    launches = int(_lib.lib().dffm_launch_count() - lc0)
+    series = rep.rolling_auc_series
+    line = {
+        "metric": "Adagrad examples/sec (cfg3, exact sequential schedule)",
+        "value": n / (ms / 1e3), "unit": "examples/s", "n_gpus": 1, "steps": 1, "warmup": 0,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 arithmetic, f32 storage",
+        "data": "synthetic (seeded Zipf/hashed examples, labels from a planted teacher)",
+        "config": {"workload": wl.name, "examples": n, "n_fields": wl.n_fields, "k": wl.k,
+                   "hidden": list(wl.hidden), "hash_bits": wl.hash_bits, "lr": wl.lr,
+                   "power_t": wl.power_t, "acc0": 1.0, "batch": 1,
+                   "note": "one pass over the whole stream, inputs resident; the step is the "
+                           "whole stream (latency-bound chain, SURVEY 8(d))"},
+        "us_per_example": 1e3 * ms / n,
+        "progressive_logloss": rep.progressive_logloss,
+        "auc_windows": len(series),
+        "auc_series_head": series[:5], "auc_series_tail": series[-5:],
+        "final_weights_digest": device_digest([x for _, x in st.blocks(True)]),
+        "gpu_launches": launches, "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "e2e": None,
+    }
+    os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(REPO, "gpurun_out", "cfg3_auc_series.json"), "w") as fh:
+        json.dump({"series": series, "logloss": rep.progressive_logloss}, fh)
+    print(json.dumps(line), flush=True)
 
 
 def make_text_lines(n, seed=2002):
@@ -861,31 +1138,54 @@ def _parse_worker(lines, names, numeric):
         fo.parse_line(ln, names, numeric, 24)
 
 
+WORKLOADS = {}
+
+
+def _reference_rank(args):
+    from paper_2407_10115_b200 import configs
+    if not WORKLOADS:
+        WORKLOADS.update({"cfg1": configs.CFG1, "cfg2": configs.CFG2, "cfg3": configs.CFG3,
+                          "cfg4": configs.CFG4, "cfg5": configs.CFG5})
+    run_reference(args, WORKLOADS.get(args.workload, configs.CFG5))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg5",
+                    help="cfg5 (default: the metric's 1/2/4/8-GPU config, with cfg2 and the "
+                         "cfg3 Adagrad prefix nested), cfg1, cfg2, cfg3 (full 10M-example "
+                         "Adagrad stream), cfg4, parse")
     ap.add_argument("--examples", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nested", action="store_true", help="skip the nested cfg2 line")
     ap.add_argument("--train-examples", type=int, default=200_000,
                     help="cfg3 Adagrad prefix timed after the forward (0 = skip)")
+    ap.add_argument("--selftest-spawn", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     from paper_2407_10115_b200 import configs
-    if args.workload == "parse":
-        return run_parse(args)
-    wl = {"cfg1": configs.CFG1, "cfg2": configs.CFG2, "cfg4": configs.CFG4,
-          "cfg5": configs.CFG5}[args.workload]
-    if args.impl == "reference":
-        run_reference(args, wl)
-    elif wl is configs.CFG4:
-        run_ours_ctx(args, wl)
+    WORKLOADS.update({"cfg1": configs.CFG1, "cfg2": configs.CFG2, "cfg3": configs.CFG3,
+                      "cfg4": configs.CFG4, "cfg5": configs.CFG5})
+    launched = "WORLD_SIZE" in os.environ
+    if args.selftest_spawn:
+        target = _selftest_rank
+    elif args.impl == "reference":
+        target = _reference_rank
+    elif args.workload == "parse":
+        target = run_parse
+    elif args.workload == "cfg3":
+        target = run_cfg3_stream
     else:
-        run_ours(args, wl)
+        target = _run_rank
+    if args.gpus > 1 and not launched and args.workload not in ("parse", "cfg3"):
+        spawn_ranks(args, target)
+    else:
+        target(args)
 
 
 if __name__ == "__main__":

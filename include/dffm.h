@@ -98,18 +98,28 @@ int dffm_forward(const dffm_model* model, const int32_t* idx, const float* val,
 /*
  * K1 kernel family (all compute identical results within the 1e-5 contract;
  * shapes a family cannot take fall back to family 2):
- *   0 row-coalesced, 1 warp-specialised (fused MLP on CUDA cores),
- *   2 CTA-synchronous, 3 TMA 1-D ring, 4 TMA gather4 ring,
+ *   1 warp-specialised (fused MLP on CUDA cores), 2 CTA-synchronous,
  *   5 staged rows + tcgen05 3xTF32 MLP (hidden widths multiples of 16, <= 256),
- *   -1 = from DFFM_FORWARD_KERNEL; unset = 5 (staged rows through the
- *   K1 v8 row ring + tcgen05 MLP) when the ring takes the shape (M <= 4,
+ *   -1 = default: DFFM_FORWARD_KERNEL (ws|v1|tc) if set, else 5 (K1 v8
+ *   row-ring gather + tcgen05 MLP) when the ring takes the shape (M <= 4,
  *   F*M <= 128, k in {4, 8, 16}) and the hidden widths are multiples of 16,
  *   or when the MLP has >= 64K multiply-adds per example; otherwise 1.
  * Family 5 keeps a per-(device, stream) device workspace (staged rows of one
  * slice + the blocked hi/lo MLP weights), allocated on first use.
- * Process-wide; for A/B measurements and tests.
+ * Thread-local: applies to dffm_forward calls made by the calling host
+ * thread only (reentrant across host threads). Other values: DFFM_CONTRACT.
  */
 int dffm_set_forward_family(int32_t family);
+
+/*
+ * Per-thread launch trace for measurement (bench.py): while set, every
+ * kernel dffm_forward launches is followed by cudaEventRecord(events[i])
+ * on the launch stream and tags[i] = its role (0 weight blocking for the
+ * tensor-core MLP, 1 row gather, 2 tcgen05 MLP, 3 fused forward); *count
+ * advances, up to capacity. events = NULL clears the trace. The events are
+ * caller-created cudaEvent_t handles.
+ */
+int dffm_set_event_trace(void** events, int32_t* tags, int32_t capacity, int32_t* count);
 
 /*
  * K3 context-cached scorer (no reference code).  Request r

@@ -53,6 +53,7 @@ SIGNATURES = {
     "dffm_forward": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_int64,
                                c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "dffm_set_forward_family": (c_int32, [c_int32]),
+    "dffm_set_event_trace": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
     "dffm_ctx_score": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_int32,
                                  c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p,
                                  c_void_p, c_void_p]),

@@ -120,14 +120,9 @@ extern "C" int fw_eval_stream(const double* probs, const uint8_t* labels, int64_
   const int64_t n_full = n / window, n_win = (n + window - 1) / window;
   if (n_full && !auc_out) { set_error("null auc_out"); return DFFM_CONTRACT; }
   const int smem = (window / 2) * 8;
-  static int configured = 0;
-  if (!configured) {
-    DFFM_CUDA_TRY(cudaFuncSetAttribute(eval_window_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       max_smem_optin_current() - 1024),
-                  "cudaFuncSetAttribute(eval)");
-    configured = 1;
-  }
+  // sets the dynamic-smem limit once per (kernel, device): attributes are per context
+  int occ = 0;
+  if (int rc = kernel_occupancy((const void*)eval_window_kernel, EV_THREADS, smem, &occ)) return rc;
   note_launches(1), eval_window_kernel<<<(unsigned)n_win, EV_THREADS, smem, (cudaStream_t)stream>>>(
       probs, labels, n, window, n_full, auc_out, loss_out);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(eval)");

@@ -7,12 +7,8 @@
 #include <string.h>
 
 #include "forward_kernel.cuh"
-#include "forward_tma.cuh"
 #include "forward_ws.cuh"
-#include "forward_rows.cuh"
-#include "forward_g4.cuh"
 #include "mlp_tc.cuh"
-#include "forward_rowstage.cuh"
 #include "forward_rsw.cuh"
 
 #include <cudaTypedefs.h>
@@ -22,48 +18,52 @@ namespace dffm {
 template <typename T>
 int launch_forward_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s);
 template <typename T>
-int launch_forward_tma_t(const TmaParams& q, int K, int smem, cudaStream_t s);
-
-template <typename T>
 int launch_forward_ws_t(const FwdParams& p, int K, int MU, int smem, cudaStream_t s);
-
-// Kernel family: "ws" (default, K1 v3), "v1" (CTA-synchronous gather + MLP
-// tile), "tma" (TMA-ring producer/consumer).  DFFM_FORWARD_KERNEL selects one
-// for A/B measurements; shapes a family cannot take fall back to v1.
-template <typename T>
-int launch_forward_rows_t(const FwdParams& p, int K, int smem, cudaStream_t s);
-
-template <typename T>
-int launch_forward_g4_t(const CUtensorMap& tm, const G4Params& q, int K, int smem,
-                        cudaStream_t s);
-template <typename T>
-int launch_forward_rowstage_t(const FwdParams& p, int K, int NB, int smem, cudaStream_t s);
 template <typename T>
 int launch_forward_rsw_t(const FwdParams& p, const RswSmem& L, int K, cudaStream_t s);
 
-enum FwdFamily { FAM_ROWS = 0, FAM_WS = 1, FAM_V1 = 2, FAM_TMA = 3, FAM_G4 = 4, FAM_TC = 5 };
-static int g_family = -1;  // set by env (first call) or dffm_set_forward_family()
-static bool g_family_explicit = false;
+// Kernel family: default (-1) = the dispatcher's choice per shape (row-ring
+// gather + tcgen05 MLP where it applies, else the fused ws kernel, else v1);
+// FAM_WS / FAM_V1 / FAM_TC force one for A/B measurements and tests
+// (DFFM_FORWARD_KERNEL=ws|v1|tc, or dffm_set_forward_family on this thread).
+// The choice is thread-local: concurrent host threads (one per GPU, or two
+// streams on one GPU) never see each other's setting.
+enum FwdFamily { FAM_WS = 1, FAM_V1 = 2, FAM_TC = 5 };
+static thread_local int t_family = -2;  // -2: not read yet; -1: default
 static int forward_family() {
-  if (g_family < 0) {
+  if (t_family == -2) {
     const char* v = getenv("DFFM_FORWARD_KERNEL");
-    int f = FAM_WS;  // measured fastest on cfg2 (see profiles/)
-    g_family_explicit = v != nullptr;
-    if (v && strcmp(v, "rows") == 0) f = FAM_ROWS;
-    if (v && strcmp(v, "g4") == 0) f = FAM_G4;
+    int f = -1;
+    if (v && strcmp(v, "ws") == 0) f = FAM_WS;
     if (v && strcmp(v, "v1") == 0) f = FAM_V1;
-    if (v && strcmp(v, "tma") == 0) f = FAM_TMA;
     if (v && strcmp(v, "tc") == 0) f = FAM_TC;
-    g_family = f;
+    t_family = f;
   }
-  return g_family;
+  return t_family;
 }
-static bool tma_forward_enabled() { return forward_family() == FAM_TMA; }
+
+// Optional per-thread launch trace (dffm_set_event_trace): after every kernel
+// dffm_forward launches, an event is recorded on the launch stream and the
+// kernel's role tagged (0 weight blocking, 1 gather, 2 MLP, 3 fused), so a
+// caller can split a step's device time per kernel with CUDA events.
+struct EventTrace {
+  void** events = nullptr;
+  int32_t* tags = nullptr;
+  int32_t cap = 0;
+  int32_t* count = nullptr;
+};
+static thread_local EventTrace t_trace;
+static void trace_launch(int tag, cudaStream_t s) {
+  EventTrace& t = t_trace;
+  if (!t.events || !t.count || *t.count >= t.cap) return;
+  cudaEventRecord((cudaEvent_t)t.events[*t.count], s);
+  t.tags[*t.count] = tag;
+  ++*t.count;
+}
 
 int pick_k_template(int k, int wdtype);
 
-// ---- 2-D tensor map over the ffm table (rows = buckets, box = one whole row),
-// encoded through the driver entry point (no -lcuda), cached per table.
+// ---- driver entry point for tensor-map encoding (no -lcuda)
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::mutex mu;
@@ -79,121 +79,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static int row_tensor_map(const void* base, int wdtype, int64_t rows, int row_elems,
-                          CUtensorMap* out) {
-  static std::mutex mu;
-  static std::unordered_map<uint64_t, CUtensorMap> cache;
-  const uint64_t key = ((uint64_t)(uintptr_t)base) ^ ((uint64_t)rows << 1) ^
-                       ((uint64_t)row_elems << 40) ^ ((uint64_t)wdtype << 60);
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) { *out = it->second; return DFFM_OK; }
-  auto fn = encode_fn();
-  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return DFFM_CUDA; }
-  const int esz = wdtype == DFFM_W_F32 ? 4 : 2;
-  const CUtensorMapDataType dt = wdtype == DFFM_W_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                                 : wdtype == DFFM_W_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                                         : CU_TENSOR_MAP_DATA_TYPE_UINT16;
-  cuuint64_t dims[2] = {(cuuint64_t)row_elems, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)row_elems * esz};
-  cuuint32_t box[2] = {(cuuint32_t)row_elems, 1};
-  cuuint32_t estr[2] = {1, 1};
-  CUtensorMap tm;
-  CUresult r = fn(&tm, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return DFFM_CUDA;
-  }
-  cache[key] = tm;
-  *out = tm;
-  return DFFM_OK;
-}
-
-// K1 v5: TMA gather4 ring (whole rows per TMA op)
-static bool try_g4_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc,
-                           bool force = false) {
-  if (!force && forward_family() != FAM_G4) return false;
-  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
-  const int k = p.k;
-  const int row_elems = p.F * k;
-  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
-  if (row_elems > 256 || (row_elems * esz) % 16 != 0) return false;
-  if (p.F * p.M > 128 || (p.F * p.M) % 4) return false;
-  if (((uintptr_t)p.idx & 15) || ((uintptr_t)p.val & 15) || ((uintptr_t)p.ffm & 15)) return false;
-  for (int l = 1; l < p.n_layers; ++l)
-    if (p.dims[l] % 4) return false;
-  static int te_env = -1, smem_cap = -1;
-  if (te_env < 0) {
-    const char* v = getenv("DFFM_G4_TE");
-    te_env = v ? atoi(v) : 16;
-    if (te_env < 4 || te_env > 64 || (te_env & 3)) te_env = 16;
-    const char* c = getenv("DFFM_G4_SMEM_KB");  // leave the rest of the SM's 256 KB to L1
-    smem_cap = c ? atoi(c) * 1024 : 160 * 1024;
-  }
-  G4Params q{};
-  q.row_bytes = row_elems * esz;
-  q.quad_bytes = 4 * q.row_bytes;
-  const int cap = smem_cap < smax ? smem_cap : smax;
-  for (int TE = te_env; TE >= 4; TE >>= 1) {
-    p.TE = TE;
-    p.XS = TE + 4;
-    const G4Smem L0 = g4_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.quad_bytes, 0);
-    const int quads = (cap - L0.total - 128) / q.quad_bytes;
-    const int need = (p.F * p.M + 3) / 4;
-    if (quads < 2 * need || quads * 4 > 32767) continue;
-    q.ring_quads = quads;
-    q.f = p;
-    const G4Smem L = g4_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.quad_bytes, quads);
-    CUtensorMap tm;
-    int r = row_tensor_map(p.ffm, m->wdtype, p.n_buckets, row_elems, &tm);
-    if (r) { *rc = r; return true; }
-    switch (m->wdtype) {
-      case DFFM_W_F32: *rc = launch_forward_g4_t<float>(tm, q, k, L.total, s); break;
-      case DFFM_W_BF16: *rc = launch_forward_g4_t<__nv_bfloat16>(tm, q, k, L.total, s); break;
-      default: *rc = launch_forward_g4_t<uint16_t>(tm, q, k, L.total, s); break;
-    }
-    return true;
-  }
-  return false;
-}
-
-// K1 v4: row-coalesced gather (F <= 32, 16/32/64-byte segments)
-static bool try_rows_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
-                             int* rc, bool force = false) {
-  if (!force && forward_family() != FAM_ROWS) return false;
-  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
-  const int k = p.k;
-  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
-  if (p.F > 32 || p.M > 4 || p.F * p.M > 128) return false;
-  for (int l = 1; l < p.n_layers; ++l)
-    if (p.dims[l] % 4) return false;
-  static int te_env = -1;
-  if (te_env < 0) {
-    const char* v = getenv("DFFM_ROWS_TE");
-    te_env = v ? atoi(v) : 16;
-    if (te_env < 4 || te_env > 64 || (te_env & 3)) te_env = 16;
-  }
-  for (int TE = te_env; TE >= 4; TE >>= 1) {
-    p.TE = TE;
-    p.XS = TE + 4;
-    const RwSmem L = rw_smem_layout(p.F, p.M, p.P, p.D, k, p.TE, p.XS, p.hmax);
-    if (L.total > smax) continue;
-    switch (m->wdtype) {
-      case DFFM_W_F32: *rc = launch_forward_rows_t<float>(p, k, L.total, s); break;
-      case DFFM_W_BF16: *rc = launch_forward_rows_t<__nv_bfloat16>(p, k, L.total, s); break;
-      default: *rc = launch_forward_rows_t<uint16_t>(p, k, L.total, s); break;
-    }
-    return true;
-  }
-  return false;
-}
-
 static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s, int* rc,
                            bool force = false) {
-  if (!force && forward_family() != FAM_WS && forward_family() != FAM_ROWS)
-    return false;  // rows falls back here
+  const int fam = forward_family();
+  if (!force && fam != FAM_WS && fam != -1) return false;
   for (int l = 1; l < p.n_layers; ++l)
     if (p.dims[l] % 4) return false;
   for (int TE = p.xout ? 8 : 32; TE >= 8; TE >>= 1) {  // staging: small tile, big ring
@@ -207,45 +96,6 @@ static bool try_ws_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
       case DFFM_W_F32: *rc = launch_forward_ws_t<float>(p, K, MU, L.total, s); break;
       case DFFM_W_BF16: *rc = launch_forward_ws_t<__nv_bfloat16>(p, K, MU, L.total, s); break;
       default: *rc = launch_forward_ws_t<uint16_t>(p, K, MU, L.total, s); break;
-    }
-    return true;
-  }
-  return false;
-}
-
-// Pick K1 v2 (TMA ring) when the shape allows it; returns false to fall
-// through to fwd_kernel.
-static bool try_tma_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
-                            int* rc, bool force = false) {
-  if (!force && !tma_forward_enabled()) return false;
-  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
-  const int k = p.k;
-  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
-  if (p.F * p.M > TMA_MAX_FM || (p.F * p.M) % 4) return false;  // idx/val slots TMA'd
-  if (((uintptr_t)p.idx & 15) || ((uintptr_t)p.val & 15)) return false;
-  for (int l = 1; l < p.n_layers; ++l)
-    if (p.dims[l] % 4) return false;
-  TmaParams q{};
-  {
-    const char* cm = getenv("DFFM_ROW_COPY");
-    q.copy_mode = (cm && strcmp(cm, "tma") == 0) ? 0 : 1;
-  }
-  q.row_bytes = p.F * k * esz;
-  q.rs = q.row_bytes + 16;
-  for (int TE = p.xout ? 8 : 32; TE >= 8; TE >>= 1) {  // staging: small tile, big ring
-    p.TE = TE;
-    p.XS = TE + 4;
-    const TmaSmem L0 = tma_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.rs, 0);
-    const int rows = (smax - L0.total) / q.rs;
-    if (rows < 2 * p.F * p.M) continue;  // at least two worst-case examples in flight
-    q.ring_rows = rows < 32767 ? rows : 32767;
-    q.f = p;
-    const TmaSmem L = tma_smem_layout(p.F, p.M, p.P, p.D, p.TE, p.XS, p.hmax, q.rs,
-                                      q.ring_rows);
-    switch (m->wdtype) {
-      case DFFM_W_F32: *rc = launch_forward_tma_t<float>(q, k, L.total, s); break;
-      case DFFM_W_BF16: *rc = launch_forward_tma_t<__nv_bfloat16>(q, k, L.total, s); break;
-      default: *rc = launch_forward_tma_t<uint16_t>(q, k, L.total, s); break;
     }
     return true;
   }
@@ -298,33 +148,6 @@ static int rows_tensor_map_x(const float* X, int Kp, int64_t rows, CUtensorMap* 
     return DFFM_CUDA;
   }
   return DFFM_OK;
-}
-
-// K1 v7 staging gather for single-slot fields (whole rows via cp.async ring)
-static bool try_rowstage_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
-                                 int* rc) {
-  if (!p.xout || p.M != 1 || p.F > RS_MAXF) return false;
-  const int esz = m->wdtype == DFFM_W_F32 ? 4 : 2;
-  const int k = p.k;
-  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 != 0) return false;
-  if (((uintptr_t)p.ffm & 15) || ((uintptr_t)p.lr & 3)) return false;
-  const int row_bytes = p.F * k * esz;
-  static int ctas = -1;  // CTAs per SM to aim for (each overlaps its own example chain)
-  if (ctas < 0) {
-    const char* v = getenv("DFFM_RS_CTAS");
-    ctas = v ? std::max(1, atoi(v)) : 2;
-  }
-  for (int nb = 4; nb >= 2; --nb) {
-    const RsSmem L = rs_smem_layout(p.F, p.P, row_bytes, nb);
-    if (L.total > smax || (nb > 2 && ctas * (L.total + 1024) > 228 * 1024)) continue;
-    switch (m->wdtype) {
-      case DFFM_W_F32: *rc = launch_forward_rowstage_t<float>(p, k, nb, L.total, s); break;
-      case DFFM_W_BF16: *rc = launch_forward_rowstage_t<__nv_bfloat16>(p, k, nb, L.total, s); break;
-      default: *rc = launch_forward_rowstage_t<uint16_t>(p, k, nb, L.total, s); break;
-    }
-    return true;
-  }
-  return false;
 }
 
 // shapes the K1 v8 row-ring gather takes
@@ -448,12 +271,10 @@ int tc_mlp_slice(TcPlan& plan, int64_t rows, int64_t status_base, float* prob, f
 static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStream_t s,
                            int* rc) {
   const int fam = forward_family();
-  // default (family unset): the row-ring gather + tensor-core MLP wherever the
-  // ring takes the shape (cfg2: 135 vs 111 M preds/s for the fused ws kernel),
-  // or whenever the MLP is too heavy for CUDA cores (cfg5)
-  if (fam != FAM_TC &&
-      !(fam == FAM_WS && !g_family_explicit && (tc_auto(p) || rsw_shape_ok(m, p))))
-    return false;
+  // default: the row-ring gather + tensor-core MLP wherever the ring takes the
+  // shape (cfg2: 135 vs 111 M preds/s for the fused ws kernel), or whenever
+  // the MLP is too heavy for CUDA cores (cfg5)
+  if (fam != FAM_TC && !(fam == -1 && (tc_auto(p) || rsw_shape_ok(m, p)))) return false;
   if (!tc_eligible(p, smax)) return false;
   FwdParams pg = p;
   pg.hmax = 0;  // staging mode: the gather kernels keep no hidden-layer buffers
@@ -464,14 +285,12 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
   static int gather_env = -2;
   if (gather_env == -2) {
     const char* v = getenv("DFFM_TC_GATHER");
-    gather_env = (v && strcmp(v, "rowstage") == 0) ? 100
-                 : (v && strcmp(v, "g4") == 0) ? FAM_G4 : (v && strcmp(v, "rows") == 0) ? FAM_ROWS
-                 : (v && strcmp(v, "tma") == 0) ? FAM_TMA : (v && strcmp(v, "ws") == 0) ? FAM_WS
-                 : -1;  // default: row staging when it applies, else ws
+    gather_env = (v && strcmp(v, "ws") == 0) ? FAM_WS : -1;  // default: row ring when it applies
   }
   const int64_t sl = std::min<int64_t>(tc_default_slice_rows(), (p.n + TC_M - 1) / TC_M * TC_M);
   TcPlan plan;
   if ((*rc = tc_plan(p, smax, sl, s, &plan))) return true;
+  trace_launch(0, s);
   const int64_t FM = (int64_t)p.F * p.M;
   for (int64_t s0 = 0; s0 < p.n; s0 += sl) {
     const int64_t ns = std::min<int64_t>(sl, p.n - s0);
@@ -488,17 +307,14 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     a.Kp = plan.Kp;
     bool launched = false;
     if (gather_env < 0) launched = try_rsw_forward(m, a, smax, s, rc);
-    if (gather_env == 100 || (gather_env < 0 && !launched))
-      launched = try_rowstage_forward(m, a, smax, s, rc);
-    if (gather_env == FAM_G4) launched = try_g4_forward(m, a, smax, s, rc, true);
-    else if (gather_env == FAM_ROWS) launched = try_rows_forward(m, a, smax, s, rc, true);
-    else if (gather_env == FAM_TMA) launched = try_tma_forward(m, a, smax, s, rc, true);
     if (!launched) launched = try_ws_forward(m, a, smax, s, rc, true);
     if (!launched) { set_error("no gather kernel fits the staging slice"); *rc = DFFM_SIZING; }
     if (*rc) return true;
+    trace_launch(1, s);
     if ((*rc = tc_mlp_slice(plan, ns, p.status_base + s0, p.prob + s0,
                             p.logit ? p.logit + s0 : nullptr, s)))
       return true;
+    trace_launch(2, s);
   }
   *rc = DFFM_OK;
   return true;
@@ -575,9 +391,21 @@ int pick_k_template(int k, int wdtype) {
 using namespace dffm;
 
 extern "C" int dffm_set_forward_family(int32_t family) {
-  if (family < -1 || family > FAM_TC) { set_error("bad forward family %d", family); return DFFM_CONTRACT; }
-  g_family = family;  // -1: re-read DFFM_FORWARD_KERNEL on the next call
-  g_family_explicit = family >= 0;
+  if (family != -1 && family != FAM_WS && family != FAM_V1 && family != FAM_TC) {
+    set_error("bad forward family %d (-1 default, 1 ws, 2 v1, 5 tc)", family);
+    return DFFM_CONTRACT;
+  }
+  t_family = family;  // this host thread only
+  return DFFM_OK;
+}
+
+extern "C" int dffm_set_event_trace(void** events, int32_t* tags, int32_t capacity,
+                                    int32_t* count) {
+  if (events && (!tags || !count || capacity < 0)) {
+    set_error("event trace needs tags, count and capacity >= 0");
+    return DFFM_CONTRACT;
+  }
+  t_trace = EventTrace{events, tags, events ? capacity : 0, count};
   return DFFM_OK;
 }
 
@@ -603,10 +431,10 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   p.M = max_per_field;
   const int smax = max_smem_optin_current();
   if (try_tc_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
-  if (try_g4_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
-  if (try_rows_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
-  if (try_ws_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
-  if (try_tma_forward(model, p, smax, (cudaStream_t)stream, &rc)) return rc;
+  if (try_ws_forward(model, p, smax, (cudaStream_t)stream, &rc)) {
+    if (!rc) trace_launch(3, (cudaStream_t)stream);
+    return rc;
+  }
   // Tile width: 16 keeps the per-block footprint small enough that the MLP
   // weights stay L1-resident next to three blocks per SM (DFFM_FWD_TE overrides).
   static int te_env = -1;
@@ -629,5 +457,7 @@ extern "C" int dffm_forward(const dffm_model* model, const int32_t* idx, const f
   }
   const int K = pick_k_template(p.k, model->wdtype);
   const int MU = p.M <= 4 ? p.M : 0;
-  return fwd_dispatch(model->wdtype, p, K, MU, L.total, (cudaStream_t)stream);
+  rc = fwd_dispatch(model->wdtype, p, K, MU, L.total, (cudaStream_t)stream);
+  if (!rc) trace_launch(3, (cudaStream_t)stream);
+  return rc;
 }

@@ -318,13 +318,17 @@ def parse_lines(text, schema: InputSchema, device, keep_f64: bool = False,
     cnt = torch.empty((n, F), dtype=torch.uint8, device=dev)
     ex_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
     mx = torch.empty(1, dtype=torch.int32, device=dev)
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    cur = torch.cuda.current_stream(dev)
+    s = stream if stream is not None else cur
+    if s != cur:
+        s.wait_stream(cur)  # inputs were uploaded and outputs allocated on `cur`
     _lib.check(lib.fw_parse_lines(t_text.data_ptr(), t_off.data_ptr(), n, nbytes,
                                   t_names.data_ptr(), t_noff.data_ptr(), t_num.data_ptr(), F,
                                   schema.hash_bits, scratch.data_ptr(), labels.data_ptr(),
                                   status.data_ptr(), cnt.data_ptr(), ex_off.data_ptr(),
                                   mx.data_ptr(), s.cuda_stream), "fw_parse_lines")
-    nnz = int(ex_off[n].item())  # synchronises: the emit pass needs the total
+    s.synchronize()  # the emit pass needs the total; .item() alone syncs only `cur`
+    nnz = int(ex_off[n].item())
     idx = torch.empty(nnz, dtype=torch.int32, device=dev)
     val = torch.empty(nnz, dtype=torch.float32, device=dev)
     val64 = torch.empty(nnz, dtype=torch.float64, device=dev) if keep_f64 else None
@@ -333,6 +337,8 @@ def parse_lines(text, schema: InputSchema, device, keep_f64: bool = False,
                                      ex_off.data_ptr(), idx.data_ptr(), val.data_ptr(),
                                      val64.data_ptr() if keep_f64 else None, s.cuda_stream),
                    "fw_parse_emit")
+    if s != cur:
+        cur.wait_stream(s)  # outputs are consumed on the caller's stream
     out = ParsedLines(RaggedBatch(ex_off, cnt, idx, val, max(1, int(mx.item()))), labels,
                       status, val64)
     if raise_on_error:

@@ -145,6 +145,11 @@ class WeightStore:
         self.nn_size = sum(i * o + o for i, o in self.nn_dims)
         self.weights_total = self.lr_size + self.ffm_size + self.nn_size
         self.total_slots = 2 * self.weights_total
+        # offsets of the blocks in the reference's flat layout (M:182-184)
+        self.ffm_offset = self.lr_size
+        self.nn_offset = self.ffm_offset + self.ffm_size
+        self.acc_offset = self.weights_total
+        self.pair_iu, self.pair_ju = pair_indices(f)
         self.version = 0
         self.q_headers = {}  # table name -> (w_min f32, bucket f32) for u16 stores
         self._cmodel = None
@@ -162,10 +167,12 @@ class WeightStore:
             if with_optimizer:
                 if wdtype != "f32":
                     raise ContractError("only f32 stores carry optimizer state")
-                self.lr_acc = torch.ones(self.lr_size, dtype=torch.float32, device=self.device)
-                self.ffm_acc = torch.ones((self.n_features, f, k), dtype=torch.float32,
-                                          device=self.device)
-                self.nn_accs = [(torch.ones_like(w), torch.ones_like(b))
+                # a bare store is all zeros, accumulators included (M:178-180);
+                # init_model sets them to 1.0 (M:271)
+                self.lr_acc = torch.zeros(self.lr_size, dtype=torch.float32, device=self.device)
+                self.ffm_acc = torch.zeros((self.n_features, f, k), dtype=torch.float32,
+                                           device=self.device)
+                self.nn_accs = [(torch.zeros_like(w), torch.zeros_like(b))
                                 for w, b in self.nn_layers]
 
     # ---------------------------------------------------------------- C view
@@ -261,6 +268,14 @@ class WeightStore:
     def mark_mutated(self):
         self.version += 1
 
+    def fill_accumulators(self, value: float = 1.0) -> "WeightStore":
+        """Set every Adagrad accumulator to ``value`` (init_model uses 1.0, M:271)."""
+        if not self.has_optimizer:
+            raise ContractError("store has no optimizer state")
+        for _, t in self.blocks(True)[len(self.blocks(False)):]:
+            t.fill_(value)
+        return self
+
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for _, t in self.blocks(self.has_optimizer))
 
@@ -303,6 +318,7 @@ def init_model(config: ModelConfig, max_slots: int = DEFAULT_MAX_SLOTS, device=N
         raise SizingError(f"model wants {total} float32 slots, cap is {max_slots};"
                           " lower hash_bits, k, or the layer widths")  # M:248-253
     store = WeightStore(config, device)
+    store.fill_accumulators(1.0)  # M:271
     rng = np.random.default_rng(config.init_seed)
     if config.init_scale_ffm > 0:
         scale = config.init_scale_ffm / math.sqrt(k)
@@ -407,7 +423,10 @@ def predict_batch(idx, val, store: WeightStore, out: torch.Tensor | None = None,
     if out is None:
         out = torch.empty(n, dtype=torch.float32, device=dev)
     st = _status(dev)
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    cur = torch.cuda.current_stream(dev)
+    s = stream if stream is not None else cur
+    if s != cur:
+        s.wait_stream(cur)  # inputs/outputs were staged on the current stream
     with torch.cuda.stream(s):
         st.clear()
         rc = _lib.lib().dffm_forward(store.c_model_ref(), idx.data_ptr(), val.data_ptr(), M, n,
@@ -464,6 +483,9 @@ class HostPredictor:
         lib = _lib.lib()
         cm = self.store.c_model_ref()
         cs, ks = self.copy_stream, self.compute_stream
+        # order K1 after whatever the caller queued on its current stream
+        # (weight writes, quantize_store, in-place edits of the tables)
+        ks.wait_stream(torch.cuda.current_stream(self.store.device))
         h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
         free = [torch.cuda.Event(), torch.cuda.Event()]
         with torch.cuda.stream(ks):
@@ -507,6 +529,9 @@ class HostPredictor:
         lib = _lib.lib()
         cm = self.store.c_model_ref()
         cs, ks = self.copy_stream, self.compute_stream
+        # order K1 after whatever the caller queued on its current stream
+        # (weight writes, quantize_store, in-place edits of the tables)
+        ks.wait_stream(torch.cuda.current_stream(self.store.device))
         dev = self.store.device
         if not hasattr(self, "rg_off"):
             self.rg_off = [torch.empty(self.chunk + 1, dtype=torch.int64, device=dev)
@@ -573,6 +598,9 @@ class HostPredictor:
         lib = _lib.lib()
         cm = self.store.c_model_ref()
         cs, ks = self.copy_stream, self.compute_stream
+        # order K1 after whatever the caller queued on its current stream
+        # (weight writes, quantize_store, in-place edits of the tables)
+        ks.wait_stream(torch.cuda.current_stream(self.store.device))
         dev = self.store.device
         bounds = _chunk_bounds(n, self.chunk)
         off_h, voff_h = batch.ex_off, batch.voff

@@ -48,11 +48,22 @@ def table_digest(*arrays) -> str:
 
 
 def broadcast_store(store, src: int = 0, group=None):
-    """Replicate a trained store's blocks from ``src`` (one NCCL broadcast per
-    block over NVLink/NVSwitch; load-time only, never on the scoring path)."""
+    """Replicate a trained store's blocks from ``src`` (one broadcast per block
+    over NVLink/NVSwitch with NCCL; load-time only, never on the scoring path).
+
+    u16 (quantised) tables travel as int16 bit patterns (NCCL has no uint16)
+    and their per-table (min, bucket) headers, which live on the host, are
+    broadcast alongside, so every replica dequantises identically."""
+    import torch
     import torch.distributed as dist
     for _, t in store.blocks(include_optimizer=store.has_optimizer):
-        dist.broadcast(t, src=src, group=group)
+        dist.broadcast(t.view(torch.int16) if t.dtype == torch.uint16 else t, src=src,
+                       group=group)
+    if store.wdtype == "u16":
+        hdr = [store.q_headers]
+        dist.broadcast_object_list(hdr, src=src, group=group)
+        store.q_headers = dict(hdr[0])
+    store.mark_mutated()  # replicas' states are invalidated like any other write
     return store
 
 

@@ -73,12 +73,12 @@ def test_forward_matches_oracle(F, k, hidden, M, bits, n):
     assert rel_err(p, ref).max() < RTOL
 
 
-@pytest.mark.parametrize("family", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("family", [1, 2, 5])
 @pytest.mark.parametrize("wdtype", ["f32", "bf16", "u16"])
 def test_every_forward_family_matches_oracle(family, wdtype):
-    """All six K1 kernel families (row-coalesced, warp-specialised,
-    CTA-synchronous, TMA-ring, TMA-gather4, gather + tcgen05 3xTF32 MLP) on
-    cfg2-shaped inputs and every table storage type."""
+    """Every K1 kernel family (1 warp-specialised fused, 2 CTA-synchronous,
+    5 row-ring gather + tcgen05 3xTF32 MLP) on cfg2-shaped inputs and every
+    table storage type."""
     from paper_2407_10115_b200 import _lib
     from paper_2407_10115_b200.quant import quantize_store
     wl = configs.CFG2

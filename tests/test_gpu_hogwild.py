@@ -22,7 +22,7 @@ BITS = 14
 def make_store(seed=3):
     cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=BITS, lr_ffm=0.05,
                       lr_lr=0.05, lr_nn=0.05)
-    st = WeightStore(cfg, DEV)
+    st = WeightStore(cfg, DEV).fill_accumulators(1.0)
     g = torch.Generator(device=DEV).manual_seed(seed)
     for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
         t.view(-1).copy_(torch.randn(t.numel(), generator=g, device=DEV) * 0.05)

@@ -75,7 +75,7 @@ def test_train_full_size_table_prefix(n):
     wl = configs.CFG3
     cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=24, lr_ffm=0.1,
                       lr_lr=0.1, lr_nn=0.1, power_t=0.5)
-    st = WeightStore(cfg, DEV)
+    st = WeightStore(cfg, DEV).fill_accumulators(1.0)
     gen = torch.Generator(device=DEV).manual_seed(wl.weight_seed)
     st.lr.copy_(synth.normal_table(st.lr.numel(), 0.05, gen, DEV))
     st.ffm.view(-1).copy_(synth.normal_table(st.ffm.numel(), 0.05, gen, DEV))

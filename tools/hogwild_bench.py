@@ -20,7 +20,7 @@ idx, val = synth.make_examples(wl, n, device=dev)
 
 
 def store(seed):
-    st = WeightStore(cfg, dev, with_optimizer=True)
+    st = WeightStore(cfg, dev, with_optimizer=True).fill_accumulators(1.0)
     g = torch.Generator(device=dev).manual_seed(seed)
     for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
         flat = t.view(-1)

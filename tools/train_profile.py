@@ -15,7 +15,7 @@ wl = configs.CFG3
 dev = torch.device("cuda:0")
 cfg = ModelConfig(n_fields=24, k=8, hidden_sizes=(64, 32), hash_bits=bits, lr_ffm=0.1, lr_lr=0.1,
                   lr_nn=0.1)
-st = WeightStore(cfg, dev)
+st = WeightStore(cfg, dev).fill_accumulators(1.0)
 g = torch.Generator(device=dev).manual_seed(1)
 for t in [st.lr, st.ffm] + [x for wb in st.nn_layers for x in wb]:
     t.view(-1).copy_(torch.randn(t.numel(), generator=g, device=dev) * 0.05)
