@@ -818,14 +818,14 @@ def bench_adagrad(args, dev, clk_index=0):
     torch.cuda.empty_cache()
     # K6: the same prefix through the Hogwild trainer with every worker the GPU
     # holds at once (T:269-336); logloss compared with the sequential run above
-    from paper_2407_10115_b200.training import hogwild_train, max_hogwild_workers
+    from paper_2407_10115_b200.training import hogwild_train_arrays, max_hogwild_workers
     sh = student()
     w = max_hogwild_workers(sh, idx.shape[2])
-    hogwild_train(idx[:warm], val[:warm], labels[:warm], sh, TrainOptions(n_threads=w))
+    hogwild_train_arrays(idx[:warm], val[:warm], labels[:warm], sh, TrainOptions(n_threads=w))
     torch.cuda.synchronize()
     hs, he = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     hs.record()
-    hrep = hogwild_train(idx[warm:], val[warm:], labels[warm:], sh,
+    hrep = hogwild_train_arrays(idx[warm:], val[warm:], labels[warm:], sh,
                          TrainOptions(n_threads=w, chunk=1 << 22))
     he.record()
     torch.cuda.synchronize()

@@ -297,6 +297,31 @@ uint64_t fw_fnv1a64_host(const uint8_t* data_host, int64_t n);
 int fw_eval_stream(const double* probs, const uint8_t* labels, int64_t n, int32_t window,
                    double* auc_out, double* loss_out, void* stream);
 
+/*
+ * K11 single-example trace (M:321-397 forward with every intermediate the
+ * reference's ForwardState keeps, M:275-290) and dense loss gradient
+ * (M:575-634 loss_gradients), f64, one CTA.  idx/val: ONE example in the
+ * padded layout [n_fields][max_per_field] (device).  trace: device f64
+ * buffer of dffm_trace_len(model) values:
+ *   [0] lr_out  [1] logit  [2] merge mu  [3] merge sd  [4] nn output
+ *   [5] sum of pair outputs  [6..7] reserved
+ *   [DFFM_TRACE_HEAD ..] latent sums S [F][F][k], pair outputs [P],
+ *   merge vector v [D], merged input [D], then per hidden layer
+ *   pre-activations [h] followed by activations [h].
+ * dffm_loss_gradients zero-fills grad (f64, the weights' flat layout
+ * lr | ffm | per layer W, b: dffm's weights_total values) and writes the
+ * log-loss gradient of that example and label; scratch holds
+ * dffm_grad_scratch_len(model) doubles.
+ */
+#define DFFM_TRACE_HEAD 8
+int64_t dffm_trace_len(const dffm_model* model);
+int dffm_forward_trace(const dffm_model* model, const int32_t* idx, const float* val,
+                       int32_t max_per_field, double* trace, void* stream);
+int64_t dffm_grad_scratch_len(const dffm_model* model);
+int dffm_loss_gradients(const dffm_model* model, const int32_t* idx, const float* val,
+                        int32_t max_per_field, const double* trace, int32_t label,
+                        double* grad, int64_t grad_len, double* scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

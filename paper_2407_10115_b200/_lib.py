@@ -18,6 +18,7 @@ from . import errors
 LIB_PATH = os.environ.get("DFFM_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libdffm.so")
 MAX_LAYERS = 5
+TRACE_HEAD = 8  # DFFM_TRACE_HEAD
 
 OK, CONTRACT, FORMAT, NUMERIC, SIZING, CUDA = range(6)
 BLOCKS = {0: None, 1: "lr", 2: "ffm", 3: "merge", 4: "nn", 5: "logit", 6: "loss"}
@@ -54,6 +55,12 @@ SIGNATURES = {
                                c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "dffm_set_forward_family": (c_int32, [c_int32]),
     "dffm_set_event_trace": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    "dffm_trace_len": (c_int64, [POINTER(DffmModel)]),
+    "dffm_forward_trace": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_void_p,
+                                     c_void_p]),
+    "dffm_grad_scratch_len": (c_int64, [POINTER(DffmModel)]),
+    "dffm_loss_gradients": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_void_p,
+                                      c_int32, c_void_p, c_int64, c_void_p, c_void_p]),
     "dffm_ctx_score": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_int32,
                                  c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p,
                                  c_void_p, c_void_p]),

@@ -17,9 +17,53 @@ inputs.
 
 from __future__ import annotations
 
+import math
+from dataclasses import dataclass
+
 import numpy as np
 
 from .errors import ContractError
+
+
+def transform_numeric(v: float) -> float:
+    """ln(1+v) for v > 0, else v (Fe:33-39); K10 applies it on the device for
+    the numeric fields of parsed text."""
+    return math.log1p(v) if v > 0 else v
+
+
+@dataclass(frozen=True)
+class FieldFeatures:
+    """Features of one field: sorted unique hashed indices (int64) and their
+    f64 values (Fe:121-143)."""
+
+    field_id: int
+    indices: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.indices.flags.writeable = False
+        self.values.flags.writeable = False
+
+    def __eq__(self, other):
+        return (isinstance(other, FieldFeatures) and self.field_id == other.field_id
+                and np.array_equal(self.indices, other.indices)
+                and np.array_equal(self.values, other.values))
+
+    def __len__(self) -> int:
+        return len(self.indices)
+
+
+@dataclass(frozen=True)
+class ParsedExample:
+    """One labeled instance: binary label plus per-field hashed features in the
+    order the fields first appear (Fe:145-157)."""
+
+    label: int
+    fields: tuple
+
+    def __eq__(self, other):
+        return (isinstance(other, ParsedExample) and self.label == other.label
+                and self.fields == other.fields)
 
 
 def pack_examples(examples, n_fields: int, max_per_field: int | None = None):
@@ -471,3 +515,94 @@ class HostTextParser:
                              self.idx[base:base + nnz], self.val[base:base + nnz], max(1, mxc))
             out.append((c0, c1, ParsedLines(rb, self.labels[c0:c1], self.status[c0:c1])))
         return out
+
+
+def _segment_field_order(line: str, schema: InputSchema):
+    """Field ids in order of first appearance (Fe:186-196): the '|' segment heads."""
+    order, seen = [], set()
+    for seg in line.split("|")[1:]:
+        atoms = seg.split()
+        if atoms:
+            fid = schema.field_id(atoms[0])
+            if fid not in seen:
+                seen.add(fid)
+                order.append(fid)
+    return order
+
+
+def _examples_from_parsed(out: "ParsedLines", lines, schema: InputSchema):
+    """K10 output (ragged, f64 values kept) -> ParsedExample per line."""
+    b = out.batch
+    ex_off = b.ex_off.cpu().numpy()
+    cnt = b.cnt.cpu().numpy()
+    idx = b.idx.cpu().numpy().astype(np.int64)
+    val = out.val64.cpu().numpy()
+    labels = out.labels.cpu().numpy()
+    res = []
+    for i, line in enumerate(lines):
+        pos = int(ex_off[i])
+        per = {}
+        for f in range(schema.n_fields):
+            m = int(cnt[i, f])
+            if m:
+                per[f] = (idx[pos:pos + m].copy(), val[pos:pos + m].copy())
+                pos += m
+        fields = []
+        for f in _segment_field_order(line, schema):
+            ii, vv = per.get(f, (np.empty(0, np.int64), np.empty(0, np.float64)))
+            fields.append(FieldFeatures(f, ii, vv))
+        res.append(ParsedExample(int(labels[i]), tuple(fields)))
+    return res
+
+
+def _check_gpu_status(out: "ParsedLines", first_line: int = 0):
+    from .errors import ParseError
+    err = out.first_error(skip_blank=False)
+    if err is not None:
+        i, msg = err
+        code = int(out.status[i])
+        if code in (8, 9, 10):  # lines the reference accepts but K10 cannot take
+            raise ContractError(f"line {first_line + i + 1}: {msg}")
+        raise ParseError(f"line {first_line + i + 1}: {msg}")
+
+
+def parse_example(line: str, schema: InputSchema, device=None) -> ParsedExample:
+    """Parse one text example (Fe:223-235) with K10 on the device: label, field
+    blocks, FNV-1a hashing, numeric transform, duplicate merge; values kept in
+    f64.  Raises ParseError exactly where the reference does."""
+    import torch
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    text = line.encode("utf-8")
+    if b"\n" in text.rstrip(b"\n"):
+        from .errors import ParseError
+        raise ParseError("one example per line")
+    out = parse_lines(text.rstrip(b"\n") + b"\n", schema, dev, keep_f64=True,
+                      raise_on_error=False, skip_blank=False)
+    if int(out.status[0]) == 11:  # whitespace-only: the reference's label check fails
+        from .errors import ParseError
+        raise ParseError(f"malformed label {line.split('|')[0].strip()!r} (want 0, 1, or -1)")
+    _check_gpu_status(out)
+    return _examples_from_parsed(out, [line], schema)[0]
+
+
+def parse_field_blocks(text: str, schema: InputSchema, device=None) -> tuple:
+    """Label-less '|field ...' request text -> FieldFeatures (Fe:238-249)."""
+    from .errors import ParseError
+    stripped = text.strip()
+    if not stripped.startswith("|"):
+        raise ParseError("field blocks must start with '|'")
+    if stripped == "|":
+        return ()
+    return parse_example("0 " + stripped, schema, device).fields
+
+
+def serialize_example(example: ParsedExample, schema: InputSchema) -> str:
+    """Debug serializer (Fe:252-264): raw '@index:value' tokens that re-parse
+    to an identical ParsedExample."""
+    parts = [str(example.label)]
+    for ff in example.fields:
+        block = [f"|{schema.field_names[ff.field_id]}"]
+        for i, v in zip(ff.indices, ff.values):
+            block.append(f"@{int(i)}:{float(v)!r}")
+        parts.append(" ".join(block))
+    return " ".join(parts)

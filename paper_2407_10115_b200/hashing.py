@@ -6,12 +6,19 @@ byte buffer + int64 offsets and hashed in one launch.
 
 from __future__ import annotations
 
+import hashlib
+from functools import lru_cache
+
 import numpy as np
 import torch
 
 from . import _lib
 from .errors import ContractError
 
+FNV32_OFFSET = 0x811C9DC5  # H:15
+FNV32_PRIME = 0x01000193  # H:16
+FNV64_OFFSET = 0xCBF29CE484222325  # H:17
+FNV64_PRIME = 0x00000100000001B3  # H:18
 FIELD_TOKEN_SEP = b"\x1f"  # H:22
 MIN_HASH_BITS = 10  # H:24
 MAX_HASH_BITS = 29  # H:25
@@ -48,3 +55,33 @@ def hash_features(pairs, hash_bits: int, device="cuda") -> torch.Tensor:
     items = [f.encode("utf-8") + FIELD_TOKEN_SEP + t.encode("utf-8") for f, t in pairs]
     blob, off = pack_strings(items)
     return hash_bytes(blob, off, hash_bits, device)
+
+
+def _device():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def fnv1a32(data: bytes) -> int:
+    """32-bit FNV-1a of a byte string (H:28-32), computed by K5 on the device."""
+    blob, off = pack_strings([bytes(data)])
+    return int(hash_bytes(blob, off, 32, _device())[0].item())
+
+
+def fnv1a64(data: bytes) -> int:
+    """64-bit FNV-1a (H:35-39): serial by definition, the library's host routine."""
+    import ctypes
+    buf = bytes(data)
+    return int(_lib.lib().fw_fnv1a64_host(ctypes.c_char_p(buf), len(buf)))
+
+
+@lru_cache(maxsize=1 << 20)
+def hash_feature(field_name: str, token: str, hash_bits: int) -> int:
+    """Map (field, token) to a stable index below 2**hash_bits (H:42-50), K5 on
+    the device; cached like the reference (H:42)."""
+    return int(hash_features([(field_name, token)], hash_bits, _device())[0].item())
+
+
+def content_digest(data) -> int:
+    """64-bit digest of a byte buffer keying patches against their base (H:53-59):
+    blake2b-64, little-endian, as the reference defines it."""
+    return int.from_bytes(hashlib.blake2b(data, digest_size=8).digest(), "little")

@@ -4,8 +4,8 @@ Host-side restatement of the reference's progressive logloss, 30k
 non-overlapping-window midrank AUC and RIG (Me:21-139), fed with the
 probabilities the GPU kernels return.  Vectorised numpy: a whole window (or a
 whole progressive stream) is folded at once instead of one Python call per
-example.  Checked against the reference's own outputs in
-tests/test_metrics.py (golden metrics.npz).
+example.  Checked against the reference's own outputs (golden metrics.npz) in
+tests/test_host.py and, for the K8 device evaluator, tests/test_gpu_eval.py.
 """
 
 from __future__ import annotations
@@ -99,6 +99,50 @@ def stream_metrics_gpu(probs, labels, window: int = 30000):
     for v in loss.cpu().numpy().tolist():
         total += v
     return series, total, n
+
+
+class MetricWindow:
+    """Bounded buffer of recent (score, label) pairs (Me:62-90)."""
+
+    def __init__(self, capacity: int = 30000):
+        if capacity < 2:
+            raise ContractError("window capacity must be >= 2")
+        self.capacity = capacity
+        self._scores: list = []
+        self._labels: list = []
+
+    def __len__(self) -> int:
+        return len(self._scores)
+
+    @property
+    def full(self) -> bool:
+        return len(self._scores) >= self.capacity
+
+    def add(self, score: float, label: int):
+        self._scores.append(score)
+        self._labels.append(label)
+
+    def auc(self):
+        if not self._scores:
+            return None
+        return window_auc(self._scores, self._labels)
+
+    def clear(self):
+        self._scores.clear()
+        self._labels.clear()
+
+
+def rolling_auc(pairs, window: int = 30000):
+    """Yield (examples_seen, auc_or_None) per completed non-overlapping window
+    (Me:93-106)."""
+    buf = MetricWindow(window)
+    seen = 0
+    for score, label in pairs:
+        buf.add(score, label)
+        seen += 1
+        if buf.full:
+            yield seen, buf.auc()
+            buf.clear()
 
 
 class StreamingEvaluator:

@@ -337,15 +337,36 @@ def init_model(config: ModelConfig, max_slots: int = DEFAULT_MAX_SLOTS, device=N
 # --------------------------------------------------------------------------- forward
 
 
+class OpCounter:
+    """Counts multiply-add units in interaction-block inner loops (M:130-139)."""
+
+    __slots__ = ("madds",)
+
+    def __init__(self):
+        self.madds = 0
+
+    def add(self, n: int):
+        self.madds += int(n)
+
+
 @dataclass
 class ForwardState:
-    """Per-example forward result (M:275-290).  The GPU path keeps the
-    intermediates on the device inside the fused kernels; only the logit
-    (and the store version it was computed against) surface here."""
+    """Per-example intermediates kept for the backward pass (M:275-290).
 
+    ``forward`` fills every field from the K11 device trace (f64); the batched
+    paths (K1 / K2) keep these on chip and never materialise them."""
+
+    lr_out: float
+    ffm_pair_outputs: np.ndarray  # float64 (n_pairs,)
+    merged_input: np.ndarray  # float64 (1 + n_pairs,)
+    layer_pre_acts: list
+    layer_acts: list
     logit: float
-    lr_out: float = float("nan")
-    _store: WeightStore = field(repr=False, default=None)
+    latent_sums: np.ndarray = field(repr=False, default=None)  # (F, F, k)
+    merge_vec: np.ndarray = field(repr=False, default=None)
+    merge_mu: float = 0.0
+    merge_sd: float = 0.0
+    _store: "WeightStore" = field(repr=False, default=None)
     _store_version: int = 0
 
 
@@ -663,13 +684,143 @@ class HostPredictor:
         return out_host
 
 
-def forward(example, store: WeightStore, mac_counter=None) -> ForwardState:
-    """One example through the fused kernel (API of M:321)."""
-    from .features import pack_examples
-    idx, val, _ = pack_examples([example], store.config.n_fields)
-    lg = torch.empty(1, dtype=torch.float32, device=store.device)
-    predict_batch(idx, val, store, logits=lg)
-    return ForwardState(logit=float(lg.item()), _store=store, _store_version=store.version)
+def _example_arrays(example, store: WeightStore):
+    """One ParsedExample-like object -> padded device idx/val [1, F, M] (M >= 1);
+    a field id >= F is the ContractError of M:331-334."""
+    f_count = store.config.n_fields
+    m = 1
+    for ff in example.fields:
+        if ff.field_id >= f_count:
+            raise ContractError(f"field id {ff.field_id} outside model's {f_count} fields")
+        m = max(m, len(ff.indices))
+    idx = np.full((1, f_count, m), -1, np.int32)
+    val = np.zeros((1, f_count, m), np.float32)
+    for ff in example.fields:
+        n = len(ff.indices)
+        if n:
+            idx[0, ff.field_id, :n] = np.asarray(ff.indices, np.int64)
+            val[0, ff.field_id, :n] = np.asarray(ff.values, np.float64)
+    return (torch.from_numpy(idx).to(store.device), torch.from_numpy(val).to(store.device))
+
+
+def _count_macs(example, store: WeightStore, state: ForwardState, counter: OpCounter):
+    """M:340-341, M:352-353, M:374-375: the reference's MAC accounting."""
+    f_count, k = store.config.n_fields, store.config.k
+    present = set()
+    for ff in example.fields:
+        m = len(ff.indices)
+        if m:
+            counter.add(m + m * f_count * k)
+            present.add(ff.field_id)
+    n_active = sum(1 for a, b in zip(store.pair_iu, store.pair_ju)
+                   if a in present and b in present)
+    if n_active:
+        counter.add(n_active * k)
+    if store.nn_dims:
+        counter.add(sum(i * o for i, o in store.nn_dims))
+
+
+def _diagnose_nonfinite(state: ForwardState) -> str:
+    """First non-finite stage in the order lr, ffm, merge, nn, logit (M:308-318)."""
+    if not math.isfinite(state.lr_out):
+        return "lr"
+    if not np.isfinite(state.ffm_pair_outputs).all():
+        return "ffm"
+    if not np.isfinite(state.merged_input).all():
+        return "merge"
+    for z in state.layer_pre_acts:
+        if not np.isfinite(z).all():
+            return "nn"
+    return "logit"
+
+
+def _trace(store: WeightStore, idx: torch.Tensor, val: torch.Tensor) -> torch.Tensor:
+    lib = _lib.lib()
+    cm = store.c_model_ref()
+    n = int(lib.dffm_trace_len(cm))
+    if n < 0:
+        _lib.check(_lib.CONTRACT, "dffm_trace_len")
+    out = torch.empty(n, dtype=torch.float64, device=store.device)
+    s = torch.cuda.current_stream(store.device)
+    _lib.check(lib.dffm_forward_trace(cm, idx.data_ptr(), val.data_ptr(), idx.shape[2],
+                                      out.data_ptr(), s.cuda_stream), "dffm_forward_trace")
+    return out
+
+
+def forward(example, store: WeightStore, mac_counter: OpCounter | None = None) -> ForwardState:
+    """One example through every block, keeping the intermediates (M:321-397).
+
+    K11 (csrc/trace.cu) computes the reference's stages in f64 on the device:
+    LR sum, latent sums S (F, F, k), DiagMask pairs, MergeNorm, the MLP layer
+    by layer, the residual logit.  Read-only on the store; a non-finite logit
+    raises NumericError(block=...) with the reference's diagnosis order."""
+    idx, val = _example_arrays(example, store)
+    tr = _trace(store, idx, val).cpu().numpy()
+    cfg = store.config
+    f_count, k, P, D = cfg.n_fields, cfg.k, store.n_pairs, store.merged_width
+    o = _lib.TRACE_HEAD
+    S = tr[o:o + f_count * f_count * k].reshape(f_count, f_count, k)
+    o += f_count * f_count * k
+    pairs = tr[o:o + P]
+    v = tr[o + P:o + P + D]
+    merged = tr[o + P + D:o + P + 2 * D]
+    o += P + 2 * D
+    pre, acts = [], []
+    for _, width in store.nn_dims[:-1]:
+        pre.append(tr[o:o + width].copy())
+        acts.append(tr[o + width:o + 2 * width].copy())
+        o += 2 * width
+    state = ForwardState(lr_out=float(tr[0]), ffm_pair_outputs=pairs.copy(),
+                         merged_input=merged.copy(), layer_pre_acts=pre, layer_acts=acts,
+                         logit=float(tr[1]), latent_sums=S.copy(), merge_vec=v.copy(),
+                         merge_mu=float(tr[2]), merge_sd=float(tr[3]), _store=store,
+                         _store_version=store.version)
+    if mac_counter is not None:
+        _count_macs(example, store, state, mac_counter)
+    if not math.isfinite(state.logit):
+        blk = _diagnose_nonfinite(state)
+        raise NumericError(f"non-finite value in {blk} block", block=blk)
+    return state
+
+
+def backward_update(state: ForwardState, example, label: int, store: WeightStore,
+                    sparse: bool = True) -> float:
+    """Backpropagate one example and apply the Adagrad updates in place
+    (M:440-533); returns the example's log-loss and bumps ``store.version``.
+
+    The step runs in K2 (csrc/train.cu), the same kernel as the batched trainer:
+    it recomputes the forward pass on chip (identical to ``state``), merges
+    duplicate buckets in occurrence order and applies the f64 Adagrad rule."""
+    if state._store is not store or state._store_version != store.version:
+        raise ContractError("forward state was not produced against this store state")
+    if label not in (0, 1):
+        raise ContractError(f"label must be 0 or 1, got {label!r}")
+    from .training import _train_one
+    p = _train_one(example, label, store, sparse)
+    return -math.log(p) if label else -math.log1p(-p)
+
+
+def loss_gradients(state: ForwardState, example, label: int, store: WeightStore) -> np.ndarray:
+    """Dense float64 gradient of the log-loss over the weights' flat layout
+    (M:575-634; lr | ffm | per layer W, b -- no accumulator block), computed
+    by K11 on the device from the example's trace."""
+    if state._store is not store or state._store_version != store.version:
+        raise ContractError("forward state was not produced against this store state")
+    if label not in (0, 1):
+        raise ContractError(f"label must be 0 or 1, got {label!r}")
+    idx, val = _example_arrays(example, store)
+    tr = _trace(store, idx, val)
+    lib = _lib.lib()
+    cm = store.c_model_ref()
+    grad = torch.empty(store.weights_total, dtype=torch.float64, device=store.device)
+    scratch = torch.empty(max(1, int(lib.dffm_grad_scratch_len(cm))), dtype=torch.float64,
+                          device=store.device)
+    s = torch.cuda.current_stream(store.device)
+    _lib.check(lib.dffm_loss_gradients(cm, idx.data_ptr(), val.data_ptr(), idx.shape[2],
+                                       tr.data_ptr(), int(label), grad.data_ptr(),
+                                       store.weights_total, scratch.data_ptr(), s.cuda_stream),
+               "dffm_loss_gradients")
+    return grad.cpu().numpy()
 
 
 # --------------------------------------------------------------------------- serialisation

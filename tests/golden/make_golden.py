@@ -21,6 +21,12 @@ outputs of the unmodified reference package ``fieldwise``:
 * ``parse.npz``     -- features.parse_example (Fe:175-235) over seeded text
                        lines with edge cases: which lines raise ParseError,
                        labels, canonical (field, index, value) per line
+* ``api.npz``       -- the per-example API and the text-source loops:
+                       ForwardState intermediates (M:275-290), mac_counter
+                       (M:130-139), loss_gradients (M:575-634), the literal
+                       T:175-185 loop, train_stream / hogwild_train(1) /
+                       evaluate_stream (T:188-236) over text lines with blank
+                       and unparseable lines
 
 Nothing here runs on the GPU box; /root/reference does not exist there.
 """
@@ -337,7 +343,99 @@ def parse_fixture():
     print("parse", len(lines), "lines,", sum(ok), "ok,", len(idx), "features")
 
 
+def api_fixture():
+    """Reference outputs of the per-example API and the text-source loops."""
+    wl = configs.CFG3
+    F, k, hidden, bits = 6, 4, (16, 8), 10
+    n = 240
+    idx, val = synth.make_examples(wl, n, seed=131, hash_bits=bits, salted=False,
+                                   n_fields=F)
+    idx, val = idx.numpy(), val.numpy()
+    idx[0] = -1  # all-empty example
+    val[0] = 0
+    idx[1, 1:] = -1  # single field
+    val[1, 1:] = 0
+    rng = np.random.default_rng(132)
+    labels = (rng.random(n) < 0.4).astype(np.uint8)
+    flat = seeded_flat(F, k, hidden, bits, 133, 0.1)
+    names = tuple(f"c{f}" for f in range(F))
+    schema = InputSchema(names, frozenset(), bits)
+    lines = [serialize_example(to_example(idx[e], val[e], labels[e]), schema) for e in range(n)]
+    # text stream with blank and unparseable lines sprinkled in (T:176-181)
+    text = []
+    for e, ln in enumerate(lines):
+        if e % 37 == 5:
+            text.append("   \n")
+        if e % 53 == 7:
+            text.append("2 |c0 @1\n")  # bad label: counted, skipped
+        text.append(ln + "\n")
+    # ForwardState / mac_counter / loss_gradients on the first 8 examples
+    st = ref_store(F, k, hidden, bits, flat)
+    keep = {}
+    for e in range(8):
+        ex = to_example(idx[e], val[e], labels[e])
+        mc = rm.OpCounter()
+        s = rm.forward(ex, st, mac_counter=mc)
+        keep[f"e{e}_lr_out"] = s.lr_out
+        keep[f"e{e}_logit"] = s.logit
+        keep[f"e{e}_pairs"] = s.ffm_pair_outputs
+        keep[f"e{e}_merged"] = s.merged_input
+        keep[f"e{e}_S"] = s.latent_sums
+        keep[f"e{e}_v"] = s.merge_vec
+        keep[f"e{e}_mu_sd"] = np.array([s.merge_mu, s.merge_sd])
+        for li, (z, a) in enumerate(zip(s.layer_pre_acts, s.layer_acts)):
+            keep[f"e{e}_pre{li}"] = z
+            keep[f"e{e}_act{li}"] = a
+        keep[f"e{e}_macs"] = mc.madds
+        keep[f"e{e}_grad"] = rm.loss_gradients(s, ex, int(labels[e]), st)
+    # the literal T:175-185 loop: forward -> predict_proba -> backward_update
+    st = ref_store(F, k, hidden, bits, flat)
+    loop_p, loop_loss = [], []
+    for e in range(n):
+        ex = to_example(idx[e], val[e], labels[e])
+        s = rm.forward(ex, st)
+        loop_p.append(rm.predict_proba(s.logit))
+        loop_loss.append(rm.backward_update(s, ex, ex.label, st))
+    loop_final = st.flat.copy()
+    loop_version = st.version
+    # train_stream over the text lines
+    st = ref_store(F, k, hidden, bits, flat)
+    rep = rt.train_stream(iter(text), st, schema)
+    ts_final = st.flat.copy()
+    # hogwild_train with one worker (byte-identical to sequential, T:1-11)
+    st = ref_store(F, k, hidden, bits, flat)
+    hrep = rt.hogwild_train(iter(text), st, schema, rt.TrainOptions(n_threads=1))
+    hw_final = st.flat.copy()
+    # evaluate_stream on the good lines (+ blank lines) against the trained store
+    st = ref_store(F, k, hidden, bits, flat)
+    st.flat[:] = ts_final
+    ev_lines = [t for t in text if not t.startswith("2 ") and ("|" in t or not t.strip())]
+    auc, ll, cnt = rt.evaluate_stream(iter(ev_lines), st, schema)
+    series = np.array([(i, np.nan if a is None else a) for i, a in rep.rolling_auc_series])
+    np.savez_compressed(os.path.join(HERE, "api.npz"), idx=idx, val=val, labels=labels,
+                        F=F, k=k, hidden=np.array(hidden, np.int64), bits=bits, w_seed=133,
+                        scale=0.1, flat_sha=sha(flat), names=np.array(names),
+                        text=np.array("".join(text)),
+                        loop_p=np.array(loop_p), loop_loss=np.array(loop_loss),
+                        loop_final=loop_final, loop_version=loop_version,
+                        ts_seen=rep.examples_seen, ts_parse_errors=rep.parse_errors,
+                        ts_logloss=rep.progressive_logloss, ts_series=series,
+                        ts_final=ts_final, ts_version=st.version,
+                        hw_seen=hrep.examples_seen, hw_parse_errors=hrep.parse_errors,
+                        hw_logloss=hrep.progressive_logloss, hw_final=hw_final,
+                        hw_series=np.array([(i, np.nan if a is None else a)
+                                            for i, a in hrep.rolling_auc_series]),
+                        ev_auc=np.nan if auc is None else auc, ev_logloss=ll, ev_n=cnt,
+                        **keep)
+    print("api", n, "examples; parse errors", rep.parse_errors, "logloss",
+          rep.progressive_logloss, "eval", auc, ll, cnt)
+
+
 def main():
+    if len(sys.argv) > 1:  # regenerate only the named fixtures
+        for name in sys.argv[1:]:
+            globals()[name + "_fixture"]()
+        return
     hash_fixture()
     fwd_fixture("cfg1", configs.CFG1, 256, 10, 101, 0.1)
     fwd_fixture("cfg2", configs.CFG2, 256, 12, 102, 0.05)
@@ -350,6 +448,7 @@ def main():
     metrics_fixture()
     serial_fixture()
     parse_fixture()
+    api_fixture()
 
 
 if __name__ == "__main__":

@@ -11,7 +11,7 @@ import torch
 from paper_2407_10115_b200 import configs, synth
 from paper_2407_10115_b200.errors import ContractError, HogwildWorkerError
 from paper_2407_10115_b200.model import ModelConfig, WeightStore, predict_batch
-from paper_2407_10115_b200.training import (TrainOptions, hogwild_train, max_hogwild_workers,
+from paper_2407_10115_b200.training import (TrainOptions, hogwild_train_arrays, max_hogwild_workers,
                                              train_sequential)
 
 pytestmark = pytest.mark.gpu
@@ -46,7 +46,7 @@ def snapshot(st):
 def test_one_worker_is_the_sequential_schedule():
     idx, val, labels = planted_stream(3000)
     a, b = make_store(), make_store()
-    ra = hogwild_train(idx, val, labels, a, TrainOptions(n_threads=1))
+    ra = hogwild_train_arrays(idx, val, labels, a, TrainOptions(n_threads=1))
     rb = train_sequential(idx, val, labels, b, TrainOptions())
     for x, y in zip(snapshot(a), snapshot(b)):
         assert torch.equal(x, y)  # byte-identical weights and accumulators
@@ -57,11 +57,11 @@ def test_one_worker_is_the_sequential_schedule():
 def test_parallel_workers_logloss_within_two_percent():
     n = 40000
     idx, val, labels = planted_stream(n)
-    ref = hogwild_train(idx, val, labels, make_store(), TrainOptions(n_threads=1))
+    ref = hogwild_train_arrays(idx, val, labels, make_store(), TrainOptions(n_threads=1))
     for w in (4, 32):
         st = make_store()
         v0 = st.version
-        rep = hogwild_train(idx, val, labels, st, TrainOptions(n_threads=w))
+        rep = hogwild_train_arrays(idx, val, labels, st, TrainOptions(n_threads=w))
         assert rep.examples_seen == n and np.isfinite(rep.progressive_logloss)
         assert rep.rolling_auc_series == []  # only meaningful for one worker
         assert st.version == v0 + 1          # T:318 mark_mutated
@@ -79,7 +79,7 @@ def test_worker_failure_surfaces_with_worker_id():
     labels[777] = 2  # M:453-454 ContractError inside a worker
     w = 8
     with pytest.raises(HogwildWorkerError) as ei:
-        hogwild_train(idx, val, labels, make_store(), TrainOptions(n_threads=w))
+        hogwild_train_arrays(idx, val, labels, make_store(), TrainOptions(n_threads=w))
     assert ei.value.worker_id == 777 % w
     assert isinstance(ei.value.__cause__, ContractError)
 
@@ -87,8 +87,8 @@ def test_worker_failure_surfaces_with_worker_id():
 def test_workers_scale_throughput():
     n = 20000
     idx, val, labels = planted_stream(n)
-    hogwild_train(idx[:500], val[:500], labels[:500], make_store(), TrainOptions(n_threads=64))
-    r1 = hogwild_train(idx, val, labels, make_store(), TrainOptions(n_threads=1))
+    hogwild_train_arrays(idx[:500], val[:500], labels[:500], make_store(), TrainOptions(n_threads=64))
+    r1 = hogwild_train_arrays(idx, val, labels, make_store(), TrainOptions(n_threads=1))
     w = min(64, max_hogwild_workers(make_store(), idx.shape[2]))
-    rw = hogwild_train(idx, val, labels, make_store(), TrainOptions(n_threads=w))
+    rw = hogwild_train_arrays(idx, val, labels, make_store(), TrainOptions(n_threads=w))
     assert rw.throughput >= 2 * r1.throughput, (rw.throughput, r1.throughput)

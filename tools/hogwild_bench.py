@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2407_10115_b200 import configs, synth  # noqa: E402
 from paper_2407_10115_b200.model import ModelConfig, WeightStore, predict_batch  # noqa: E402
-from paper_2407_10115_b200.training import (TrainOptions, hogwild_train,  # noqa: E402
+from paper_2407_10115_b200.training import (TrainOptions, hogwild_train_arrays,  # noqa: E402
                                              max_hogwild_workers)
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200000
@@ -40,10 +40,10 @@ print(f"max concurrent workers: {wmax}")
 for w in [1, 4, 16, 64, 148, wmax]:
     st = store(1004)
     m = n if w > 1 else min(n, 50000)
-    hogwild_train(idx[:200], val[:200], labels[:200], st, TrainOptions(n_threads=w))
+    hogwild_train_arrays(idx[:200], val[:200], labels[:200], st, TrainOptions(n_threads=w))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rep = hogwild_train(idx[200:m], val[200:m], labels[200:m], st, TrainOptions(n_threads=w))
+    rep = hogwild_train_arrays(idx[200:m], val[200:m], labels[200:m], st, TrainOptions(n_threads=w))
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     print(f"workers={w:4d} examples={m - 200} ex/s={(m - 200) / dt:12.0f} "
