@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -263,6 +264,28 @@ struct Seg<0, T> {
 };
 
 // np.maximum(z, 0.0) semantics (M:370): NaN propagates (fmaxf would drop it)
+// Staged MergeNorm rows for the tensor-core MLP (mlp_tc.cu): two fp16 planes,
+// x = hi + lo with hi = fp16(x), lo = fp16(x - hi) (22 significant bits), each
+// plane row-major [rows][Kp] halfs, lo plane `plane` halfs after hi.
+__device__ __forceinline__ void xstore1(__half* x, int64_t plane, int64_t i, float v) {
+  const __half h = __float2half_rn(v);
+  x[i] = h;
+  x[plane + i] = __float2half_rn(v - __half2float(h));
+}
+__device__ __forceinline__ void xstore4(__half* x, int64_t plane, int64_t i, const float* v) {
+  uint32_t h[2], l[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const __half a = __float2half_rn(v[2 * t]), b = __float2half_rn(v[2 * t + 1]);
+    const __half al = __float2half_rn(v[2 * t] - __half2float(a));
+    const __half bl = __float2half_rn(v[2 * t + 1] - __half2float(b));
+    h[t] = (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+    l[t] = (uint32_t)__half_as_ushort(al) | ((uint32_t)__half_as_ushort(bl) << 16);
+  }
+  *(uint2*)(x + i) = make_uint2(h[0], h[1]);
+  *(uint2*)(x + plane + i) = make_uint2(l[0], l[1]);
+}
+
 __device__ __forceinline__ float relu_nan(float z) { return z != z ? z : fmaxf(z, 0.f); }
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -410,6 +410,7 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
         a.f.status_base = r0 * n_cand;
         a.f.prob = prob + r0 * n_cand;
         a.f.xout = plan.X;
+        a.f.xplane = plan.xplane;
         a.f.rout = plan.resid;
         a.f.fout = plan.flags;
         a.f.Kp = plan.Kp;
@@ -442,6 +443,7 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
     a.f.status_base = r0 * n_cand;
     a.f.prob = prob + r0 * n_cand;
     a.f.xout = plan.X;
+    a.f.xplane = plan.xplane;
     a.f.rout = plan.resid;
     a.f.fout = plan.flags;
     a.f.Kp = plan.Kp;

@@ -193,21 +193,20 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
       const double rden = 1.0 / (sqrt(s2 / D) + 1e-6);
       const float m0 = (float)((lr_out - mu) * rden);
       int mbad = !isfinite(m0);
-      float* row = p.xout + e * p.Kp;
       // ctx positions and padding first, then the candidate positions overwrite theirs
       for (int c = lane; c < p.Kp; c += 32) {
         float m = 0.f;
         if (c == 0) m = m0;
         else if (c < D) m = (float)(((double)cpx[c - 1] - mu) * rden);
         mbad |= !isfinite(m);
-        row[c] = m;
+        xstore1(p.xout, p.xplane, e * p.Kp + c, m);
       }
       __syncwarp();
       for (int t = lane; t < Pc; t += 32) {
         const int pos = (int)(ptab[t] >> 16);
         const float m = (float)(((double)xv[t] - mu) * rden);
         mbad |= !isfinite(m);
-        row[1 + pos] = m;
+        xstore1(p.xout, p.xplane, e * p.Kp + 1 + pos, m);
       }
       mbad = __any_sync(0xffffffffu, mbad);
       if (lane == 0) {

@@ -13,6 +13,9 @@
 // trailing partial window gets its own loss slot.  Per-element logs are the
 // CUDA f64 log/log1p (<= 1 ulp from the host libm), so loss sums agree with
 // the reference to ~1e-15 relative, not bitwise.
+#include <mutex>
+#include <unordered_set>
+
 #include "common.cuh"
 
 namespace dffm {
@@ -120,9 +123,21 @@ extern "C" int fw_eval_stream(const double* probs, const uint8_t* labels, int64_
   const int64_t n_full = n / window, n_win = (n + window - 1) / window;
   if (n_full && !auc_out) { set_error("null auc_out"); return DFFM_CONTRACT; }
   const int smem = (window / 2) * 8;
-  // sets the dynamic-smem limit once per (kernel, device): attributes are per context
-  int occ = 0;
-  if (int rc = kernel_occupancy((const void*)eval_window_kernel, EV_THREADS, smem, &occ)) return rc;
+  // the dynamic-smem limit is a per-device (context) attribute: set it once per device
+  {
+    static std::mutex mu;
+    static std::unordered_set<int> done;
+    int dev = 0;
+    DFFM_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.count(dev)) {
+      DFFM_CUDA_TRY(cudaFuncSetAttribute(eval_window_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         max_smem_optin_current() - 1024),
+                    "cudaFuncSetAttribute(eval)");
+      done.insert(dev);
+    }
+  }
   note_launches(1), eval_window_kernel<<<(unsigned)n_win, EV_THREADS, smem, (cudaStream_t)stream>>>(
       probs, labels, n, window, n_full, auc_out, loss_out);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(eval)");

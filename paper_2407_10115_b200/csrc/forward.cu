@@ -133,15 +133,19 @@ static int tc_workspace(cudaStream_t s, size_t bytes, unsigned char** out) {
   return DFFM_OK;
 }
 
-static int rows_tensor_map_x(const float* X, int Kp, int64_t rows, CUtensorMap* tm) {
+// staged rows as two fp16 planes [2][rows][Kp]: 4-D map {8 halfs, rows, Kp/8
+// K cores, 2 planes}; one box {8, 128, 2, 2} lands as the A0 | A1 tiles of a
+// 16-wide chunk in the K-major core-matrix layout of mlp_tc.cu
+static int rows_tensor_map_x(const __half* X, int Kp, int64_t rows, int64_t xplane,
+                             CUtensorMap* tm) {
   auto fn = encode_fn();
   if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return DFFM_CUDA; }
-  cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)Kp * 4};
-  cuuint32_t box[2] = {(cuuint32_t)TC_KC, (cuuint32_t)TC_M};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+  cuuint64_t dims[4] = {8, (cuuint64_t)rows, (cuuint64_t)(Kp / 8), 2};
+  cuuint64_t strides[3] = {(cuuint64_t)Kp * 2, 16, (cuuint64_t)xplane * 2};
+  cuuint32_t box[4] = {8, (cuuint32_t)TC_M, 2, 2};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(X), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled(staged rows) failed (%d)", (int)r);
@@ -194,7 +198,11 @@ bool tc_eligible(const FwdParams& p, int smax) {
     if (w < TC_WIDTH_MULT || w > 256 || w % TC_WIDTH_MULT) return false;  // 16-col blocks per part
     nmax = std::max(nmax, w);
   }
-  return tc_smem_bytes(2, tc_stage_bytes(nmax)) <= smax;
+  // one TMEM accumulation group per layer: layer 0's K (D padded to 16) <= 16 TC_GROUP
+  if (((p.D + 15) & ~15) > 16 * TC_GROUP) return false;
+  int kamax = 0;
+  for (int l = 1; l < NH; ++l) kamax = std::max(kamax, p.dims[l]);
+  return tc_smem_bytes(2, tc_stage_bytes(nmax), TC_M * kamax * 4) <= smax;
 }
 
 int64_t tc_default_slice_rows() {
@@ -215,39 +223,53 @@ int tc_plan(const FwdParams& p, int smax, int64_t slice_rows, cudaStream_t s, Tc
   for (int l = 1; l <= NH; ++l) nmax = std::max(nmax, p.dims[l]);
   q.n_hidden = NH;
   const int Kp = (p.D + 15) & ~15;
-  size_t wfloats = 0;
+  size_t whalfs = 0;
   for (int l = 0; l < NH; ++l) {
     q.kin[l] = l == 0 ? Kp : p.dims[l];
     q.nout[l] = p.dims[l + 1];
-    wfloats += (size_t)q.kin[l] * q.nout[l] * 2;
+    whalfs += (size_t)q.kin[l] * q.nout[l] * 2;
   }
   q.stage_bytes = tc_stage_bytes(nmax);
-  q.stages = TC_MAX_STAGES;
-  while (q.stages > 2 && tc_smem_bytes(q.stages, q.stage_bytes) > smax) --q.stages;
+  static int stages_env = -1;
+  if (stages_env < 0) {
+    const char* v = getenv("DFFM_TC_STAGES");
+    stages_env = v ? std::max(2, std::min(TC_MAX_STAGES, atoi(v))) : TC_MAX_STAGES;
+  }
+  q.stages = stages_env;
+  int kamax = 0;
+  for (int l = 1; l < NH; ++l) kamax = std::max(kamax, q.kin[l]);
+  q.abuf_bytes = TC_M * kamax * 4;
+  while (q.stages > 2 && tc_smem_bytes(q.stages, q.stage_bytes, q.abuf_bytes) > smax) --q.stages;
   int cols = 32;
   while (cols < 2 * nmax) cols <<= 1;
   q.tmem_cols = cols;
-  plan->smem = tc_smem_bytes(q.stages, q.stage_bytes);
+  plan->smem = tc_smem_bytes(q.stages, q.stage_bytes, q.abuf_bytes);
   plan->Kp = Kp;
   plan->slice_rows = slice_rows;
   auto a256 = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  const size_t b_w = a256(wfloats * 4), b_x = a256((size_t)slice_rows * Kp * 4),
+  const size_t b_e = 256, b_w = a256(whalfs * 2), b_x = a256((size_t)slice_rows * Kp * 4),  // 2 fp16 planes
                b_r = a256((size_t)slice_rows * 8), b_f = a256((size_t)slice_rows * 4);
   unsigned char* ws = nullptr;
-  int rc = tc_workspace(s, b_w + b_x + b_r + b_f, &ws);
+  int rc = tc_workspace(s, b_e + b_w + b_x + b_r + b_f, &ws);
   if (rc) return rc;
-  float* wblk = (float*)ws;
-  plan->X = (float*)(ws + b_w);
-  plan->resid = (double*)(ws + b_w + b_x);
-  plan->flags = (int*)(ws + b_w + b_x + b_r);
-  float* wl = wblk;
+  int* wexp = (int*)ws;            // [TC_MAXH] per-layer weight scale exponents
+  int* wmax = wexp + TC_MAXH;      // [TC_MAXH] max |w| scratch
+  __half* wblk = (__half*)(ws + b_e);
+  plan->X = (__half*)(ws + b_e + b_w);
+  plan->xplane = (int64_t)slice_rows * Kp;
+  plan->resid = (double*)(ws + b_e + b_w + b_x);
+  plan->flags = (int*)(ws + b_e + b_w + b_x + b_r);
+  __half* wl = wblk;
   for (int l = 0; l < NH; ++l) {
     const int kreal = l == 0 ? p.D : p.dims[l];
-    if ((rc = launch_tc_prep_weights(p.W[l], kreal, q.nout[l], q.kin[l], wl, s))) return rc;
+    if ((rc = launch_tc_prep_weights(p.W[l], kreal, q.nout[l], q.kin[l], wl, wmax + l, wexp + l,
+                                     s)))
+      return rc;
     q.wblk[l] = wl;
     q.bias[l] = p.b[l];
     wl += (size_t)q.kin[l] * q.nout[l] * 2;
   }
+  q.wexp = wexp;
   q.w_out = p.W[NH];
   q.b_out = p.b[NH];
   q.resid = plan->resid;
@@ -259,7 +281,7 @@ int tc_plan(const FwdParams& p, int smax, int64_t slice_rows, cudaStream_t s, Tc
 int tc_mlp_slice(TcPlan& plan, int64_t rows, int64_t status_base, float* prob, float* logit,
                  cudaStream_t s) {
   CUtensorMap tm;
-  int rc = rows_tensor_map_x(plan.X, plan.Kp, rows, &tm);
+  int rc = rows_tensor_map_x(plan.X, plan.Kp, rows, plan.xplane, &tm);
   if (rc) return rc;
   plan.q.rows = rows;
   plan.q.status_base = status_base;
@@ -302,6 +324,7 @@ static bool try_tc_forward(const dffm_model* m, FwdParams& p, int smax, cudaStre
     a.prob = p.prob + s0;
     a.logit = nullptr;
     a.xout = plan.X;
+    a.xplane = plan.xplane;
     a.rout = plan.resid;
     a.fout = plan.flags;
     a.Kp = plan.Kp;

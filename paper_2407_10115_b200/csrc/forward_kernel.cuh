@@ -53,9 +53,10 @@ struct FwdParams {
   Deq dlr, dffm;
   // staging mode (tensor-core MLP, mlp_tc.cu): when xout is set the MLP warps
   // do not run the MLP; they write each example's MergeNorm row to
-  // xout[e][0..Kp) (zero padded), lr_out + sum(pairs) to rout[e] and the
-  // non-finite stage bits to fout[e]
-  float* xout;
+  // xout[e][0..Kp) as fp16 hi / lo planes (xstore*, zero padded), lr_out +
+  // sum(pairs) to rout[e] and the non-finite stage bits to fout[e]
+  __half* xout;
+  int64_t xplane;  // halfs between the hi and the lo plane
   double* rout;
   int* fout;
   int Kp;
@@ -273,8 +274,8 @@ __device__ __forceinline__ void mlp_tile(const FwdParams& p, float* X, float* Ha
   if (p.xout) {  // staging mode (mlp_tc.cu): rows, residuals, stage bits; row index = out_base + el
     for (int el = warp; el < nvalid; el += FWD_WARPS) {
       const int64_t e = out_base + el;
-      float* row = p.xout + e * p.Kp;
-      for (int i = lane; i < p.Kp; i += 32) row[i] = i < p.D ? X[i * XS + el] : 0.f;
+      for (int i = lane; i < p.Kp; i += 32)
+        xstore1(p.xout, p.xplane, e * p.Kp + i, i < p.D ? X[i * XS + el] : 0.f);
       if (lane == 0) {
         p.rout[e] = exd[el] + exd[TE + el];
         p.fout[e] = flag[el];
@@ -489,8 +490,8 @@ __device__ __forceinline__ void mlp_warps_tile(const FwdParams& p, const float* 
     for (int el = mw; el < TE; el += NM) {
       const int64_t e = base + el;
       if (e >= p.n) continue;
-      float* row = p.xout + e * p.Kp;
-      for (int i = lane; i < p.Kp; i += 32) row[i] = i < p.D ? xin[i * XS + el] : 0.f;
+      for (int i = lane; i < p.Kp; i += 32)
+        xstore1(p.xout, p.xplane, e * p.Kp + i, i < p.D ? xin[i * XS + el] : 0.f);
       if (lane == 0) {
         p.rout[e] = exd[el] + exd[TE + el];
         p.fout[e] = flag[el];

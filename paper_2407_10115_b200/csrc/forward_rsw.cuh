@@ -190,7 +190,6 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       const double rden = 1.0 / denom;  // one f64 division per example
       const float m0 = (float)((lr_out - mu) * rden);
       int mbad = 0;
-      float4* row = (float4*)(p.xout + e * p.Kp);
       for (int q = lane; q < (p.Kp >> 2); q += 32) {
         float v[4];
 #pragma unroll
@@ -202,7 +201,7 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
           mbad |= !isfinite(m);
           v[t] = m;
         }
-        row[q] = make_float4(v[0], v[1], v[2], v[3]);
+        xstore4(p.xout, p.xplane, e * p.Kp + 4 * q, v);
       }
       mbad = __any_sync(0xffffffffu, mbad);
       if (lane == 0) {

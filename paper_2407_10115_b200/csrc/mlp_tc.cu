@@ -1,36 +1,57 @@
 // K1 MLP stage on tcgen05 tensor cores (M:362-377 for a slice of examples whose
 // MergeNorm rows the gather kernel staged in HBM/L2; see forward.cu).
 //
+// Precision: every f32 operand is split into two fp16 pieces and the products
+// run as kind::f16 MMAs with f32 accumulation (twice the tensor rate of tf32
+// and half its operand bytes):
+//     x = x0 + x1     x0 = fp16(x),  x1 = fp16(x - x0)      (22 significant bits)
+//     x.w ~= x0.w0 + x0.w1 + x1.w0                           (x1.w1 ~ 2^-22 x.w dropped)
+// so one K=16 chunk is three MMAs into the same accumulator.  fp16's exponent
+// range is narrow, so each layer's weights and each example row of hidden
+// activations are scaled by a power of two (exact) that puts their maximum in
+// [2^14, 2^15): nothing overflows and the residual pieces stay normal.  The
+// epilogue undoes both scales exactly.  Non-finite values stay non-finite
+// (NaN/inf propagate), as the diagnosis of M:308-318 needs.
+//
 // One persistent CTA per SM walks tiles of 128 examples.  For each hidden
 // layer l the tile's pre-activations Z_l[128 x N_l] accumulate in TMEM (f32,
 // one lane per example) as a K-loop of 16-wide chunks through a ring of
 // shared-memory stages:
-//   warp 0     TMA producer: layer 0's A chunk (X rows, 2-D tensor map, 64-B
-//              swizzle) and every layer's W chunk (pre-blocked hi/lo, 1-D bulk)
-//   warp 1     MMA issuer (one thread): per 8-wide K step three
-//              tcgen05.mma.kind::tf32 -- A_hi*W_hi + A_hi*W_lo + A_lo*W_hi
-//              (3xTF32: ~fp32 accuracy from the TF32 tensor cores; the
-//              tensor core truncates f32 operands to tf32, so A_hi is the raw
-//              f32 and A_lo = x - trunc_tf32(x))
-//   warps 2-9  (two per TMEM lane quadrant, each owning half of a layer's
-//              columns) layer 0: A_lo for each landed X chunk; every layer:
-//              drain each accumulation group from TMEM into f32 register sums
-//              (see below), then +bias, ReLU (NaN kept, M:370) -> the next
-//              layer's hi/lo A chunks straight from registers; last: output
-//              column dot product (halves meet in shared memory), residual
-//              logit (M:377), clamped sigmoid (M:304-305), status.
-// All operand layouts are the canonical K-major core-matrix layouts
-// (validated by tools/tc_probe.cu).
+//   warp 0     TMA producer: layer 0's A tiles (one 4-D TMA of the staged hi /
+//              lo planes the gather kernel wrote, xstore4) and every layer's
+//              blocked fp16 W chunk (1-D bulk copy)
+//   warp 1     MMA issuer (one thread): three tcgen05.mma.kind::f16 per chunk
+//   epilogue   (four column parts per TMEM lane quadrant) drain each
+//              accumulation group from TMEM into IEEE f32 register sums, then
+//              unscale, +bias, ReLU (NaN kept, M:370) -> the next layer's fp16
+//              A tiles straight from registers; last: output column dot
+//              product (parts meet in shared memory), residual logit (M:377),
+//              clamped sigmoid (M:304-305), status.
+// Operand layouts are the canonical no-swizzle K-major core-matrix layouts
+// (8 rows x 16 bytes per core matrix; LBO = K-direction core stride, SBO =
+// 8-row group stride), as validated for tf32 by tools/tc_probe.cu.
 #include "mlp_tc.cuh"
 
 namespace dffm {
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1,
-                                            uint64_t* bar) {
+#ifdef DFFM_TC_TRACE  // measurement variant: MMA-issuer timeline of CTA 0
+constexpr int TCT_N = 4096;
+__device__ long long g_tct[TCT_N];
+__device__ int g_tct_n;
+#define TCT(tag) do { if (blockIdx.x == 0) { int i_ = atomicAdd(&g_tct_n, 1); if (i_ < TCT_N) \
+    g_tct[i_] = (clock64() << 8) | (tag); } } while (0)
+#define TCE(tag) do { if (threadIdx.x == 64) TCT(tag); } while (0)
+#else
+#define TCT(tag) do { } while (0)
+#define TCE(tag) do { } while (0)
+#endif
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int c1,
+                                            int c2, int c3, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -44,25 +65,22 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// shared-memory matrix descriptor (sm_100 version bit 46; base offset 0)
-__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
-                                              uint32_t layout) {
+// shared-memory matrix descriptor (sm_100 version bit 46; base offset 0, no swizzle)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) |
-         ((uint64_t)layout << 61);
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
 
-// instruction descriptor: D f32, A/B tf32, both K-major, M x N
-__device__ __forceinline__ uint32_t idesc_tf32(int m, int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(m >> 4) << 24);
+// instruction descriptor: D f32, A/B f16, both K-major, M x N
+__device__ __forceinline__ uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t id,
-                                         uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t id,
+                                        uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
@@ -88,47 +106,45 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
-__device__ __forceinline__ float tf32_lo(float x) {
-  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+__device__ __forceinline__ float pow2f(int e) {  // 2^e, e in [-126, 127]
+  return __int_as_float((127 + e) << 23);
 }
 
-// Accumulation precision: the tensor core's f32 accumulation is coarser than
-// IEEE round-to-nearest (tools/tc_accuracy.cu: one accumulator over K=784 at
-// cfg5 scale errs 2.5e-5 x rms vs 3.7e-6 for a sequential fp32 FMA chain), so
-// each layer's K-loop is cut into groups of TC_GROUP chunks: a group
-// accumulates in one TMEM region (regions alternate), and the epilogue drains
-// it into IEEE f32 register sums while the MMAs run the next group.
-
-// one thread's part of a row of accumulators, statically indexed (registers)
-struct HalfRow {
-  float v[TC_PART_MAX];
-};
-
-__device__ __forceinline__ void drain_group(HalfRow& acc, uint32_t taddr, int nblk, bool first) {
-#pragma unroll
-  for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
-    if (cb < nblk) {
-      float v[16];
-      tmem_ld16(taddr + (uint32_t)cb * 16, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc.v[cb * 16 + j] = first ? v[j] : acc.v[cb * 16 + j] + v[j];
-    }
-  }
+// fp16 pieces (hi, lo) of 2 consecutive values, packed in pairs (paired cvts)
+__device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x, y);
+  const float2 b = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x - b.x, y - b.y);
+  hi = *(const uint32_t*)&h;
+  lo = *(const uint32_t*)&l;
 }
 
-// drain accumulation group #dg (region dg & 1) into this thread's half-row
-__device__ __forceinline__ void epi_drain(HalfRow& acc, uint64_t* accf, uint64_t* tempty,
-                                          uint32_t& dg, uint32_t lane_base, uint32_t RS,
-                                          int col0, int nblk, bool first, int lane) {
-  const uint32_t reg = dg & 1;
-  mbar_wait(&accf[reg], (dg >> 1) & 1);
-  tc_fence_after();
-  drain_group(acc, lane_base + reg * RS + (uint32_t)col0, nblk, first);
-  tc_fence_before();
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&tempty[reg]);
-  ++dg;
+// write 8 consecutive K values (one core-matrix row) of example row r into the
+// two A tiles of a stage; kc = K core (0 or 1) within the 16-wide chunk
+__device__ __forceinline__ void write_a8(unsigned char* st, int r, int kc, const float* a,
+                                         float scale) {
+  const int off = TC_OFF_A + (kc * 16 + (r >> 3)) * 128 + (r & 7) * 16;
+  uint4 u0, u1;
+  split2(a[0] * scale, a[1] * scale, u0.x, u1.x);
+  split2(a[2] * scale, a[3] * scale, u0.y, u1.y);
+  split2(a[4] * scale, a[5] * scale, u0.z, u1.z);
+  split2(a[6] * scale, a[7] * scale, u0.w, u1.w);
+  *(uint4*)(st + off) = u0;
+  *(uint4*)(st + off + 4096) = u1;
 }
+
+// power-of-two exponent putting a maximum magnitude m in [2^14, 2^15)
+__device__ __forceinline__ int range_exp(float m) {
+  return m > 0.f ? max(-100, min(100, TC_HEXP - ilogbf(m))) : 0;
+}
+
+// Accumulation: each layer accumulates in one TMEM region (regions alternate
+// per layer, so the MMAs of the next layer or tile run while the epilogue
+// reads the previous accumulator).  The tensor core's f32 accumulation is
+// coarser than IEEE round-to-nearest (tools/tc_accuracy.cu); with the fp16
+// pieces a whole cfg5 layer 0 (49 chunks) stays at 3e-6 relative error on the
+// probabilities against the 1e-5 contract, so layers are one group of at most
+// TC_GROUP chunks (the host checks kin <= 16 * TC_GROUP).
 
 // first 16-column block of part h of an N-wide layer (N % 16 == 0): the
 // N/16 blocks are dealt to the TC_PARTS parts as evenly as possible
@@ -139,24 +155,25 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages, SB = p.stage_bytes, NH = p.n_hidden;
-  uint64_t* full = (uint64_t*)(smem + S * SB);
-  uint64_t* aready = full + S;
-  uint64_t* empty = aready + S;
-  uint64_t* lready = empty + S;  // [S] split warps: the stage's A_lo is written (every chunk)
-  uint64_t* accf = lready + S;   // [2] TMEM region holds a finished group
+  unsigned char* abuf = smem + S * SB;  // hidden layers' A operands, chunk c at c * 8 KB
+  uint64_t* full = (uint64_t*)(abuf + p.abuf_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* abar = empty + S;    // [1] the epilogue wrote the next layer's A buffer
+  uint64_t* accf = abar + 2;     // [2] TMEM region holds a finished group
   uint64_t* tempty = accf + 2;   // [2] TMEM region drained by the epilogue
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  float* xpart = (float*)(smem + S * SB + (4 * S + 4) * 8 + 16);  // [2][TC_PARTS][TC_M]
+  float* xpart = (float*)((unsigned char*)full + (2 * S + 6) * 8 + 16);  // [2][TC_PARTS][TC_M]
   int* xbad = (int*)(xpart + 2 * TC_PARTS * TC_M);                 // [2][TC_PARTS][TC_M]
+  int* xexp = xbad + 2 * TC_PARTS * TC_M;                          // [2][TC_PARTS][TC_M]
+  float* cst = (float*)(xexp + 2 * TC_PARTS * TC_M);  // biases | w_out | b_out | 2^-wexp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&aready[s], TC_EPI_WARPS);
       mbar_init(&empty[s], 1);
-      mbar_init(&lready[s], TC_SPLIT_WARPS);
     }
+    mbar_init(abar, TC_EPI_WARPS);
     for (int r = 0; r < 2; ++r) {
       mbar_init(&accf[r], 1);
       mbar_init(&tempty[r], TC_EPI_WARPS);
@@ -169,6 +186,13 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
                  "r"(p.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // stage the constants the epilogue reads for every tile (layer l's bias at
+  // offset 256 l, w_out at 1024, b_out at 1280, 2^-wexp[l] at 1281 + l)
+  for (int l = 0; l < NH; ++l)
+    for (int i = threadIdx.x; i < p.nout[l]; i += blockDim.x) cst[256 * l + i] = p.bias[l][i];
+  for (int i = threadIdx.x; i < p.nout[NH - 1]; i += blockDim.x) cst[1024 + i] = p.w_out[i];
+  if (threadIdx.x == 0) cst[1280] = *p.b_out;
+  if (threadIdx.x < NH) cst[1281 + threadIdx.x] = pow2f(-p.wexp[threadIdx.x]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -186,15 +210,16 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int l = 0; l < NH; ++l) {
           const int nck = p.kin[l] >> 4;
-          const uint32_t wbytes = (uint32_t)p.nout[l] * 128u;
+          const uint32_t wbytes = (uint32_t)p.nout[l] * 64u;
           for (int c = 0; c < nck; ++c, ++g) {
             const int s = (int)(g % S);
             const uint32_t u = g / S;
             if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
             unsigned char* st = smem + s * SB;
             mbar_arrive_expect_tx(&full[s], wbytes + (l == 0 ? 8192u : 0u));
-            if (l == 0) tma_load_2d(st, &tmx, c * TC_KC, (int)(tile_row(t) * TC_M), &full[s]);
-            tma_load_1d(st + 16384, p.wblk[l] + (size_t)c * p.nout[l] * 32, wbytes, &full[s]);
+            if (l == 0)  // {8 halfs, 128 rows, 2 K cores, 2 planes} -> A0 | A1
+              tma_load_4d(st + TC_OFF_A, &tmx, 0, (int)(tile_row(t) * TC_M), 2 * c, 0, &full[s]);
+            tma_load_1d(st + TC_OFF_B, p.wblk[l] + (size_t)c * p.nout[l] * 32, wbytes, &full[s]);
           }
         }
       }
@@ -203,13 +228,17 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       uint32_t g = 0, gg = 0;  // chunk counter, accumulation-group counter
-      uint32_t apar = 0;       // per-stage phase bits of aready (used by layer >= 1 chunks only)
+      uint32_t abph = 0;       // phase of abar (one completion per tile and layer >= 1)
       uint32_t d = tmem;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int l = 0; l < NH; ++l) {
           const int nck = p.kin[l] >> 4, N = p.nout[l];
-          const uint32_t id = idesc_tf32(TC_M, N);
+          const uint32_t id = idesc_f16(TC_M, N);
           const uint32_t lboW = (uint32_t)(N >> 3) * 128u;
+          if (l > 0) {  // the epilogue filled this layer's A buffer in one burst
+            mbar_wait(abar, abph);
+            abph ^= 1u;
+          }
           for (int c = 0; c < nck; ++c, ++g) {
             const int cg = c % TC_GROUP;
             if (cg == 0) {  // a new group: its region must have been drained
@@ -219,32 +248,21 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
             }
             const int s = (int)(g % S);
             const uint32_t u = g / S;
-            if (l > 0) {  // A chunk written by the epilogue from the previous layer
-              mbar_wait(&aready[s], (apar >> s) & 1u);
-              apar ^= 1u << s;
-            }
-            mbar_wait(&lready[s], u & 1);
+            if (c == 0) TCT(l * 2);
             mbar_wait(&full[s], u & 1);
+            if (c == 0) TCT(l * 2 + 1);
             tc_fence_after();
             const uint32_t st = smem_u32(smem + s * SB);
-            const uint32_t whi = st + 16384, wlo = whi + (uint32_t)N * 64u;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              uint64_t ahi, alo;
-              if (l == 0) {  // TMA tile: 128 rows x 64 B, 64-byte swizzle
-                ahi = umma_desc(st + ks * 32, 16, 512, 4);
-                alo = umma_desc(st + 8192 + ks * 32, 16, 512, 4);
-              } else {       // epilogue-written: core-matrix blocked, no swizzle
-                ahi = umma_desc(st + ks * 4096, 2048, 128, 0);
-                alo = umma_desc(st + 8192 + ks * 4096, 2048, 128, 0);
-              }
-              const uint64_t bhi = umma_desc(whi + ks * 2 * lboW, lboW, 128, 0);
-              const uint64_t blo = umma_desc(wlo + ks * 2 * lboW, lboW, 128, 0);
-              mma_tf32(d, ahi, bhi, id, (cg | ks) != 0);
-              mma_tf32(d, ahi, blo, id, 1);
-              mma_tf32(d, alo, bhi, id, 1);
-            }
+            const uint32_t at = l == 0 ? st + TC_OFF_A : smem_u32(abuf) + (uint32_t)c * 8192u;
+            const uint64_t a0 = umma_desc(at, 2048, 128);
+            const uint64_t a1 = umma_desc(at + 4096, 2048, 128);
+            const uint64_t b0 = umma_desc(st + TC_OFF_B, lboW, 128);
+            const uint64_t b1 = umma_desc(st + TC_OFF_B + (uint32_t)N * 32u, lboW, 128);
+            mma_f16(d, a0, b0, id, cg != 0);
+            mma_f16(d, a0, b1, id, 1);
+            mma_f16(d, a1, b0, id, 1);
             mma_commit(&empty[s]);  // stage reusable once these MMAs finish
+            if (c == nck - 1) TCT(16 + l);
             if (cg == TC_GROUP - 1 || c == nck - 1) {
               mma_commit(&accf[gg & 1]);  // group complete in its region
               ++gg;
@@ -253,114 +271,93 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
         }
       }
     }
-  } else if (warp >= 2 + TC_EPI_WARPS) {
-    // ------------------------------------------------------------ split warps
-    // A_lo = x - trunc_tf32(x) of each landed layer-0 X chunk (same swizzled
-    // positions), off the epilogue warps so accumulator drains never hold
-    // the MMAs back; they walk every chunk in order and arrive on lready[s]
-    // for each (layer >= 1 chunks: nothing to split), which keeps the
-    // mbarrier phases of full/lready in lock step with the MMA issuer.
-    const int sw = warp - 2 - TC_EPI_WARPS;
-    uint32_t g = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      for (int l = 0; l < NH; ++l) {
-        const int nck = p.kin[l] >> 4;
-        for (int c = 0; c < nck; ++c, ++g) {
-          const int s = (int)(g % S);
-          mbar_wait(&full[s], (g / S) & 1);
-          if (l == 0) {
-            unsigned char* st = smem + s * SB;
-            const float4* a = (const float4*)st;
-            float4* lo = (float4*)(st + 8192);
-#pragma unroll
-            for (int i = sw * 32 + lane; i < 512; i += 32 * TC_SPLIT_WARPS) {
-              const float4 x = a[i];
-              lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
-            }
-            fence_async_smem();
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&lready[s]);
-        }
-      }
-    }
   } else {
     // ------------------------------------------------------------ epilogue warps
+    // One accumulation group per layer (nck <= TC_GROUP, checked on the host):
+    // each layer's accumulator is read from TMEM in 16-column blocks, twice
+    // for hidden->hidden layers (pass 1: the row's maximum for its power-of-
+    // two scale; pass 2: the scaled fp16 A pieces of the next layer), so only
+    // one block is live in registers at a time.
     const int ew = warp - 2;               // 0 .. TC_EPI_WARPS-1
     const int h = ew >> 2;                 // column part owned by this warp
     const int q = warp & 3;                // TMEM lane quadrant this warp may access
     const int r = q * 32 + lane;           // tile row = example of this thread
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    uint32_t g = 0, dg = 0;                // chunk counter, drained-group counter
-    HalfRow acc;
+    uint32_t dg = 0;                       // drained-group counter
     int tl = 0;                            // local tile counter (exchange buffer parity)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
       int nn_bad = 0;
+      int row_e = 0;                       // power-of-two scale of this row's layer input
+      float part = 0.f;                    // this part's share of the output dot (M:372)
       for (int l = 0; l < NH; ++l) {
-        const int nck = p.kin[l] >> 4, N = p.nout[l];
-        // this part's 16-column blocks [b0, b1) of layer l (parts may be empty
-        // when N < 64) and of the previous layer (ownership of its A chunks)
-        const int b0 = part_blk(h, N), hc = (part_blk(h + 1, N) - b0) * 16;
-        const int ngr = (nck + TC_GROUP - 1) / TC_GROUP;
-        const int pb0 = l > 0 ? part_blk(h, p.nout[l - 1]) : 0;
-        const int pb1 = l > 0 ? part_blk(h + 1, p.nout[l - 1]) : 0;
-        for (int gi = 0; gi < ngr; ++gi) {
-          const int cend = min(nck, (gi + 1) * TC_GROUP);
-          for (int c = gi * TC_GROUP; c < cend; ++c, ++g) {
-            if (l == 0) continue;  // layer 0's A (hi: TMA, lo: split warps)
-            const int s = (int)(g % S);
-            mbar_wait(&full[s], (g / S) & 1);  // stage free again (W landed)
-            unsigned char* st = smem + s * SB;
-            if (c >= pb0 && c < pb1) {  // this part holds the chunk's 16 columns
-              const int cbl = c - pb0;
-#pragma unroll
-              for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
-                if (cb == cbl) {
-#pragma unroll
-                  for (int kq = 0; kq < 4; ++kq) {
-                    const float* a4 = acc.v + cb * 16 + kq * 4;
-                    const int off = ((kq * 16 + (r >> 3)) * 128) + (r & 7) * 16;
-                    *(float4*)(st + off) = make_float4(a4[0], a4[1], a4[2], a4[3]);
-                    *(float4*)(st + 8192 + off) =
-                        make_float4(tf32_lo(a4[0]), tf32_lo(a4[1]), tf32_lo(a4[2]), tf32_lo(a4[3]));
-                  }
-                }
-              }
-            }
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&aready[s]);
-          }
-          if (gi > 0)  // one group behind the MMAs
-            epi_drain(acc, accf, tempty, dg, lane_base, RS, b0 * 16, hc >> 4, gi == 1, lane);
-        }
-        epi_drain(acc, accf, tempty, dg, lane_base, RS, b0 * 16, hc >> 4, ngr == 1, lane);
-        // acc = this part's pre-activations of layer l: + bias, ReLU (M:368-370)
-        const float* __restrict__ bl = p.bias[l] + b0 * 16;
-#pragma unroll
-        for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
-          if (cb < (hc >> 4)) {
+        const int N = p.nout[l];
+        // this part's 16-column blocks [b0, b0 + nb) of layer l (parts may be
+        // empty when N < 64); they are also the K chunks of layer l + 1 that
+        // this part writes into abuf
+        const int b0 = part_blk(h, N), nb = part_blk(h + 1, N) - b0;
+        const uint32_t reg = dg & 1;
+        mbar_wait(&accf[reg], (dg >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ta = lane_base + reg * RS + (uint32_t)(b0 * 16);
+        // acc * 2^-(weight scale) * 2^-(row scale) = pre-activations (M:368)
+        const float zs = cst[1281 + l] * pow2f(-row_e);
+        const float* bl = cst + 256 * l + b0 * 16;
+        if (l + 1 < NH) {
+          float amax = 0.f;
+          for (int cb = 0; cb < nb; ++cb) {  // pass 1: ReLU (M:370) maxima
+            float v[16];
+            tmem_ld16(ta + (uint32_t)cb * 16, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float z = acc.v[cb * 16 + j] + __ldg(bl + cb * 16 + j);
+              const float z = v[j] * zs + bl[cb * 16 + j];
               nn_bad |= !isfinite(z);
-              acc.v[cb * 16 + j] = relu_nan(z);
+              const float a = relu_nan(z);
+              if (a < 3.0e38f) amax = fmaxf(amax, a);  // finite maximum (NaN compares false)
+            }
+          }
+          int* xe = xexp + (l & 1) * TC_PARTS * TC_M;
+          xe[h * TC_M + r] = __float_as_int(amax);  // non-negative: int order = float order
+          named_bar_sync(2, 32 * TC_EPI_WARPS);
+          int mb = 0;
+#pragma unroll
+          for (int k2 = 0; k2 < TC_PARTS; ++k2) mb = max(mb, xe[k2 * TC_M + r]);
+          const int e_next = range_exp(__int_as_float(mb));
+          const float a_scale = pow2f(e_next);
+          for (int cb = 0; cb < nb; ++cb) {  // pass 2: layer l + 1's A chunks (abuf)
+            float v[16];
+            tmem_ld16(ta + (uint32_t)cb * 16, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = relu_nan(v[j] * zs + bl[cb * 16 + j]);
+            // the MMAs of layer l, abuf's previous readers, completed before
+            // its accumulator could be read
+            unsigned char* at = abuf + (size_t)(b0 + cb) * 8192 - TC_OFF_A;
+            write_a8(at, r, 0, v, a_scale);
+            write_a8(at, r, 1, v + 8, a_scale);
+          }
+          row_e = e_next;
+          fence_async_smem();
+        } else {
+          const float* wo = cst + 1024 + b0 * 16;
+          for (int cb = 0; cb < nb; ++cb) {  // last hidden layer: straight into the dot
+            float v[16];
+            tmem_ld16(ta + (uint32_t)cb * 16, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float z = v[j] * zs + bl[cb * 16 + j];
+              nn_bad |= !isfinite(z);
+              part = fmaf(relu_nan(z), wo[cb * 16 + j], part);
             }
           }
         }
-      }
-      // ---- output layer (M:372-373): the parts' partial dots meet in shared memory
-      const int lb0 = part_blk(h, p.nout[NH - 1]);
-      const int hcl = (part_blk(h + 1, p.nout[NH - 1]) - lb0) * 16;
-      const float* __restrict__ wo = p.w_out + lb0 * 16;
-      float part = 0.f;
-#pragma unroll
-      for (int cb = 0; cb < TC_PART_MAX / 16; ++cb) {
-        if (cb < (hcl >> 4)) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) part = fmaf(acc.v[cb * 16 + j], __ldg(wo + cb * 16 + j), part);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&tempty[reg]);
+          if (l + 1 < NH) mbar_arrive(abar);
         }
+        ++dg;
       }
+      // ---- output (M:372-373): the parts' partial dots meet in shared memory
       float* xp = xpart + (tl & 1) * TC_PARTS * TC_M;
       int* xb = xbad + (tl & 1) * TC_PARTS * TC_M;
       if (h > 0) { xp[h * TC_M + r] = part; xb[h * TC_M + r] = nn_bad; }
@@ -373,7 +370,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
           acc_nn += xp[k2 * TC_M + r];
           nn_bad |= xb[k2 * TC_M + r];
         }
-        const double nn = (double)acc_nn + (double)__ldg(p.b_out);
+        const double nn = (double)acc_nn + (double)cst[1280];
         const double logit = nn + p.resid[e];  // M:377
         p.prob[e] = (float)sigmoid_clamped(logit);
         if (p.logit) p.logit[e] = (float)logit;
@@ -398,31 +395,56 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   }
 }
 
-// W [K][N] f32 row-major (M:198-210) -> kin/16 chunks, each [hi N x 16][lo N x 16]
-// in the K-major core-matrix layout the B descriptor expects (rows = outputs).
-// hi = tf32 round-to-nearest of w, lo = w - hi (exact in f32).
+// max |w| over the finite weights of one layer (bit pattern of a non-negative
+// float: integer order = float order) -> *wmax (zeroed by the host first)
+__global__ void tc_wmax_kernel(const float* __restrict__ W, int64_t n, int* wmax) {
+  int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float a = fabsf(W[i]);
+    if (a < 3.0e38f) m = max(m, __float_as_int(a));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(wmax, m);
+}
+
+// W [K][N] f32 row-major (M:198-210) -> kin/16 chunks, each [B0 N x 16][B1 N x 16]
+// fp16 in the K-major core-matrix layout the B descriptor expects (rows =
+// outputs, 8 K values = 16 bytes per core-matrix row).  The layer is scaled
+// by 2^e, e = range_exp(max |w|), so the pieces fit fp16 and the residuals
+// stay normal; *wexp = e.
 __global__ void tc_prep_weights_kernel(const float* __restrict__ W, int K, int N, int Kp,
-                                       float* __restrict__ dst) {
+                                       const int* __restrict__ wmax, __half* __restrict__ dst,
+                                       int* __restrict__ wexp) {
+  const int e = range_exp(__int_as_float(*wmax));
+  const float sc = pow2f(e);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *wexp = e;
   const int64_t total = (int64_t)Kp * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(i / N), n = (int)(i - (int64_t)k * N);
-    const float w = k < K ? W[(int64_t)k * N + n] : 0.f;
-    uint32_t hb;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(w));
-    const float hi = __uint_as_float(hb);
+    const float w = k < K ? W[(int64_t)k * N + n] * sc : 0.f;
+    const __half w0 = __float2half_rn(w);
+    const __half w1 = __float2half_rn(w - __half2float(w0));
     const int c = k >> 4, kk = k & 15;
-    float* chunk = dst + (int64_t)c * N * 32;
-    const int off = (((kk >> 2) * (N >> 3) + (n >> 3)) * 32) + (n & 7) * 4 + (kk & 3);
-    chunk[off] = hi;
-    chunk[N * 16 + off] = w - hi;
+    __half* chunk = dst + (int64_t)c * N * 32;
+    const int off = (((kk >> 3) * (N >> 3) + (n >> 3)) * 64) + (n & 7) * 8 + (kk & 7);
+    chunk[off] = w0;
+    chunk[N * 16 + off] = w1;
   }
 }
 
-int launch_tc_prep_weights(const float* W, int K, int N, int Kp, float* dst, cudaStream_t s) {
+int launch_tc_prep_weights(const float* W, int K, int N, int Kp, __half* dst, int* wmax,
+                           int* wexp, cudaStream_t s) {
   const int64_t total = (int64_t)Kp * N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
-  note_launches(1), tc_prep_weights_kernel<<<blocks, 256, 0, s>>>(W, K, N, Kp, dst);
+  DFFM_CUDA_TRY(cudaMemsetAsync(wmax, 0, sizeof(int), s), "memset(wmax)");
+  const int64_t nw = (int64_t)K * N;
+  note_launches(1), tc_wmax_kernel<<<(int)std::min<int64_t>((nw + 255) / 256, 1024), 256, 0, s>>>(
+                        W, nw, wmax);
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(tc_wmax)");
+  note_launches(1), tc_prep_weights_kernel<<<blocks, 256, 0, s>>>(W, K, N, Kp, wmax, dst, wexp);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(tc_prep_weights)");
   return DFFM_OK;
 }
@@ -439,3 +461,16 @@ int launch_mlp_tc(const CUtensorMap& tmx, const MlpTcParams& p, int smem, cudaSt
 }
 
 }  // namespace dffm
+
+#ifdef DFFM_TC_TRACE
+extern "C" int dffm_debug_tc_trace(long long* out, int n) {
+  int cnt = 0;
+  cudaMemcpyFromSymbol(&cnt, dffm::g_tct_n, sizeof(int));
+  cnt = cnt < n ? cnt : n;
+  if (cnt > dffm::TCT_N) cnt = dffm::TCT_N;
+  cudaMemcpyFromSymbol(out, dffm::g_tct, sizeof(long long) * cnt);
+  int z = 0;
+  cudaMemcpyToSymbol(dffm::g_tct_n, &z, sizeof(int));
+  return cnt;
+}
+#endif

@@ -402,6 +402,7 @@ def api_fixture():
     st = ref_store(F, k, hidden, bits, flat)
     rep = rt.train_stream(iter(text), st, schema)
     ts_final = st.flat.copy()
+    ts_version = st.version
     # hogwild_train with one worker (byte-identical to sequential, T:1-11)
     st = ref_store(F, k, hidden, bits, flat)
     hrep = rt.hogwild_train(iter(text), st, schema, rt.TrainOptions(n_threads=1))
@@ -420,7 +421,7 @@ def api_fixture():
                         loop_final=loop_final, loop_version=loop_version,
                         ts_seen=rep.examples_seen, ts_parse_errors=rep.parse_errors,
                         ts_logloss=rep.progressive_logloss, ts_series=series,
-                        ts_final=ts_final, ts_version=st.version,
+                        ts_final=ts_final, ts_version=ts_version,
                         hw_seen=hrep.examples_seen, hw_parse_errors=hrep.parse_errors,
                         hw_logloss=hrep.progressive_logloss, hw_final=hw_final,
                         hw_series=np.array([(i, np.nan if a is None else a)
