@@ -200,9 +200,7 @@ bool tc_eligible(const FwdParams& p, int smax) {
   }
   // one TMEM accumulation group per layer: layer 0's K (D padded to 16) <= 16 TC_GROUP
   if (((p.D + 15) & ~15) > 16 * TC_GROUP) return false;
-  int kamax = 0;
-  for (int l = 1; l < NH; ++l) kamax = std::max(kamax, p.dims[l]);
-  return tc_smem_bytes(2, tc_stage_bytes(nmax), TC_M * kamax * 4) <= smax;
+  return tc_smem_bytes(2, tc_stage_bytes(nmax)) <= smax;
 }
 
 int64_t tc_default_slice_rows() {
@@ -236,14 +234,11 @@ int tc_plan(const FwdParams& p, int smax, int64_t slice_rows, cudaStream_t s, Tc
     stages_env = v ? std::max(2, std::min(TC_MAX_STAGES, atoi(v))) : TC_MAX_STAGES;
   }
   q.stages = stages_env;
-  int kamax = 0;
-  for (int l = 1; l < NH; ++l) kamax = std::max(kamax, q.kin[l]);
-  q.abuf_bytes = TC_M * kamax * 4;
-  while (q.stages > 2 && tc_smem_bytes(q.stages, q.stage_bytes, q.abuf_bytes) > smax) --q.stages;
+  while (q.stages > 2 && tc_smem_bytes(q.stages, q.stage_bytes) > smax) --q.stages;
   int cols = 32;
   while (cols < 2 * nmax) cols <<= 1;
   q.tmem_cols = cols;
-  plan->smem = tc_smem_bytes(q.stages, q.stage_bytes, q.abuf_bytes);
+  plan->smem = tc_smem_bytes(q.stages, q.stage_bytes);
   plan->Kp = Kp;
   plan->slice_rows = slice_rows;
   auto a256 = [](size_t b) { return (b + 255) & ~(size_t)255; };

@@ -107,7 +107,13 @@ int launch_forward_rsw_t(const FwdParams& p, const RswSmem& L, int K, cudaStream
   int occ = 0;
   int rc = kernel_occupancy((const void*)kern, RSW_THREADS, L.total, &occ);
   if (rc) return rc;
-  const int64_t grid = std::min<int64_t>(p.n, (int64_t)sm_count_current());
+  static int grid_env = -1;  // DFFM_RSW_GRID: SMs given to the gather (measurement knob)
+  if (grid_env < 0) {
+    const char* v = getenv("DFFM_RSW_GRID");
+    grid_env = v ? atoi(v) : 0;
+  }
+  const int64_t sms = grid_env > 0 ? std::min(grid_env, sm_count_current()) : sm_count_current();
+  const int64_t grid = std::min<int64_t>(p.n, sms);
   if (grid <= 0) return DFFM_OK;
   note_launches(1), kern<<<(unsigned)grid, RSW_THREADS, L.total, s>>>(p, L);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rsw)");

@@ -84,6 +84,23 @@ __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
+// same, A (M x 16 fp16) read from TMEM: one lane per row, 8 columns of packed pairs
+__device__ __forceinline__ void mma_f16_ta(uint32_t d, uint32_t a, uint64_t b, uint32_t id,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+// 32 lanes x 8 consecutive 32-bit columns of TMEM <- 8 registers per thread
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -119,20 +136,6 @@ __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t&
   lo = *(const uint32_t*)&l;
 }
 
-// write 8 consecutive K values (one core-matrix row) of example row r into the
-// two A tiles of a stage; kc = K core (0 or 1) within the 16-wide chunk
-__device__ __forceinline__ void write_a8(unsigned char* st, int r, int kc, const float* a,
-                                         float scale) {
-  const int off = TC_OFF_A + (kc * 16 + (r >> 3)) * 128 + (r & 7) * 16;
-  uint4 u0, u1;
-  split2(a[0] * scale, a[1] * scale, u0.x, u1.x);
-  split2(a[2] * scale, a[3] * scale, u0.y, u1.y);
-  split2(a[4] * scale, a[5] * scale, u0.z, u1.z);
-  split2(a[6] * scale, a[7] * scale, u0.w, u1.w);
-  *(uint4*)(st + off) = u0;
-  *(uint4*)(st + off + 4096) = u1;
-}
-
 // power-of-two exponent putting a maximum magnitude m in [2^14, 2^15)
 __device__ __forceinline__ int range_exp(float m) {
   return m > 0.f ? max(-100, min(100, TC_HEXP - ilogbf(m))) : 0;
@@ -155,8 +158,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages, SB = p.stage_bytes, NH = p.n_hidden;
-  unsigned char* abuf = smem + S * SB;  // hidden layers' A operands, chunk c at c * 8 KB
-  uint64_t* full = (uint64_t*)(abuf + p.abuf_bytes);
+  uint64_t* full = (uint64_t*)(smem + S * SB);
   uint64_t* empty = full + S;
   uint64_t* abar = empty + S;    // [1] the epilogue wrote the next layer's A buffer
   uint64_t* accf = abar + 2;     // [2] TMEM region holds a finished group
@@ -206,20 +208,22 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      uint32_t g = 0;
+      uint32_t s = 0, ph = 0, wrapped = 0;  // ring stage, its phase, past the first round
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int row0 = (int)(tile_row(t) * TC_M);
         for (int l = 0; l < NH; ++l) {
           const int nck = p.kin[l] >> 4;
           const uint32_t wbytes = (uint32_t)p.nout[l] * 64u;
-          for (int c = 0; c < nck; ++c, ++g) {
-            const int s = (int)(g % S);
-            const uint32_t u = g / S;
-            if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          const unsigned char* wsrc = (const unsigned char*)p.wblk[l];
+          for (int c = 0; c < nck; ++c) {
+            if (wrapped) mbar_wait(&empty[s], ph ^ 1u);
             unsigned char* st = smem + s * SB;
             mbar_arrive_expect_tx(&full[s], wbytes + (l == 0 ? 8192u : 0u));
             if (l == 0)  // {8 halfs, 128 rows, 2 K cores, 2 planes} -> A0 | A1
-              tma_load_4d(st + TC_OFF_A, &tmx, 0, (int)(tile_row(t) * TC_M), 2 * c, 0, &full[s]);
-            tma_load_1d(st + TC_OFF_B, p.wblk[l] + (size_t)c * p.nout[l] * 32, wbytes, &full[s]);
+              tma_load_4d(st + TC_OFF_A, &tmx, 0, row0, 2 * c, 0, &full[s]);
+            tma_load_1d(st + TC_OFF_B, wsrc, wbytes, &full[s]);
+            wsrc += wbytes;
+            if (++s == (uint32_t)S) { s = 0; ph ^= 1u; wrapped = 1; }
           }
         }
       }
@@ -227,47 +231,55 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint32_t g = 0, gg = 0;  // chunk counter, accumulation-group counter
+      uint32_t s = 0, ph = 0;  // ring stage and its phase
+      uint32_t gg = 0;         // accumulation-group (= layer) counter
       uint32_t abph = 0;       // phase of abar (one completion per tile and layer >= 1)
-      uint32_t d = tmem;
+      uint32_t d = tmem, dprev = tmem;  // this / the previous layer's accumulator region
+      // descriptors of stage 0; stage s adds (s * SB) >> 4 to the 14-bit address field
+      const uint32_t st0 = smem_u32(smem);
+      const uint64_t a0_0 = umma_desc(st0 + TC_OFF_A, 2048, 128);
+      const uint64_t a1_0 = umma_desc(st0 + TC_OFF_A + 4096, 2048, 128);
+      const uint32_t sstep = (uint32_t)SB >> 4;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int l = 0; l < NH; ++l) {
           const int nck = p.kin[l] >> 4, N = p.nout[l];
           const uint32_t id = idesc_f16(TC_M, N);
           const uint32_t lboW = (uint32_t)(N >> 3) * 128u;
-          if (l > 0) {  // the epilogue filled this layer's A buffer in one burst
+          const uint64_t b0_0 = umma_desc(st0 + TC_OFF_B, lboW, 128);
+          const uint64_t b1_0 = umma_desc(st0 + TC_OFF_B + (uint32_t)N * 32u, lboW, 128);
+          if (l > 0) {  // the epilogue rewrote the previous layer's region as this layer's A
             mbar_wait(abar, abph);
             abph ^= 1u;
+            dprev = d;
           }
-          for (int c = 0; c < nck; ++c, ++g) {
-            const int cg = c % TC_GROUP;
-            if (cg == 0) {  // a new group: its region must have been drained
-              const uint32_t reg = gg & 1;
-              if (gg >= 2) mbar_wait(&tempty[reg], ((gg >> 1) - 1) & 1);
-              d = tmem + reg * RS;
-            }
-            const int s = (int)(g % S);
-            const uint32_t u = g / S;
+          {  // one accumulation group per layer: its region must have been released
+            const uint32_t reg = gg & 1;
+            if (gg >= 2) mbar_wait(&tempty[reg], ((gg >> 1) - 1) & 1);
+            d = tmem + reg * RS;
+          }
+          for (int c = 0; c < nck; ++c) {
             if (c == 0) TCT(l * 2);
-            mbar_wait(&full[s], u & 1);
+            mbar_wait(&full[s], ph);
             if (c == 0) TCT(l * 2 + 1);
             tc_fence_after();
-            const uint32_t st = smem_u32(smem + s * SB);
-            const uint32_t at = l == 0 ? st + TC_OFF_A : smem_u32(abuf) + (uint32_t)c * 8192u;
-            const uint64_t a0 = umma_desc(at, 2048, 128);
-            const uint64_t a1 = umma_desc(at + 4096, 2048, 128);
-            const uint64_t b0 = umma_desc(st + TC_OFF_B, lboW, 128);
-            const uint64_t b1 = umma_desc(st + TC_OFF_B + (uint32_t)N * 32u, lboW, 128);
-            mma_f16(d, a0, b0, id, cg != 0);
-            mma_f16(d, a0, b1, id, 1);
-            mma_f16(d, a1, b0, id, 1);
-            mma_commit(&empty[s]);  // stage reusable once these MMAs finish
-            if (c == nck - 1) TCT(16 + l);
-            if (cg == TC_GROUP - 1 || c == nck - 1) {
-              mma_commit(&accf[gg & 1]);  // group complete in its region
-              ++gg;
+            const uint64_t so = (uint64_t)(s * sstep);
+            const uint64_t b0 = b0_0 + so, b1 = b1_0 + so;
+            if (l == 0) {
+              mma_f16(d, a0_0 + so, b0, id, c != 0);
+              mma_f16(d, a0_0 + so, b1, id, 1);
+              mma_f16(d, a1_0 + so, b0, id, 1);
+            } else {  // chunk c of A: hi pieces at column 16c, lo pieces at 16c + 8
+              const uint32_t a0 = dprev + (uint32_t)c * 16u, a1 = a0 + 8u;
+              mma_f16_ta(d, a0, b0, id, c != 0);
+              mma_f16_ta(d, a0, b1, id, 1);
+              mma_f16_ta(d, a1, b0, id, 1);
             }
+            mma_commit(&empty[s]);  // stage reusable once these MMAs finish
+            if (++s == (uint32_t)S) { s = 0; ph ^= 1u; }
           }
+          TCT(16 + l);
+          mma_commit(&accf[gg & 1]);  // the layer's accumulator is complete
+          ++gg;
         }
       }
     }
@@ -293,7 +305,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
         const int N = p.nout[l];
         // this part's 16-column blocks [b0, b0 + nb) of layer l (parts may be
         // empty when N < 64); they are also the K chunks of layer l + 1 that
-        // this part writes into abuf
+        // this part writes (as fp16 pieces, in place) into the accumulator region
         const int b0 = part_blk(h, N), nb = part_blk(h + 1, N) - b0;
         const uint32_t reg = dg & 1;
         mbar_wait(&accf[reg], (dg >> 1) & 1);
@@ -323,19 +335,19 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
           for (int k2 = 0; k2 < TC_PARTS; ++k2) mb = max(mb, xe[k2 * TC_M + r]);
           const int e_next = range_exp(__int_as_float(mb));
           const float a_scale = pow2f(e_next);
-          for (int cb = 0; cb < nb; ++cb) {  // pass 2: layer l + 1's A chunks (abuf)
+          for (int cb = 0; cb < nb; ++cb) {  // pass 2: layer l + 1's A, in place in TMEM
             float v[16];
             tmem_ld16(ta + (uint32_t)cb * 16, v);
+            uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = relu_nan(v[j] * zs + bl[cb * 16 + j]);
-            // the MMAs of layer l, abuf's previous readers, completed before
-            // its accumulator could be read
-            unsigned char* at = abuf + (size_t)(b0 + cb) * 8192 - TC_OFF_A;
-            write_a8(at, r, 0, v, a_scale);
-            write_a8(at, r, 1, v + 8, a_scale);
+            for (int j = 0; j < 8; ++j)
+              split2(relu_nan(v[2 * j] * zs + bl[cb * 16 + 2 * j]) * a_scale,
+                     relu_nan(v[2 * j + 1] * zs + bl[cb * 16 + 2 * j + 1]) * a_scale, hi[j], lo[j]);
+            tmem_st8(ta + (uint32_t)cb * 16, hi);
+            tmem_st8(ta + (uint32_t)cb * 16 + 8, lo);
           }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           row_e = e_next;
-          fence_async_smem();
         } else {
           const float* wo = cst + 1024 + b0 * 16;
           for (int cb = 0; cb < nb; ++cb) {  // last hidden layer: straight into the dot
@@ -352,8 +364,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmx, const MlpTcParams p) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&tempty[reg]);
+          // region release: layer l's MMAs have consumed layer l's A, which
+          // lived in layer l-1's region; the last layer's own region is read
+          if (l > 0) mbar_arrive(&tempty[reg ^ 1u]);
           if (l + 1 < NH) mbar_arrive(abar);
+          else mbar_arrive(&tempty[reg]);
         }
         ++dg;
       }

@@ -28,8 +28,9 @@ constexpr int TC_WIDTH_MULT = 16;            // hidden widths: multiples of this
 constexpr int TC_GROUP = DFFM_TC_GROUP;  // max K chunks of a layer (one TMEM accumulation)
 constexpr int TC_MAX_STAGES = 8;
 // stage layout (bytes): A0 A1 fp16 tiles (layer 0: one TMA of the staged hi/lo
-// planes) | B0 B1 fp16 tiles.  Later layers read A from a dedicated buffer the
-// epilogue fills in one burst (abuf: per 16-wide chunk, the same A0 | A1 tiles).
+// planes) | B0 B1 fp16 tiles.  Later layers read A from TMEM: the epilogue
+// rewrites the previous layer's accumulator region in place as packed fp16
+// pieces (chunk c: hi at column 16c, lo at 16c + 8).
 constexpr int TC_OFF_A = 0;           // 2 tiles of 128 x 16 fp16 (4 KB each)
 constexpr int TC_OFF_B = 8192;
 constexpr int TC_HEXP = 14;           // operands are scaled to a maximum in [2^14, 2^15)
@@ -55,7 +56,6 @@ struct MlpTcParams {
   const float* w_out;   // [nout[n_hidden-1]] output layer column (M:372)
   const float* b_out;   // [1]
   int stages;
-  int abuf_bytes;       // 128 rows x max(kin[l >= 1]) x 4 B: hidden layers' A operands
   int stage_bytes;      // 8 KB (A tiles) + nmax * 64 B (B tiles), 1 KB aligned
   int tmem_cols;        // power of two >= 2 * nmax: two accumulator regions
 };
@@ -63,12 +63,12 @@ struct MlpTcParams {
 __host__ __device__ inline int tc_stage_bytes(int nmax) {
   return (TC_OFF_B + nmax * 64 + 1023) & ~1023;
 }
-// dynamic shared memory: 1 KB alignment slack, stages, the hidden-layer A
-// buffer, barriers (full/empty per stage, abar, accf/tempty per TMEM region),
+// dynamic shared memory: 1 KB alignment slack, stages, barriers (full/empty
+// per stage, abar, accf/tempty per TMEM region),
 // TMEM slot, the parts' row exchange (double-buffered by tile) and the row
 // exponent exchange (double-buffered by layer)
-__host__ __device__ inline int tc_smem_bytes(int stages, int stage_bytes, int abuf_bytes) {
-  return 1024 + stages * stage_bytes + abuf_bytes + (2 * stages + 6) * 8 + 16 +
+__host__ __device__ inline int tc_smem_bytes(int stages, int stage_bytes) {
+  return 1024 + stages * stage_bytes + (2 * stages + 6) * 8 + 16 +
          2 * TC_PARTS * TC_M * 8 + 2 * TC_PARTS * TC_M * 4 + TC_CONST_FLOATS * 4;
 }
 
