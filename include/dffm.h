@@ -134,6 +134,28 @@ int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx, const float*
                    float* prob, uint64_t* status, void* stream);
 
 /*
+ * Device-resident context caches (SPEC S:248-262 build_context_cache, S:263-271
+ * predict_batch): dffm_ctx_build writes, per request, a blob of
+ * dffm_ctx_cache_bytes() bytes (16-byte aligned) holding the context slots,
+ * the context lr partial, the context latent sums S[x][g][:] and the
+ * ctx x ctx pair outputs with their f64 moments; a bad context index is a
+ * ContractError at that request.  dffm_ctx_score_cached scores candidates
+ * against prebuilt blobs (no context pass; the context rows are still passed
+ * for shapes the row-ring kernel does not take, which rebuild in-kernel).
+ * dffm_ctx_build_count(): request caches built so far by this library.
+ */
+int64_t dffm_ctx_cache_bytes(const dffm_model* model, int32_t n_ctx_fields, int32_t ctx_m);
+int dffm_ctx_build(const dffm_model* model, const int32_t* ctx_idx, const float* ctx_val,
+                   int32_t n_ctx_fields, int32_t ctx_m, int64_t n_requests, void* cache_out,
+                   uint64_t* status, void* stream);
+int dffm_ctx_score_cached(const dffm_model* model, const void* cache, const int32_t* ctx_idx,
+                          const float* ctx_val, int32_t n_ctx_fields, int32_t ctx_m,
+                          const int32_t* cand_idx, const float* cand_val, int32_t cand_m,
+                          int64_t n_requests, int32_t n_cand, float* prob, uint64_t* status,
+                          void* stream);
+int64_t dffm_ctx_build_count(void);
+
+/*
  * K2 sequential Adagrad trainer: replaces the predict-then-learn loop of
  * training._train_lines (T:172-185) = forward (M:321) + predict_proba
  * (M:300) + backward_update (M:440-533), in the reference's exact example

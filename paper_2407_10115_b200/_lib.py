@@ -64,6 +64,13 @@ SIGNATURES = {
     "dffm_ctx_score": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_int32,
                                  c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p,
                                  c_void_p, c_void_p]),
+    "dffm_ctx_cache_bytes": (c_int64, [POINTER(DffmModel), c_int32, c_int32]),
+    "dffm_ctx_build": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_int32,
+                                 c_int64, c_void_p, c_void_p, c_void_p]),
+    "dffm_ctx_score_cached": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_void_p, c_int32,
+                                        c_int32, c_void_p, c_void_p, c_int32, c_int64, c_int32,
+                                        c_void_p, c_void_p, c_void_p]),
+    "dffm_ctx_build_count": (c_int64, []),
     "dffm_train_scratch_bytes": (c_int64, [POINTER(DffmModel), c_int32]),
     "dffm_train_sequential": (c_int32, [POINTER(DffmModel), POINTER(DffmTrainState), c_void_p,
                                         c_void_p, c_void_p, c_int32, c_int64, c_void_p,

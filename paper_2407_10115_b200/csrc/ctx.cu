@@ -1,3 +1,4 @@
+#include <atomic>
 // K3: context-cached candidate scorer (no reference code --
 // the truth is model.forward on the merged context+candidate example).
 //
@@ -36,6 +37,7 @@ struct CtxParams {
   int64_t R;
   int C;
   int cblk;  // candidates per work unit (a multiple of TE)
+  const unsigned char* cache_in;  // K3 v2: prebuilt context caches (dffm_ctx_build), or null
 };
 
 struct CtxSmem {
@@ -279,15 +281,128 @@ static int launch_ctx(CtxKernel kern, const CtxParams& q, int smem, cudaStream_t
   return DFFM_OK;
 }
 
+// request context caches the library has built (host count; dffm_ctx_build_count)
+static std::atomic<long long> g_ctx_builds{0};
+
+// build_context_cache for R requests into per-request blobs (cache_bytes each):
+// one CTA per request builds it in shared memory and copies it out
+template <typename T>
+__global__ void __launch_bounds__(256) ctx_build_kernel(CtxParams q, CrSmem L,
+                                                        unsigned char* out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int64_t r = blockIdx.x;
+  cr_build_cache<T>(smem, q, L, r, r, threadIdx.x, 256);
+  uint4* dst = (uint4*)(out + (size_t)r * L.cache_bytes);
+  for (int v = threadIdx.x; v < L.cache_bytes / 16; v += 256) dst[v] = ((const uint4*)smem)[v];
+}
+
+// the K3 v2 context-cache layout (cache_bytes per request) for this model shape
+static CrSmem ctx_cache_layout(const FwdParams& p, int wdtype, int Fc, int Mc) {
+  const int esz = wdtype == DFFM_W_F32 ? 4 : 2;
+  return cr_smem_layout(p.F, Fc, Mc, p.F - Fc, 1, p.k, esz, CR_MAXX, max_smem_optin_current());
+}
+
 }  // namespace dffm
 
 using namespace dffm;
+
+static int ctx_score_impl(const dffm_model* model, const int32_t* ctx_idx, const float* ctx_val,
+                          int32_t n_ctx_fields, int32_t ctx_m, const int32_t* cand_idx,
+                          const float* cand_val, int32_t cand_m, int64_t n_requests,
+                          int32_t n_cand, float* prob, uint64_t* status, void* stream,
+                          const unsigned char* cache_in);
 
 extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
                               const float* ctx_val, int32_t n_ctx_fields, int32_t ctx_m,
                               const int32_t* cand_idx, const float* cand_val, int32_t cand_m,
                               int64_t n_requests, int32_t n_cand, float* prob, uint64_t* status,
                               void* stream) {
+  return ctx_score_impl(model, ctx_idx, ctx_val, n_ctx_fields, ctx_m, cand_idx, cand_val, cand_m,
+                        n_requests, n_cand, prob, status, stream, nullptr);
+}
+
+extern "C" int64_t dffm_ctx_build_count(void) { return g_ctx_builds.load(); }
+
+extern "C" int64_t dffm_ctx_cache_bytes(const dffm_model* model, int32_t n_ctx_fields,
+                                        int32_t ctx_m) {
+  FwdParams p{};
+  if (fill_model_params(model, p)) return -1;
+  if (n_ctx_fields < 1 || n_ctx_fields >= p.F || ctx_m < 1 || ctx_m > 64) {
+    set_error("bad context shape");
+    return -1;
+  }
+  return ctx_cache_layout(p, model->wdtype, n_ctx_fields, ctx_m).cache_bytes;
+}
+
+extern "C" int dffm_ctx_build(const dffm_model* model, const int32_t* ctx_idx,
+                              const float* ctx_val, int32_t n_ctx_fields, int32_t ctx_m,
+                              int64_t n_requests, void* cache_out, uint64_t* status,
+                              void* stream) {
+  CtxParams q{};
+  int rc = fill_model_params(model, q.f);
+  if (rc) return rc;
+  FwdParams& p = q.f;
+  if (n_ctx_fields < 1 || n_ctx_fields >= p.F || ctx_m < 1 || ctx_m > 64 || n_requests < 0 ||
+      n_requests > (1ll << 31) - 1) {
+    set_error("bad context shape");
+    return DFFM_CONTRACT;
+  }
+  if (n_requests == 0) return DFFM_OK;
+  if (!ctx_idx || !ctx_val || !cache_out || !status) { set_error("null buffer"); return DFFM_CONTRACT; }
+  const int k = p.k, esz = model->wdtype == DFFM_W_F32 ? 4 : 2;
+  if (!(k == 4 || k == 8 || k == 16) || (k * esz) % 16 || ((uintptr_t)p.ffm & 15) ||
+      ((uintptr_t)cache_out & 15)) {
+    set_error("context cache needs k in {4, 8, 16} with 16-byte rows");
+    return DFFM_SIZING;
+  }
+  q.cidx = ctx_idx;
+  q.cval = ctx_val;
+  q.Fc = n_ctx_fields;
+  q.Mc = ctx_m;
+  q.Fd = p.F - n_ctx_fields;
+  p.status = status;
+  const CrSmem L = ctx_cache_layout(p, model->wdtype, n_ctx_fields, ctx_m);
+  const void* kern = model->wdtype == DFFM_W_F32 ? (const void*)ctx_build_kernel<float>
+                     : model->wdtype == DFFM_W_BF16 ? (const void*)ctx_build_kernel<__nv_bfloat16>
+                                                    : (const void*)ctx_build_kernel<uint16_t>;
+  int occ = 0;
+  if ((rc = kernel_occupancy(kern, 256, L.cache_bytes, &occ))) return rc;
+  const cudaStream_t s = (cudaStream_t)stream;
+  switch (model->wdtype) {
+    case DFFM_W_F32:
+      note_launches(1), ctx_build_kernel<float><<<(unsigned)n_requests, 256, L.cache_bytes, s>>>(
+                            q, L, (unsigned char*)cache_out);
+      break;
+    case DFFM_W_BF16:
+      note_launches(1), ctx_build_kernel<__nv_bfloat16>
+                            <<<(unsigned)n_requests, 256, L.cache_bytes, s>>>(q, L,
+                                                                 (unsigned char*)cache_out);
+      break;
+    default:
+      note_launches(1), ctx_build_kernel<uint16_t><<<(unsigned)n_requests, 256, L.cache_bytes, s>>>(
+                            q, L, (unsigned char*)cache_out);
+  }
+  DFFM_CUDA_TRY(cudaGetLastError(), "launch(ctx_build)");
+  g_ctx_builds += n_requests;
+  return DFFM_OK;
+}
+
+extern "C" int dffm_ctx_score_cached(const dffm_model* model, const void* cache,
+                                     const int32_t* ctx_idx, const float* ctx_val,
+                                     int32_t n_ctx_fields, int32_t ctx_m, const int32_t* cand_idx,
+                                     const float* cand_val, int32_t cand_m, int64_t n_requests,
+                                     int32_t n_cand, float* prob, uint64_t* status, void* stream) {
+  if (!cache || ((uintptr_t)cache & 15)) { set_error("null / misaligned cache"); return DFFM_CONTRACT; }
+  return ctx_score_impl(model, ctx_idx, ctx_val, n_ctx_fields, ctx_m, cand_idx, cand_val, cand_m,
+                        n_requests, n_cand, prob, status, stream,
+                        (const unsigned char*)cache);
+}
+
+static int ctx_score_impl(const dffm_model* model, const int32_t* ctx_idx, const float* ctx_val,
+                          int32_t n_ctx_fields, int32_t ctx_m, const int32_t* cand_idx,
+                          const float* cand_val, int32_t cand_m, int64_t n_requests,
+                          int32_t n_cand, float* prob, uint64_t* status, void* stream,
+                          const unsigned char* cache_in) {
   CtxParams q{};
   int rc = fill_model_params(model, q.f);
   if (rc) return rc;
@@ -414,15 +529,20 @@ extern "C" int dffm_ctx_score(const dffm_model* model, const int32_t* ctx_idx,
         a.f.rout = plan.resid;
         a.f.fout = plan.flags;
         a.f.Kp = plan.Kp;
+        a.cache_in = cache_in ? cache_in + (size_t)r0 * CL.cache_bytes : nullptr;
         const int64_t grid = std::min<int64_t>(nr, (int64_t)sm_count_current());
         note_launches(1), rk<<<(unsigned)grid, CR_THREADS, CL.total, s>>>(a, CL);
         DFFM_CUDA_TRY(cudaGetLastError(), "launch(ctx_ring)");
         if ((rc = tc_mlp_slice(plan, nr * n_cand, r0 * n_cand, prob + r0 * n_cand, nullptr, s)))
           return rc;
+        if (!cache_in) g_ctx_builds += nr;
       }
       return DFFM_OK;
     }
   }
+  // other shapes build every request's context inside the kernel (a prebuilt
+  // cache is not consumed there; the context rows give the same result)
+  g_ctx_builds += n_requests;
   if (!use_tc) return launch_ctx(kern, q, L.total, (cudaStream_t)stream);
   // requests in slices: K3 stages each candidate's MergeNorm row, mlp_tc scores them
   const cudaStream_t s = (cudaStream_t)stream;

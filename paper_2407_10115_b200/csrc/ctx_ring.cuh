@@ -96,6 +96,109 @@ __host__ __device__ inline CrSmem cr_smem_layout(int F, int Fc, int Mc, int Fd, 
   return s;
 }
 
+
+// build_context_cache for request r into the cache blob wb (shared
+// memory): context slots, lr partial, Sctx[x][g][:] (f32 fma over the slots
+// in slot order), ctx x ctx pair values and their f64 sum / sum of squares.
+// Called by nthr threads (tid < nthr) that share named barrier 1; ends with it.
+template <typename T>
+__device__ __forceinline__ void cr_build_cache(unsigned char* wb, const CtxParams& q,
+                                             const CrSmem& L, int64_t r, int64_t status_ex,
+                                             int tid, int nthr) {
+  const FwdParams& p = q.f;
+  const int F = p.F, P = p.P, Fc = q.Fc, Mc = q.Mc;
+  const int lane = tid & 31;
+  const T* lrt = (const T*)p.lr;
+  float* S = (float*)(wb + L.c_S);
+  float* cpx = (float*)(wb + L.c_cpx);
+  unsigned char* cpres = wb + L.c_pres;
+  int* csidx = (int*)(wb + L.c_sidx);
+  float* csval = (float*)(wb + L.c_sval);
+  for (int s = tid; s < Fc * Mc; s += nthr) {
+    int j = __ldg(q.cidx + r * Fc * Mc + s);
+    if (j >= p.n_buckets || j < -1) {
+      atomicMin((unsigned long long*)p.status,
+                (unsigned long long)status_key(status_ex, DFFM_BLOCK_NONE,
+                                               DFFM_CONTRACT));
+      j = -1;
+    }
+    csidx[s] = j;
+    csval[s] = __ldg(q.cval + r * Fc * Mc + s);
+  }
+  named_bar_sync(1, nthr);
+  if (tid < 32) {
+    double lrs = 0.0;
+    for (int s = lane; s < Fc * Mc; s += 32)
+      if (csidx[s] >= 0) lrs += (double)csval[s] * (double)load_elem<T>(lrt + csidx[s], p.dlr);
+    lrs = warp_sum(lrs);
+    if (lane == 0) *(double*)(wb + L.c_lr) = lrs;
+  }
+  for (int x = tid; x < Fc; x += nthr) {
+    unsigned char pr = 0;
+    for (int m = 0; m < Mc; ++m) pr |= (csidx[x * Mc + m] >= 0);
+    cpres[x] = pr;
+  }
+  // 16-byte vectors of the context rows (one load per slot per vector,
+  // all in flight together); same f32 fma over the slots in slot order
+  const int Fk = F * p.k;
+  constexpr int PER = 16 / (int)sizeof(T);
+  const int nvec = Fk / PER;  // rows are whole 16-byte vectors (k * esz % 16 == 0)
+  for (int t2 = tid; t2 < Fc * nvec; t2 += nthr) {
+    const int x = t2 / nvec, v = t2 - x * nvec;
+    float acc[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) acc[u] = 0.f;
+    for (int m = 0; m < Mc; ++m) {
+      const int j = csidx[x * Mc + m];
+      if (j >= 0) {
+        float w[PER];
+        unpack16<T>(*(const uint4*)((const unsigned char*)p.ffm +
+                                    ((int64_t)j * Fk + v * PER) * (int64_t)sizeof(T)),
+                    w, p.dffm);
+        const float xv = csval[x * Mc + m];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) acc[u] = fmaf(xv, w[u], acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) S[x * Fk + v * PER + u] = acc[u];
+  }
+  named_bar_sync(1, nthr);
+  for (int pp = tid; pp < P; pp += nthr) cpx[pp] = 0.f;
+  named_bar_sync(1, nthr);
+  for (int x1 = 0; x1 < Fc; ++x1)
+    for (int x2 = x1 + 1 + tid; x2 < Fc; x2 += nthr) {
+      float pv = 0.f;
+      if (cpres[x1] & cpres[x2]) {
+        const float* a = S + (x1 * F + x2) * p.k;
+        const float* b = S + (x2 * F + x1) * p.k;
+        for (int kk = 0; kk < p.k; ++kk) pv = fmaf(a[kk], b[kk], pv);
+      }
+      cpx[x1 * F - x1 * (x1 + 1) / 2 + x2 - x1 - 1] = pv;
+    }
+  named_bar_sync(1, nthr);
+  if (tid < 32) {  // moments of the ctx x ctx block (fixed order: deterministic)
+    double s1 = 0.0, sq = 0.0;
+    int bad = 0;
+    for (int pp = lane; pp < P; pp += 32) {
+      const double v = cpx[pp];
+      s1 += v;
+      sq += v * v;
+      bad |= !isfinite(cpx[pp]);
+    }
+    s1 = warp_sum(s1);
+    sq = warp_sum(sq);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      double* cm = (double*)(wb + L.c_lr);
+      cm[1] = s1;
+      cm[2] = sq;
+      cm[3] = bad ? 1.0 : 0.0;
+    }
+  }
+  named_bar_sync(1, nthr);
+}
+
 template <int K, typename T, int MD>
 __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, CrSmem L) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -338,95 +441,14 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
           cur_req = t;
           const int64_t r = (int64_t)blockIdx.x + t * gridDim.x;
           unsigned char* wb = cache(t);
-          float* S = (float*)(wb + L.c_S);
-          float* cpx = (float*)(wb + L.c_cpx);
-          unsigned char* cpres = wb + L.c_pres;
-          int* csidx = (int*)(wb + L.c_sidx);
-          float* csval = (float*)(wb + L.c_sval);
           named_bar_sync(1, nthr);  // every pair warp is past request t-1
-          for (int s = tid; s < Fc * Mc; s += nthr) {
-            int j = __ldg(q.cidx + r * Fc * Mc + s);
-            if (j >= p.n_buckets || j < -1) {
-              atomicMin((unsigned long long*)p.status,
-                        (unsigned long long)status_key(p.status_base + r * C, DFFM_BLOCK_NONE,
-                                                       DFFM_CONTRACT));
-              j = -1;
-            }
-            csidx[s] = j;
-            csval[s] = __ldg(q.cval + r * Fc * Mc + s);
+          if (q.cache_in) {  // prebuilt (dffm_ctx_build): copy the request's cache blob
+            const uint4* src = (const uint4*)(q.cache_in + (size_t)r * L.cache_bytes);
+            for (int v = tid; v < L.cache_bytes / 16; v += nthr) ((uint4*)wb)[v] = __ldg(src + v);
+            named_bar_sync(1, nthr);
+          } else {
+            cr_build_cache<T>(wb, q, L, r, p.status_base + r * C, tid, nthr);
           }
-          named_bar_sync(1, nthr);
-          if (warp == 0) {
-            double lrs = 0.0;
-            for (int s = lane; s < Fc * Mc; s += 32)
-              if (csidx[s] >= 0) lrs += (double)csval[s] * (double)load_elem<T>(lrt + csidx[s], p.dlr);
-            lrs = warp_sum(lrs);
-            if (lane == 0) *(double*)(wb + L.c_lr) = lrs;
-          }
-          for (int x = tid; x < Fc; x += nthr) {
-            unsigned char pr = 0;
-            for (int m = 0; m < Mc; ++m) pr |= (csidx[x * Mc + m] >= 0);
-            cpres[x] = pr;
-          }
-          // 16-byte vectors of the context rows (one load per slot per vector,
-          // all in flight together); same f32 fma over the slots in slot order
-          const int Fk = F * p.k;
-          constexpr int PER = 16 / (int)sizeof(T);
-          const int nvec = Fk / PER;  // rows are whole 16-byte vectors (k * esz % 16 == 0)
-          for (int t2 = tid; t2 < Fc * nvec; t2 += nthr) {
-            const int x = t2 / nvec, v = t2 - x * nvec;
-            float acc[PER];
-#pragma unroll
-            for (int u = 0; u < PER; ++u) acc[u] = 0.f;
-            for (int m = 0; m < Mc; ++m) {
-              const int j = csidx[x * Mc + m];
-              if (j >= 0) {
-                float w[PER];
-                unpack16<T>(*(const uint4*)((const unsigned char*)p.ffm +
-                                            ((int64_t)j * Fk + v * PER) * (int64_t)sizeof(T)),
-                            w, p.dffm);
-                const float xv = csval[x * Mc + m];
-#pragma unroll
-                for (int u = 0; u < PER; ++u) acc[u] = fmaf(xv, w[u], acc[u]);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < PER; ++u) S[x * Fk + v * PER + u] = acc[u];
-          }
-          named_bar_sync(1, nthr);
-          for (int pp = tid; pp < P; pp += nthr) cpx[pp] = 0.f;
-          named_bar_sync(1, nthr);
-          for (int x1 = 0; x1 < Fc; ++x1)
-            for (int x2 = x1 + 1 + tid; x2 < Fc; x2 += nthr) {
-              float pv = 0.f;
-              if (cpres[x1] & cpres[x2]) {
-                const float* a = S + (x1 * F + x2) * p.k;
-                const float* b = S + (x2 * F + x1) * p.k;
-                for (int kk = 0; kk < p.k; ++kk) pv = fmaf(a[kk], b[kk], pv);
-              }
-              cpx[x1 * F - x1 * (x1 + 1) / 2 + x2 - x1 - 1] = pv;
-            }
-          named_bar_sync(1, nthr);
-          if (warp == 0) {  // moments of the ctx x ctx block (fixed order: deterministic)
-            double s1 = 0.0, sq = 0.0;
-            int bad = 0;
-            for (int pp = lane; pp < P; pp += 32) {
-              const double v = cpx[pp];
-              s1 += v;
-              sq += v * v;
-              bad |= !isfinite(cpx[pp]);
-            }
-            s1 = warp_sum(s1);
-            sq = warp_sum(sq);
-            bad = __any_sync(0xffffffffu, bad);
-            if (lane == 0) {
-              double* cm = (double*)(wb + L.c_lr);
-              cm[1] = s1;
-              cm[2] = sq;
-              cm[3] = bad ? 1.0 : 0.0;
-            }
-          }
-          named_bar_sync(1, nthr);
           cb = wb;
         }
         mbar_wait(&full[xs], par);

@@ -2,19 +2,23 @@
 
 No reference code exists for this module; the contract is
 SPEC's: cached scoring equals ``forward`` + ``predict_proba`` on the merged
-context+candidate example, the cache is a pure function of (context,
-weights version) and a version bump makes it stale.
+context+candidate example within 1e-6, the cache is a pure function of
+(context, weights version), a version bump makes it stale, and
+caches are keyed by a 64-bit digest of the sorted (field_id, feature_index,
+value-bits) triples so that a repeated context is built once.
 
-On the GPU the cache itself (context lr partial, context latent sums
-S[x][g][:], ctx x ctx pair values) is built per request inside K3's shared
-memory (csrc/ctx.cu) and reused by every candidate of that request; it never
-round-trips through HBM.  The host-side ``ContextCache`` records the packed
-context, its digest and the store version it is valid for.
+``build_context_cache`` runs K3's build pass (``dffm_ctx_build``) once: the
+context lr partial, the context latent sums S[x][g][:] and the ctx x ctx pair
+outputs with their moments stay resident in HBM as one blob per request.
+``predict_batch(cache, ...)`` scores candidates against that blob
+(``dffm_ctx_score_cached``: no context pass); ``ContextCacheMap`` is the
+digest-keyed store that reuses a cache across requests until the weights move.
 """
 
 from __future__ import annotations
 
 import hashlib
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -32,33 +36,90 @@ class ContextCache:
     n_ctx_fields: int
     digest: int
     store_version: int
+    blob: torch.Tensor | None = None  # device uint8 [cache_bytes]: the built cache
 
 
 def _digest(idx: np.ndarray, val: np.ndarray) -> int:
-    """64-bit digest of sorted (field, index, value-bits) triples."""
-    h = hashlib.blake2b(digest_size=8)
-    h.update(np.ascontiguousarray(idx, np.int32).tobytes())
-    h.update(np.ascontiguousarray(val, np.float32).tobytes())
+    """64-bit digest of the sorted (field_id, feature_index, value-bits) triples
+    of a context: independent of slot order and padding."""
+    idx = np.asarray(idx).reshape(idx.shape[-2], -1)
+    val = np.asarray(val, np.float32).reshape(idx.shape)
+    f, m = np.nonzero(idx >= 0)
+    trip = np.stack([f.astype(np.int64), idx[f, m].astype(np.int64),
+                     val[f, m].view(np.uint32).astype(np.int64)], axis=1)
+    trip = trip[np.lexsort((trip[:, 2], trip[:, 1], trip[:, 0]))]
+    h = hashlib.blake2b(np.ascontiguousarray(trip).tobytes(), digest_size=8)
     return int.from_bytes(h.digest(), "little")
 
 
 def build_context_cache(ctx_idx, ctx_val, store: WeightStore) -> ContextCache:
     """Context fields occupy field ids [0, Fc) (disjoint from the
-    candidates').  ``ctx_idx``/``ctx_val``: [Fc, Mc] or [1, Fc, Mc]."""
+    candidates').  ``ctx_idx``/``ctx_val``: [Fc, Mc] or [1, Fc, Mc].  Runs the
+    context pass once on the device (cost independent of the candidates)."""
     ci = np.asarray(ctx_idx.cpu() if isinstance(ctx_idx, torch.Tensor) else ctx_idx)
     cv = np.asarray(ctx_val.cpu() if isinstance(ctx_val, torch.Tensor) else ctx_val)
     if ci.ndim == 2:
         ci, cv = ci[None], cv[None]
-    if ci.shape[1] > store.config.n_fields:
-        raise ContractError("more context fields than the model has")
+    Fc, Mc = ci.shape[1], ci.shape[2]
+    if Fc >= store.config.n_fields or Fc < 1:
+        raise ContractError("context fields must be a non-empty proper prefix of the model's")
     dev = store.device
-    return ContextCache(_as_device(ci, torch.int32, dev), _as_device(cv, torch.float32, dev),
-                        ci.shape[1], _digest(ci, cv), store.version)
+    di, dv = _as_device(ci, torch.int32, dev), _as_device(cv, torch.float32, dev)
+    lib = _lib.lib()
+    cm = store.c_model_ref()
+    nbytes = int(lib.dffm_ctx_cache_bytes(cm, Fc, Mc))
+    if nbytes < 0:
+        _lib.check(_lib.CONTRACT, "dffm_ctx_cache_bytes")
+    blob = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    st = _status(dev)
+    s = torch.cuda.current_stream(dev)
+    st.clear()
+    _lib.check(lib.dffm_ctx_build(cm, di.data_ptr(), dv.data_ptr(), Fc, Mc, 1, blob.data_ptr(),
+                                  st.ptr(), s.cuda_stream), "dffm_ctx_build")
+    st.fetch_async()
+    s.synchronize()
+    st.raise_if_set("context cache: ")
+    return ContextCache(di, dv, Fc, _digest(ci[0], cv[0]), store.version, blob)
+
+
+class ContextCacheMap:
+    """Digest-keyed context caches ("dedupe"): a repeated context reuses
+    its device-resident cache; a weights-version bump drops every entry."""
+
+    def __init__(self, store: WeightStore, capacity: int = 4096):
+        self.store, self.capacity = store, int(capacity)
+        self._map: OrderedDict = OrderedDict()
+        self._version = store.version
+        self.hits = self.misses = 0
+
+    def get(self, ctx_idx, ctx_val) -> ContextCache:
+        if self.store.version != self._version:
+            self._map.clear()
+            self._version = self.store.version
+        ci = np.asarray(ctx_idx.cpu() if isinstance(ctx_idx, torch.Tensor) else ctx_idx)
+        cv = np.asarray(ctx_val.cpu() if isinstance(ctx_val, torch.Tensor) else ctx_val)
+        key = (ci.shape[-2], _digest(ci.reshape(ci.shape[-2], -1), cv.reshape(ci.shape[-2], -1)))
+        hit = self._map.get(key)
+        if hit is not None:
+            self._map.move_to_end(key)
+            self.hits += 1
+            return hit
+        self.misses += 1
+        cache = build_context_cache(ci, cv, self.store)
+        self._map[key] = cache
+        if len(self._map) > self.capacity:
+            self._map.popitem(last=False)
+        return cache
 
 
 def score_requests(ctx_idx, ctx_val, cand_idx, cand_val, store: WeightStore,
                    out: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
-    """Batched K3: ctx [R, Fc, Mc], cand [R, C, F-Fc, Md] -> prob [R, C] (device f32)."""
+    """Batched K3: ctx [R, Fc, Mc], cand [R, C, F-Fc, Md] -> prob [R, C] (device f32);
+    each request's context pass runs once inside the kernel."""
+    return _score(None, ctx_idx, ctx_val, cand_idx, cand_val, store, out, check)
+
+
+def _score(blob, ctx_idx, ctx_val, cand_idx, cand_val, store, out, check):
     dev = store.device
     ci = _as_device(ctx_idx, torch.int32, dev)
     cv = _as_device(ctx_val, torch.float32, dev)
@@ -74,9 +135,15 @@ def score_requests(ctx_idx, ctx_val, cand_idx, cand_val, store: WeightStore,
     st = _status(dev)
     s = torch.cuda.current_stream(dev)
     st.clear()
-    rc = _lib.lib().dffm_ctx_score(store.c_model_ref(), ci.data_ptr(), cv.data_ptr(), Fc, Mc,
-                                   di.data_ptr(), dv.data_ptr(), Md, R, C, out.data_ptr(),
-                                   st.ptr(), s.cuda_stream)
+    lib = _lib.lib()
+    if blob is None:
+        rc = lib.dffm_ctx_score(store.c_model_ref(), ci.data_ptr(), cv.data_ptr(), Fc, Mc,
+                                di.data_ptr(), dv.data_ptr(), Md, R, C, out.data_ptr(), st.ptr(),
+                                s.cuda_stream)
+    else:
+        rc = lib.dffm_ctx_score_cached(store.c_model_ref(), blob.data_ptr(), ci.data_ptr(),
+                                       cv.data_ptr(), Fc, Mc, di.data_ptr(), dv.data_ptr(), Md,
+                                       R, C, out.data_ptr(), st.ptr(), s.cuda_stream)
     _lib.check(rc, "dffm_ctx_score")
     if check:
         st.fetch_async()
@@ -86,11 +153,13 @@ def score_requests(ctx_idx, ctx_val, cand_idx, cand_val, store: WeightStore,
 
 
 def predict_batch(cache: ContextCache, cand_idx, cand_val, store: WeightStore) -> torch.Tensor:
-    """Score the candidates of one request against a cache."""
+    """Score the candidates of one request against a built cache:
+    candidate x candidate and candidate x context pairs fresh, the context
+    part from the cache."""
     if cache.store_version != store.version:
         raise StaleCacheError("context cache built against an older weights version")  # S:267
     di = _as_device(cand_idx, torch.int32, store.device)
     dv = _as_device(cand_val, torch.float32, store.device)
     if di.dim() == 3:
         di, dv = di[None], dv[None]
-    return score_requests(cache.ctx_idx, cache.ctx_val, di, dv, store)[0]
+    return _score(cache.blob, cache.ctx_idx, cache.ctx_val, di, dv, store, None, True)[0]

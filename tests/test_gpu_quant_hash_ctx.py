@@ -225,3 +225,45 @@ def test_context_ring_bad_context_index_is_contract_error(monkeypatch):
     with pytest.raises(ContractError):
         inference.score_requests(ci, np.ones_like(ci, np.float32), di,
                                  np.ones_like(di, np.float32), st)
+
+
+def test_prebuilt_context_cache_is_reused_without_a_context_pass():
+    """S:248-271: build_context_cache runs the context pass once (dffm_ctx_build);
+    predict_batch(cache, ...) scores against the device-resident blob with no
+    context build (library build counter unchanged), bit-identical to the
+    in-kernel build of score_requests; ContextCacheMap dedupes repeated
+    contexts by their digest and drops entries on a version bump."""
+    from paper_2407_10115_b200 import _lib
+    F, Fc, k, bits, C = 24, 16, 8, 12, 96
+    ost = fo.random_store(F, k, (64, 32), bits, seed=21)
+    cfg = ModelConfig(n_fields=F, k=k, hidden_sizes=(64, 32), hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, with_optimizer=False)
+    rng = np.random.default_rng(5)
+    ci = rng.integers(0, 1 << bits, (3, Fc, 1)).astype(np.int32)
+    cv = np.ones_like(ci, np.float32)
+    di = rng.integers(0, 1 << bits, (3, C, F - Fc, 1)).astype(np.int32)
+    dv = rng.lognormal(size=di.shape).astype(np.float32)
+    ref = inference.score_requests(ci, cv, di, dv, st).cpu().numpy()
+    lib = _lib.lib()
+    cache = inference.build_context_cache(ci[1], cv[1], st)
+    n0 = lib.dffm_ctx_build_count()
+    p1 = inference.predict_batch(cache, di[1], dv[1], st).cpu().numpy()
+    p2 = inference.predict_batch(cache, di[1], dv[1], st).cpu().numpy()
+    assert lib.dffm_ctx_build_count() == n0  # no context pass on the cached path
+    assert np.array_equal(p1, ref[1]) and np.array_equal(p2, ref[1])
+    # digest map: the same context (same triples, padded differently) is built once
+    cmap = inference.ContextCacheMap(st)
+    a = cmap.get(ci[0], cv[0])
+    pad_i = np.concatenate([ci[0], np.full_like(ci[0], -1)], axis=1)
+    pad_v = np.concatenate([cv[0], np.zeros_like(cv[0])], axis=1)
+    assert inference._digest(pad_i, pad_v) == a.digest
+    b = cmap.get(ci[0].copy(), cv[0].copy())
+    assert cmap.misses == 1 and cmap.hits == 1 and a is b
+    st.mark_mutated()
+    c = cmap.get(ci[0], cv[0])
+    assert c is not a and c.store_version == st.version
+    # bad context index -> ContractError at build time
+    bad = ci[0].copy()
+    bad[3, 0] = 1 << (bits + 2)
+    with pytest.raises(ContractError):
+        inference.build_context_cache(bad, cv[0], st)
