@@ -51,14 +51,14 @@ def broadcast_store(store, src: int = 0, group=None):
     """Replicate a trained store's blocks from ``src`` (one broadcast per block
     over NVLink/NVSwitch with NCCL; load-time only, never on the scoring path).
 
-    u16 (quantised) tables travel as int16 bit patterns (NCCL has no uint16)
-    and their per-table (min, bucket) headers, which live on the host, are
-    broadcast alongside, so every replica dequantises identically."""
+    Every block travels as its raw bytes (a uint8 view: NCCL and gloo have no
+    uint16, and a byte copy keeps every bit), and the per-table (min, bucket)
+    headers of u16 (quantised) tables, which live on the host, are broadcast
+    alongside, so every replica dequantises identically."""
     import torch
     import torch.distributed as dist
     for _, t in store.blocks(include_optimizer=store.has_optimizer):
-        dist.broadcast(t.view(torch.int16) if t.dtype == torch.uint16 else t, src=src,
-                       group=group)
+        dist.broadcast(t.reshape(-1).view(torch.uint8), src=src, group=group)
     if store.wdtype == "u16":
         hdr = [store.q_headers]
         dist.broadcast_object_list(hdr, src=src, group=group)

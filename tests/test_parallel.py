@@ -90,3 +90,55 @@ def test_gloo_world2_sharded_inference_matches_single_process():
         covered += b - a
     assert covered == 203
     np.testing.assert_array_equal(got, full)
+
+
+def _bcast_worker(rank, world, port, q):
+    """parallel.broadcast_store itself: rank 0 holds the trained blocks (f32 with
+    accumulators, and a u16 store with its host-side headers), rank 1 starts empty."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_10115_b200.model import ModelConfig, WeightStore
+    from paper_2407_10115_b200.parallel import broadcast_store
+    cfg = ModelConfig(n_fields=4, k=2, hidden_sizes=(8,), hash_bits=10)
+    st = WeightStore(cfg, "cpu")
+    sq = WeightStore(cfg, "cpu", "u16", with_optimizer=False)
+    if rank == 0:
+        g = torch.Generator().manual_seed(1)
+        for _, t in st.blocks(True):
+            t.copy_(torch.randn(t.shape, generator=g))
+        for _, t in sq.blocks(False):
+            if t.dtype == torch.uint16:
+                t.copy_(torch.randint(0, 65536, t.shape, generator=g).to(torch.uint16))
+            else:
+                t.copy_(torch.randn(t.shape, generator=g))
+        sq.q_headers = {"lr": (-0.5, 1e-5), "ffm": (-0.25, 2e-6)}
+    broadcast_store(st)
+    broadcast_store(sq)
+    digs = [table_digest(*[t.numpy().view(np.uint8) if t.dtype != torch.uint16
+                           else t.view(torch.int16).numpy() for _, t in x.blocks(x.has_optimizer)])
+            for x in (st, sq)]
+    out = [None] * world
+    dist.all_gather_object(out, (digs, sq.q_headers, st.version))
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_broadcast_store_replicates_every_block():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    (d0, h0, v0), (d1, h1, v1) = out
+    assert d0 == d1  # f32 + accumulators and u16 tables byte-identical on both ranks
+    assert h0 == h1 == {"lr": (-0.5, 1e-5), "ffm": (-0.25, 2e-6)}
+    assert v0 == v1 == 1  # the broadcast marks the store mutated
