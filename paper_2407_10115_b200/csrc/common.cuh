@@ -104,7 +104,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// Blocking wait for phase `parity` of `bar`.  DFFM_MBAR_HINT (ns, 0 = none) is the
+// try_wait suspend-time hint: a waiting warp sleeps until the phase completes (or
+// the hint expires) instead of re-issuing the probe, which frees issue slots for
+// the warps doing work.
+#ifndef DFFM_MBAR_HINT
+#define DFFM_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if DFFM_MBAR_HINT > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(DFFM_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
@@ -112,6 +128,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,

@@ -1,1 +1,2 @@
-for g in 148 128 112 96; do echo "== gather grid $g"; DFFM_RSW_GRID=$g python tools/mlp_quick.py 606208 5 2>&1 | grep cfg; done
+for v in hl hf; do echo "== $v"; DFFM_LIB_PATH=build_var/$v/libdffm.so python tools/mlp_quick.py 2097152 3 2>&1 | grep cfg; done
+python tools/mlp_quick.py 2097152 3 2>&1 | grep cfg
