@@ -7,7 +7,13 @@ SRC := $(wildcard $(PKG)/csrc/*.cu)
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 HDR := $(wildcard $(PKG)/csrc/*.cuh) include/dffm.h
 
+# deterministic library identity: digest of every source that goes into it
+SRC_DIGEST := $(shell cat Makefile $(sort $(SRC) $(HDR)) $(PKG)/csrc/pow10_dd.h | sha256sum | cut -c1-16)
+
 all: $(PKG)/libdffm.so
+
+build/capi.o: $(SRC) $(HDR) $(PKG)/csrc/pow10_dd.h Makefile
+build/capi.o: NVFLAGS += -DDFFM_SRC_DIGEST=\"$(SRC_DIGEST)\"
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build

@@ -294,20 +294,17 @@ def run_reference(args, wl):
     }), flush=True)
 
 
-def so_sha16() -> str:
-    import hashlib
-    p = os.path.join(REPO, "paper_2407_10115_b200", "libdffm.so")
-    try:
-        with open(p, "rb") as fh:
-            return hashlib.sha256(fh.read()).hexdigest()[:16]
-    except OSError:
-        return ""
+def build_id() -> str:
+    """dffm_build_id() of the loaded libdffm.so: a digest of the sources it was
+    built from (deterministic, unlike the .so bytes)."""
+    from paper_2407_10115_b200 import _lib
+    return _lib.lib().dffm_build_id().decode()
 
 
 def ncu_traffic_for(workload: str):
     """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the
     dominant kernel from the committed ncu capture, only if it was taken on the
-    libdffm.so that is loaded now (same sha); else None."""
+    libdffm.so that is loaded now (same build id = source digest); else None."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None, "no capture"
@@ -316,8 +313,8 @@ def ncu_traffic_for(workload: str):
     ent = d.get("captures", {}).get(workload)
     if not ent:
         return None, "no capture for this workload"
-    if ent.get("so_sha16") != so_sha16():
-        return None, f"capture taken on libdffm.so {ent.get('so_sha16')}, loaded {so_sha16()}"
+    if ent.get("build_id") != build_id():
+        return None, f"capture taken on libdffm.so build {ent.get('build_id')}, loaded {build_id()}"
     return float(ent["dram_bytes_per_launch"]), ent.get("source", "")
 
 

@@ -79,6 +79,8 @@ typedef struct dffm_model {
 /* Library identity / diagnostics */
 int dffm_abi_version(void);
 const char* dffm_last_error(void);
+/* sha256 prefix of the kernel sources + Makefile the library was built from */
+const char* dffm_build_id(void);
 int dffm_device_sm_count(int device);
 
 /*

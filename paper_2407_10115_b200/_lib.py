@@ -50,6 +50,7 @@ class DffmTrainState(ctypes.Structure):
 SIGNATURES = {
     "dffm_abi_version": (c_int32, []),
     "dffm_last_error": (ctypes.c_char_p, []),
+    "dffm_build_id": (ctypes.c_char_p, []),
     "dffm_device_sm_count": (c_int32, [c_int32]),
     "dffm_forward": (c_int32, [POINTER(DffmModel), c_void_p, c_void_p, c_int32, c_int64,
                                c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),

@@ -88,6 +88,13 @@ extern "C" {
 
 int dffm_abi_version(void) { return 1; }
 
+#ifndef DFFM_SRC_DIGEST
+#define DFFM_SRC_DIGEST "unknown"
+#endif
+// sha256 (first 16 hex) of the sources this library was built from (Makefile):
+// deterministic, unlike the .so bytes, so a committed ncu capture can be tied to it
+const char* dffm_build_id(void) { return DFFM_SRC_DIGEST; }
+
 const char* dffm_last_error(void) { return dffm::g_err; }
 
 int dffm_device_sm_count(int device) {

@@ -45,13 +45,15 @@ def per_launch(path):
     return {k: {"launches": v[0], "ms": round(v[1], 4), "dram_bytes": v[2]} for k, v in by.items()}
 
 
-sha = hashlib.sha256(open("paper_2407_10115_b200/libdffm.so", "rb").read()).hexdigest()[:16]
+sys.path.insert(0, os.getcwd())
+from paper_2407_10115_b200 import _lib  # noqa: E402
+bid = _lib.lib().dffm_build_id().decode()
 traffic = {"_note": "roofline.traffic of bench.py: dram__bytes_read.sum + dram__bytes_write.sum "
                     "per launch of the dominant kernel (fwd_rsw_kernel, the K1 v8 row-ring "
                     "gather), averaged over the launches of ONE forward step (ncu launch list "
                     "of tools/one_forward.py, NVTX range 'step', --clock-control none; "
-                    "cold-cache serialised replay); valid only for the libdffm.so whose sha "
-                    "is recorded", "captures": {}}
+                    "cold-cache serialised replay); valid only for the libdffm.so whose build id "
+                    "(dffm_build_id: digest of its sources) is recorded", "captures": {}}
 for w, key in [("cfg2", "cfg2_deepffm_fwd"), ("cfg5", "cfg5_large_bf16")]:
     path = os.path.join(src, f"launches_{w}.csv")
     if not os.path.exists(path):
@@ -59,7 +61,7 @@ for w, key in [("cfg2", "cfg2_deepffm_fwd"), ("cfg5", "cfg5_large_bf16")]:
     by = per_launch(path)
     g = by.get("dffm::fwd_rsw_kernel")
     if g:
-        traffic["captures"][key] = {"so_sha16": sha, "dram_bytes_per_launch": g["dram_bytes"] / g["launches"],
+        traffic["captures"][key] = {"build_id": bid, "dram_bytes_per_launch": g["dram_bytes"] / g["launches"],
                                     "launches": g["launches"], "source": f"profiles/r02_launches_{w}.csv",
                                     "step_kernels": by}
 json.dump(traffic, open(os.path.join(src, "ncu_traffic.json"), "w"), indent=1)
