@@ -164,9 +164,13 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
-// inline dequantisation: w = qmin + q*qb, f32 multiply then f32 add
+// inline dequantisation: w = qmin + q*qb, f32 multiply then f32 add.
+// float(q) for q < 2^16 through the 2^23 magic constant (bit pattern 0x4B000000 | q
+// is exactly 2^23 + q): one logic op and one exact FADD instead of an I2F on the
+// quarter-rate conversion pipe -- the hottest opcode of the K3 pair warps.
 __device__ __forceinline__ float deq(uint32_t q, const Deq& d) {
-  return __fadd_rn(d.qmin, __fmul_rn((float)q, d.qb));
+  const float fq = __fadd_rn(__uint_as_float(0x4B000000u | q), -8388608.f);
+  return __fadd_rn(d.qmin, __fmul_rn(fq, d.qb));
 }
 
 // Scalar table element -> float

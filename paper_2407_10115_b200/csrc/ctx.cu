@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(256) ctx_build_kernel(CtxParams q, CrSmem L,
 // the K3 v2 context-cache layout (cache_bytes per request) for this model shape
 static CrSmem ctx_cache_layout(const FwdParams& p, int wdtype, int Fc, int Mc) {
   const int esz = wdtype == DFFM_W_F32 ? 4 : 2;
-  return cr_smem_layout(p.F, Fc, Mc, p.F - Fc, 1, p.k, esz, CR_MAXX, max_smem_optin_current());
+  return cr_smem_layout(p.F, Fc, Mc, p.F - Fc, 1, p.k, esz, 1, max_smem_optin_current());
 }
 
 }  // namespace dffm
@@ -481,7 +481,7 @@ static int ctx_score_impl(const dffm_model* model, const int32_t* ctx_idx, const
     }
     const int esz = model->wdtype == DFFM_W_F32 ? 4 : 2;
     const int k = p.k;
-    const int NX = CR_MAXX;
+    const int NX = CR_MAXX;  // candidates in flight (CR_MAXX / B bundle slots)
     const int64_t per_cta = ((n_requests + 147) / 148 + 1) * (int64_t)n_cand;
     bool ok = ring_env && ctx_mlp == nullptr && tc_eligible(p, smax) && n_ctx_fields >= 1 &&
               per_cta < (1ll << 30) &&
@@ -490,8 +490,15 @@ static int ctx_score_impl(const dffm_model* model, const int32_t* ctx_idx, const
               !((uintptr_t)p.ffm & 15) && !((uintptr_t)p.lr & 3);
     CrSmem CL{};
     if (ok) {
-      CL = cr_smem_layout(p.F, q.Fc, q.Mc, q.Fd, cand_m, k, esz, NX, smax);
-      ok = CL.R >= 2 * q.Fd * cand_m;
+      static int bun_env = -1;  // DFFM_CTX_BUNDLE=1: one candidate per slot (A/B knob)
+      if (bun_env < 0) {
+        const char* v = getenv("DFFM_CTX_BUNDLE");
+        bun_env = v ? atoi(v) : 4;
+      }
+      int B = cr_bundle(q.Fd * cand_m, n_cand);
+      while (B > bun_env && B > 1) B >>= 1;
+      CL = cr_smem_layout(p.F, q.Fc, q.Mc, q.Fd, cand_m, k, esz, B, smax);
+      ok = CL.R >= 2 * B * q.Fd * cand_m;
     }
     CtxRingKernel rk = nullptr;
     if (ok) {

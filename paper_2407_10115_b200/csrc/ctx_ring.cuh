@@ -4,7 +4,11 @@
 // SPEC S:239-296 (no reference code; truth = model.forward on the merged
 // example).  Context fields are 0..Fc-1, candidate fields Fc..F-1
 // (disjoint).  The examples of the ring are the candidates of this
-// CTA's requests, in order (request r = blockIdx.x + t*gridDim.x):
+// CTA's requests, in order (request r = blockIdx.x + t*gridDim.x).  A candidate
+// is only Fd * Md rows (8 at cfg4), so the single-warp stages -- allocator and
+// issue warps -- handle a BUNDLE of B consecutive candidates per step with
+// B * Fd * Md lanes active (ncu, round 2: with one candidate per step the
+// allocator warp never waited and every other role waited on it):
 //   allocator warp   streams candidate slots (cp.async, IDXD ahead), allocates
 //                    their present rows in the ring, publishes meta[i]
 //   issue warps      one 1-D bulk copy per candidate row (full[i])
@@ -15,8 +19,8 @@
 //                    values and the context lr partial; then per candidate
 //                    the pairs that involve a candidate field:
 //                    <S[c][x], Sctx[x][c]> and <S[c1][c2], S[c2][c1]>, in
-//                    32-pair chunks; G groups of min(NPW, nch) warps take
-//                    alternate candidates (phase-safe waits: G divides NX)
+//                    32-pair chunks; G groups of warps take alternate bundles
+//                    (phase-safe waits: G divides NX)
 //   merge warps      lr_out = bias + ctx lr partial + candidate lr terms;
 //                    MergeNorm over [lr_out, all P pairs] (ctx x ctx from the
 //                    cache: never cached past MergeNorm) in f64 ->
@@ -39,7 +43,7 @@ namespace dffm {
 #define DFFM_CR_NPW 10
 #endif
 #ifndef DFFM_CR_NMW
-#define DFFM_CR_NMW 6
+#define DFFM_CR_NMW 12
 #endif
 #ifndef DFFM_CR_NISS
 #define DFFM_CR_NISS 2
@@ -53,20 +57,33 @@ constexpr int CR_CHUNK = 32;  // pairs per chunk (lane per pair)
 constexpr int CR_IDXD = 8;    // candidates of slot data streamed ahead
 
 struct CrSmem {
-  int off_bar, off_ptab, off_cnt, off_pidx, off_cache, off_slot, off_ring, total;
+  int off_bar, off_ptab, off_stab, off_cnt, off_pidx, off_cache, off_slot, off_ring, total;
   int cache_bytes, c_S, c_cpx, c_lr, c_pres, c_sidx, c_sval;  // within a cache buffer
-  int slot_bytes, s_sidx, s_sval, s_rpos, s_xv;                // within a slot
+  int slot_bytes, s_sidx, s_sval, s_rpos, s_xv, xv_stride;     // within a slot (one bundle)
   int row_stride, R, NX, nch, Pc;
+  int B, lgB;  // candidates per bundle (power of two)
 };
 
+// Candidates per bundle: the largest power of two B <= 4 with B * FM <= 32 lanes
+// that divides the candidates per request (bundles never straddle requests).
+__host__ __device__ inline int cr_bundle(int FM, int C) {
+  int B = 1;
+  while (2 * B <= 4 && 2 * B * FM <= CR_MAXFM && C % (2 * B) == 0) B *= 2;
+  return B;
+}
+
+// NX = bundle slots in flight (CR_MAXX / B: the same 64 candidates for every B)
 __host__ __device__ inline CrSmem cr_smem_layout(int F, int Fc, int Mc, int Fd, int Md, int k,
-                                                 int esz, int NX, int smem_max) {
+                                                 int esz, int B, int smem_max) {
   CrSmem s;
   const int P = F * (F - 1) / 2;
   s.Pc = Fc * Fd + Fd * (Fd - 1) / 2;
   s.nch = (s.Pc + CR_CHUNK - 1) / CR_CHUNK;
-  s.NX = NX;
-  const int FM = Fd * Md;
+  s.B = B;
+  s.lgB = B == 4 ? 2 : B == 2 ? 1 : 0;
+  s.NX = CR_MAXX / B;
+  const int FMB = Fd * Md * B;
+  const int Kp = (P + 1 + 15) & ~15;  // staged row width (tc_plan)
   s.row_stride = F * k * esz + 16;
   int q = 0;
   s.c_S = q; q = align16(q + Fc * F * k * 4);
@@ -77,18 +94,20 @@ __host__ __device__ inline CrSmem cr_smem_layout(int F, int Fc, int Mc, int Fd, 
   s.c_sval = q; q = align16(q + Fc * Mc * 4);
   s.cache_bytes = q;
   q = 0;
-  s.s_sidx = q; q = align16(q + FM * 4);
-  s.s_sval = q; q = align16(q + FM * 4);
-  s.s_rpos = q; q = align16(q + FM * 2);
-  s.s_xv = q; q = align16(q + s.Pc * 4);
+  s.s_sidx = q; q = align16(q + FMB * 4);
+  s.s_sval = q; q = align16(q + FMB * 4);
+  s.s_rpos = q; q = align16(q + FMB * 2);
+  s.xv_stride = s.Pc;
+  s.s_xv = q; q = align16(q + B * s.Pc * 4);
   s.slot_bytes = q;
   int o = 0;
   s.off_bar = o; o = align16(o + 4 * CR_MAXX * 8);
   s.off_ptab = o; o = align16(o + s.Pc * 4);
+  s.off_stab = o; o = align16(o + Kp * 2);
   s.off_cnt = o; o = align16(o + CR_MAXX * 4);
-  s.off_pidx = o; o = align16(o + CR_IDXD * 2 * FM * 4);
+  s.off_pidx = o; o = align16(o + CR_IDXD * 2 * FMB * 4);
   s.off_cache = o; o = align16(o + 2 * s.cache_bytes);
-  s.off_slot = o; o = align16(o + NX * s.slot_bytes);
+  s.off_slot = o; o = align16(o + s.NX * s.slot_bytes);
   s.off_ring = o;
   s.R = (smem_max - o) / s.row_stride;
   if (s.R > 65535) s.R = 65535;
@@ -199,6 +218,21 @@ __device__ __forceinline__ void cr_build_cache(unsigned char* wb, const CtxParam
   named_bar_sync(1, nthr);
 }
 
+// Position of a stream of candidates that advances by a fixed step: request
+// ordinal t of this CTA (request blockIdx.x + t * gridDim.x) and the candidate
+// number within it -- no per-candidate division.
+struct CrCursor {
+  int64_t t;
+  int w;
+  __device__ __forceinline__ void advance(int step, int C) {
+    w += step;
+    while (w >= C) { w -= C; ++t; }
+  }
+  __device__ __forceinline__ int64_t cand(int C) const {  // global candidate number
+    return ((int64_t)blockIdx.x + t * gridDim.x) * C + w;
+  }
+};
+
 template <int K, typename T, int MD>
 __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, CrSmem L) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -207,68 +241,109 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
   constexpr int M = MD;
   const int FM = Fd * M;
   const int C = q.C;
+  // B candidates (a bundle: consecutive candidates of one request, B | C) share a
+  // slot: the allocator / issue warps work per bundle with B * FM lanes active
+  const int B = L.B, lgB = L.lgB, FMB = FM * B;
+  const int CB = C >> lgB;  // bundles per request
   constexpr int SEGB = K * (int)sizeof(T);
   const int row_bytes = F * SEGB;
   const int RSB = L.row_stride, R = L.R, NX = L.NX, nch = L.nch, Pc = L.Pc;
+  const int nchB = nch * B;
   uint64_t* full = (uint64_t*)(smem + L.off_bar);
   uint64_t* pdone = full + CR_MAXX;
   uint64_t* mfree = pdone + CR_MAXX;
   uint64_t* meta = mfree + CR_MAXX;
   uint32_t* ptab = (uint32_t*)(smem + L.off_ptab);  // candidate pairs: f1 | f2 << 8 | pos << 16
+  uint16_t* stab = (uint16_t*)(smem + L.off_stab);  // staged column -> source (see merge warps)
   int* my_cnt = (int*)(smem + L.off_cnt);
   unsigned char* slots = smem + L.off_slot;
   unsigned char* ring = smem + L.off_ring;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const T* lrt = (const T*)p.lr;
-  const T* ffm = (const T*)p.ffm;
 
-  // candidate-pair table in global pair order (position = index into pairs)
+  // candidate-pair table in global pair order (position = index into pairs) and
+  // the staged row's source per column: 0x6000 = lr_out, 0x4000 = zero padding,
+  // 0x8000 | pos = cached ctx x ctx pair, else the candidate pair's index
+  // pair warps per bundle (each arrives on pdone once): as computed by the pair warps
+  int pd_count;
+  {
+    int G = 1;
+    while (2 * G <= CR_GT && NX % (2 * G) == 0 && 2 * G <= CB) G *= 2;
+    pd_count = CR_NPW / G < nchB ? CR_NPW / G : nchB;
+  }
   if (threadIdx.x == 0) {
     int n = 0, pos = 0;
+    stab[0] = 0x6000;
     for (int f1 = 0; f1 < F; ++f1)
-      for (int f2 = f1 + 1; f2 < F; ++f2, ++pos)
-        if (f2 >= Fc) ptab[n++] = (uint32_t)f1 | ((uint32_t)f2 << 8) | ((uint32_t)pos << 16);
+      for (int f2 = f1 + 1; f2 < F; ++f2, ++pos) {
+        if (f2 >= Fc) {
+          stab[1 + pos] = (uint16_t)n;
+          ptab[n++] = (uint32_t)f1 | ((uint32_t)f2 << 8) | ((uint32_t)pos << 16);
+        } else {
+          stab[1 + pos] = (uint16_t)(0x8000 | pos);
+        }
+      }
+    for (int c = D; c < p.Kp; ++c) stab[c] = 0x4000;
     for (int b = 0; b < NX; ++b) {
       mbar_init(&full[b], CR_NISS);
       mbar_init(&meta[b], 1);
-      mbar_init(&pdone[b], nch);
-      mbar_init(&mfree[b], 1);
+      mbar_init(&pdone[b], pd_count);
+      mbar_init(&mfree[b], B);
     }
     mbar_fence_init();
   }
   __syncthreads();
 
   const int64_t my_req = q.R > blockIdx.x ? (q.R - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t my_n = my_req * C;
+  const int64_t my_n = my_req * C;    // candidates of this CTA
+  const int64_t my_nb = my_req * CB;  // bundles
   auto slot = [&](int xs) { return slots + (size_t)xs * L.slot_bytes; };
   auto cache = [&](int64_t t) { return smem + L.off_cache + (size_t)(t & 1) * L.cache_bytes; };
-  auto cand_e = [&](int64_t i) {  // global candidate number of local candidate i
-    const int t = (int)((uint32_t)i / (uint32_t)C);  // i < 2^31 (host check): 32-bit divide
-    return ((int64_t)blockIdx.x + (int64_t)t * gridDim.x) * C + (i - (int64_t)t * C);
-  };
 
   if (warp >= CR_NPW + 1 + CR_NISS) {
     // ================================================================ merge warps
+    // one candidate per warp; its bundle's slot / phase follow from the bundle
+    // number (a warp never waits on a phase it has no candidate in, and a slot
+    // cannot advance past a phase before every candidate of it is merged).
+    // The warp is a latency chain per candidate (LR loads -> f64 reductions ->
+    // sqrt / reciprocal -> row), so the next candidate's LR terms are loaded
+    // before this candidate's row is written (its metadata only depends on
+    // merges of older candidates: no cycle).
     const int mw = warp - CR_NPW - 1 - CR_NISS;
     const float bias = load_elem<T>(lrt + p.n_buckets, p.dlr);
-    int xs = mw % NX;
-    uint32_t par = (uint32_t)((mw / NX) & 1);
-    for (int64_t i = mw; i < my_n; i += CR_NMW) {
-      const int64_t e = cand_e(i);
-      unsigned char* sb = slot(xs);
-      const int* sidx = (const int*)(sb + L.s_sidx);
-      const float* sval = (const float*)(sb + L.s_sval);
-      mbar_wait(&meta[xs], par);
-      float lw = 0.f, lx = 0.f;
+    const int lgNX = 31 - __clz(NX);
+    const double rD = 1.0 / (double)D;
+    CrCursor cu{0, 0};
+    cu.advance(mw, C);
+    float lw = 0.f, lx = 0.f;
+    auto lr_terms = [&](int64_t i) {  // LR weight / value of lane's slot of candidate i
+      const int64_t ib = i >> lgB;
+      const int xs = (int)(ib & (NX - 1));
+      const unsigned char* sb = slot(xs);
+      mbar_wait(&meta[xs], (uint32_t)((ib >> lgNX) & 1));
+      lw = 0.f;
+      lx = 0.f;
       if (lane < FM) {
-        const int j = sidx[lane];
-        lx = j >= 0 ? sval[lane] : 0.f;
-        lw = j >= 0 ? load_elem<T>(lrt + j, p.dlr) : 0.f;
+        const int sub = (int)(i & (B - 1));
+        const int j = ((const int*)(sb + L.s_sidx))[sub * FM + lane];
+        if (j >= 0) {
+          lx = ((const float*)(sb + L.s_sval))[sub * FM + lane];
+          lw = load_elem<T>(lrt + j, p.dlr);
+        }
       }
+    };
+    if (mw < my_n) lr_terms(mw);
+    for (int64_t i = mw; i < my_n; i += CR_NMW, cu.advance(CR_NMW, C)) {
+      const int64_t e = cu.cand(C);
+      const int64_t ib = i >> lgB;
+      const int sub = (int)(i & (B - 1));
+      const int xs = (int)(ib & (NX - 1));
+      const uint32_t par = (uint32_t)((ib >> lgNX) & 1);
+      unsigned char* sb = slot(xs);
       mbar_wait(&pdone[xs], par);
-      const unsigned char* cb = cache((uint32_t)i / (uint32_t)C);
+      const unsigned char* cb = cache(cu.t);
       const float* cpx = (const float*)(cb + L.c_cpx);
-      const float* xv = (const float*)(sb + L.s_xv);
+      const float* xv = (const float*)(sb + L.s_xv) + sub * L.xv_stride;
       // candidate pairs land in xv in ptab order; the ctx x ctx pairs' sum and
       // sum of squares come from the cache (f64, computed once per request)
       const double* cst = (const double*)(cb + L.c_lr);  // lr partial, sum v, sum v^2, bad
@@ -279,10 +354,11 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
         ps += (double)v;
         pbad |= !isfinite(v);
       }
+      const double lrc = warp_sum((double)lx * (double)lw);
       const double psum = warp_sum(ps) + cst[1];
       pbad = __any_sync(0xffffffffu, pbad) | (cst[3] != 0.0);
-      const double lr_out = (double)bias + cst[0] + warp_sum((double)lx * (double)lw);  // M:327
-      const double mu = (psum + lr_out) / D;
+      const double lr_out = (double)bias + cst[0] + lrc;  // M:327
+      const double mu = (psum + lr_out) * rD;
       // population variance (M:359): candidate deviations two-pass, the ctx x ctx
       // block through its cached moments: sum (v-mu)^2 = S2 - 2 mu S1 + n mu^2
       double s2 = 0.0;
@@ -293,23 +369,29 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
       const int nctx = P - Pc;
       s2 = warp_sum(s2) + (cst[2] - 2.0 * mu * cst[1] + (double)nctx * mu * mu) +
            (lr_out - mu) * (lr_out - mu);
-      const double rden = 1.0 / (sqrt(s2 / D) + 1e-6);
+      const double rden = 1.0 / (sqrt(s2 * rD) + 1e-6);
       const float m0 = (float)((lr_out - mu) * rden);
-      int mbad = !isfinite(m0);
-      // ctx positions and padding first, then the candidate positions overwrite theirs
-      for (int c = lane; c < p.Kp; c += 32) {
-        float m = 0.f;
-        if (c == 0) m = m0;
-        else if (c < D) m = (float)(((double)cpx[c - 1] - mu) * rden);
-        mbad |= !isfinite(m);
-        xstore1(p.xout, p.xplane, e * p.Kp + c, m);
-      }
-      __syncwarp();
-      for (int t = lane; t < Pc; t += 32) {
-        const int pos = (int)(ptab[t] >> 16);
-        const float m = (float)(((double)xv[t] - mu) * rden);
-        mbad |= !isfinite(m);
-        xstore1(p.xout, p.xplane, e * p.Kp + 1 + pos, m);
+      if (i + CR_NMW < my_n) lr_terms(i + CR_NMW);  // next candidate's LR loads in flight
+      // The standardised row in global pair order, four columns per lane.  The
+      // element arithmetic is two-float f32: (v - mu_hi) - mu_lo keeps the
+      // cancellation exact to 2^-24 of the difference, so the row carries more
+      // bits than the fp16 hi/lo planes it is staged in (22).
+      const float muh = (float)mu, mul = (float)(mu - (double)muh), rdf = (float)rden;
+      int mbad = 0;
+      for (int qd = lane; qd < (p.Kp >> 2); qd += 32) {
+        const uint2 cd = *(const uint2*)(stab + 4 * qd);
+        const uint32_t code[4] = {cd.x & 0xFFFFu, cd.x >> 16, cd.y & 0xFFFFu, cd.y >> 16};
+        float v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float* src = (code[t] & 0x8000u) ? cpx : xv;
+          const float raw = src[code[t] & 0x3FFu];
+          float m = ((raw - muh) - mul) * rdf;
+          if (code[t] & 0x4000u) m = (code[t] & 0x2000u) ? m0 : 0.f;
+          mbad |= !isfinite(m);
+          v[t] = m;
+        }
+        xstore4(p.xout, p.xplane, e * p.Kp + 4 * qd, v);
       }
       mbad = __any_sync(0xffffffffu, mbad);
       if (lane == 0) {
@@ -318,21 +400,19 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&mfree[xs]);
-      xs += CR_NMW;
-      while (xs >= NX) { xs -= NX; par ^= 1u; }
     }
   } else if (warp > CR_NPW) {
     // ================================================================ TMA issue warps
     const int iw = warp - CR_NPW - 1;
     int xs = 0;
     uint32_t par = 0;
-    for (int64_t i = 0; i < my_n; ++i) {
+    for (int64_t i = 0; i < my_nb; ++i) {
       mbar_wait(&meta[xs], par);
       const unsigned char* sb = slot(xs);
       const int* sidx = (const int*)(sb + L.s_sidx);
       const uint16_t* rpos = (const uint16_t*)(sb + L.s_rpos);
       const int s = iw + CR_NISS * lane;
-      const int r = s < FM ? (int)rpos[s] : 0xFFFF;
+      const int r = s < FMB ? (int)rpos[s] : 0xFFFF;
       const int mine = __popc(__ballot_sync(0xffffffffu, r != 0xFFFF));
       if (lane == 0) {
         if (mine) mbar_arrive_expect_tx(&full[xs], (uint32_t)(mine * row_bytes));
@@ -346,14 +426,16 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
     }
   } else if (warp == CR_NPW) {
     // ================================================================ allocator warp
-    int* pidx = (int*)(smem + L.off_pidx);  // [IDXD][idx FM | val FM]
+    int* pidx = (int*)(smem + L.off_pidx);  // [IDXD][idx FMB | val FMB]
+    CrCursor ahead{0, 0};  // bundle being streamed in
     auto issue_ex = [&](int64_t i) {
-      if (i < my_n && lane < FM) {
-        const int64_t e = cand_e(i);
-        int* d = pidx + (int)(i & (CR_IDXD - 1)) * 2 * FM;
-        cp_async4(d + lane, q.didx + e * FM + lane);
-        cp_async4(d + FM + lane, q.dval + e * FM + lane);
+      if (i < my_nb && lane < FMB) {
+        const int64_t e0 = ahead.cand(C);
+        int* d = pidx + (int)(i & (CR_IDXD - 1)) * 2 * FMB;
+        cp_async4(d + lane, q.didx + e0 * FM + lane);
+        cp_async4(d + FMB + lane, q.dval + e0 * FM + lane);
       }
+      ahead.advance(B, C);
       cp_async_commit();
     };
 #pragma unroll 1
@@ -363,19 +445,19 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
     const uint32_t lt = (1u << lane) - 1u;
     int xs = 0, ts = 0;
     uint32_t fpar = 1, tpar = 0;
-    for (int64_t i = 0; i < my_n; ++i) {
-      const int64_t e = cand_e(i);
+    CrCursor cu{0, 0};
+    for (int64_t i = 0; i < my_nb; ++i, cu.advance(B, C)) {
       cp_async_wait<CR_IDXD - 1>();
-      const int* d = pidx + (int)(i & (CR_IDXD - 1)) * 2 * FM;
-      int j = lane < FM ? d[lane] : -1;
-      const float x = lane < FM ? __int_as_float(d[FM + lane]) : 0.f;
-      int bad = 0;
-      if (j >= p.n_buckets || j < -1) { bad = 1; j = -1; }
-      issue_ex(i + CR_IDXD);
-      if (__any_sync(0xffffffffu, bad) && lane == 0)
+      const int* d = pidx + (int)(i & (CR_IDXD - 1)) * 2 * FMB;
+      int j = lane < FMB ? d[lane] : -1;
+      const float x = lane < FMB ? __int_as_float(d[FMB + lane]) : 0.f;
+      if (j >= p.n_buckets || j < -1) {  // ContractError at this lane's candidate
         atomicMin((unsigned long long*)p.status,
-                  (unsigned long long)status_key(p.status_base + e, DFFM_BLOCK_NONE,
-                                                 DFFM_CONTRACT));
+                  (unsigned long long)status_key(p.status_base + cu.cand(C) + lane / FM,
+                                                 DFFM_BLOCK_NONE, DFFM_CONTRACT));
+        j = -1;
+      }
+      issue_ex(i + CR_IDXD);
       const uint32_t mask = __ballot_sync(0xffffffffu, j >= 0);
       const int cnt = __popc(mask);
       if (i >= NX) {
@@ -399,7 +481,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
         if (++ts == NX) { ts = 0; tpar ^= 1u; }
       }
       unsigned char* sb = slot(xs);
-      if (lane < FM) {
+      if (lane < FMB) {
         int r = head + __popc(mask & lt);
         if (r >= R) r -= R;
         ((int*)(sb + L.s_sidx))[lane] = j;
@@ -417,115 +499,193 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
     cp_async_wait<0>();
   } else {
     // ================================================================ pair warps
-    // G groups of npg warps; group g takes candidates g, g+G, ... (chunk c of
-    // a candidate on warp c % npg of the group).  Phase-safe: G divides NX, so
-    // a group revisits a slot only through its own candidates, and every warp
-    // of a group has a chunk in each of the group's candidates.
+    // G groups of npg warps; group g takes bundles g, g+G, ... (chunk c of a
+    // bundle -- chunk c % nch of its candidate c / nch -- on warp c % npg of the
+    // group; each warp arrives on pdone once per bundle).  Phase-safe: G divides
+    // NX, so a group revisits a slot only through its own bundles, and every warp
+    // of a group has a chunk in each of them.
     int G = 1;
-    while (2 * G <= CR_GT && NX % (2 * G) == 0 && 2 * G <= C) G *= 2;
-    const int npg = CR_NPW / G < nch ? CR_NPW / G : nch;
+    while (2 * G <= CR_GT && NX % (2 * G) == 0 && 2 * G <= CB) G *= 2;
+    const int npg = CR_NPW / G < nchB ? CR_NPW / G : nchB;
     const int gw = warp / npg, wi = warp - gw * npg;
     if (gw >= G) return;
-    int64_t i = gw;
-    int c = wi, xs = gw;
+    int xs = gw;
     uint32_t par = 0;
-    int64_t cur = -1, cur_req = -1;
-    const unsigned char* sb = nullptr;
+    int64_t cur_req = -1;
+    CrCursor cu{0, 0};  // in bundles: w = bundle within the request
+    cu.advance(gw, CB);
     const unsigned char* cb = nullptr;
     const int tid = warp * 32 + lane, nthr = G * npg * 32;
-    for (; i < my_n;) {
-      if (i != cur) {
-        const int64_t t = (uint32_t)i / (uint32_t)C;
-        if (t != cur_req) {
-          // ---- build_context_cache for request t, buffer t & 1
-          cur_req = t;
-          const int64_t r = (int64_t)blockIdx.x + t * gridDim.x;
-          unsigned char* wb = cache(t);
-          named_bar_sync(1, nthr);  // every pair warp is past request t-1
-          if (q.cache_in) {  // prebuilt (dffm_ctx_build): copy the request's cache blob
-            const uint4* src = (const uint4*)(q.cache_in + (size_t)r * L.cache_bytes);
-            for (int v = tid; v < L.cache_bytes / 16; v += nthr) ((uint4*)wb)[v] = __ldg(src + v);
-            named_bar_sync(1, nthr);
-          } else {
-            cr_build_cache<T>(wb, q, L, r, p.status_base + r * C, tid, nthr);
-          }
-          cb = wb;
-        }
-        mbar_wait(&full[xs], par);
-        cur = i;
-        sb = slot(xs);
-      }
-      const float* S = (const float*)(cb + L.c_S);
-      const unsigned char* cpres = cb + L.c_pres;
-      const float* sval = (const float*)(sb + L.s_sval);
-      const uint16_t* rpos = (const uint16_t*)(sb + L.s_rpos);
-      float* xv = (float*)(sb + L.s_xv);
-      const int t = c * CR_CHUNK + lane;
-      if (t < Pc) {
-        const uint32_t pr = ptab[t];
-        const int f1 = pr & 0xFF, f2 = (pr >> 8) & 0xFF;
-        constexpr int PER = 16 / (int)sizeof(T);
-        float a[K], bb[K];
+    constexpr int PER = 16 / (int)sizeof(T);
+    // One slot per candidate field and one warp per chunk (npg == nch): warp wi
+    // owns pairs wi*32 .. wi*32+31 of EVERY candidate, so the pair's fields and,
+    // for a context x candidate pair, the cached S[x][c] segment stay in registers
+    // for the whole request; per candidate only the candidate row's segment is
+    // read.  pair = x_c * <S[x][c], w_c[x]> (x_c = 1.0 for categorical fields:
+    // the same bits as scaling the row first, as K1 v8 does for M == 1).
+    const bool fixed = (M == 1) && npg == nch;
+    const int tf = wi * CR_CHUNK + lane;
+    const bool valid = fixed && tf < Pc;
+    const uint32_t prf = valid ? ptab[tf] : 0u;
+    const int ff1 = prf & 0xFF, ff2 = (prf >> 8) & 0xFF;
+    const bool isctx = ff1 < Fc;
+    const bool allctx = __all_sync(0xffffffffu, isctx || !valid);
+    float areg[K];
+    bool p1c = false;
 #pragma unroll
-        for (int u = 0; u < K; ++u) { a[u] = 0.f; bb[u] = 0.f; }
-        bool p1 = false, p2 = false;
-        const int c2 = f2 - Fc;
-#pragma unroll
-        for (int m = 0; m < M; ++m) {  // candidate field f2: its slots' segment f1
-          const int r2 = rpos[c2 * M + m];
-          if (r2 != 0xFFFF) {
-            p2 = true;
-            const float x2 = sval[c2 * M + m];
-            const unsigned char* q2 = ring + (size_t)r2 * RSB + f1 * SEGB;
-#pragma unroll
-            for (int u = 0; u < SEGB / 16; ++u) {
-              float w[PER];
-              unpack16<T>(*(const uint4*)(q2 + u * 16), w, p.dffm);
-#pragma unroll
-              for (int v = 0; v < PER; ++v) bb[u * PER + v] = fmaf(x2, w[v], bb[u * PER + v]);
-            }
-          }
-        }
-        if (f1 < Fc) {  // context field: the cached S[x][c]
-          p1 = cpres[f1] != 0;
-          const float* sc = S + (f1 * F + f2) * K;
-#pragma unroll
-          for (int u = 0; u < K; ++u) a[u] = sc[u];
+    for (int u = 0; u < K; ++u) areg[u] = 0.f;
+    for (int64_t i = gw; i < my_nb; i += G, cu.advance(G, CB)) {
+      if (cu.t != cur_req) {
+        // ---- build_context_cache for request t, buffer t & 1
+        cur_req = cu.t;
+        const int64_t r = (int64_t)blockIdx.x + cur_req * gridDim.x;
+        unsigned char* wb = cache(cur_req);
+        named_bar_sync(1, nthr);  // every pair warp is past request t-1
+        if (q.cache_in) {  // prebuilt (dffm_ctx_build): copy the request's cache blob
+          const uint4* src = (const uint4*)(q.cache_in + (size_t)r * L.cache_bytes);
+          for (int v = tid; v < L.cache_bytes / 16; v += nthr) ((uint4*)wb)[v] = __ldg(src + v);
+          named_bar_sync(1, nthr);
         } else {
-          const int c1 = f1 - Fc;
+          cr_build_cache<T>(wb, q, L, r, p.status_base + r * C, tid, nthr);
+        }
+        cb = wb;
+        if (valid && isctx) {
+          const float* sc = (const float*)(cb + L.c_S) + (ff1 * F + ff2) * K;
 #pragma unroll
-          for (int m = 0; m < M; ++m) {
-            const int r1 = rpos[c1 * M + m];
-            if (r1 != 0xFFFF) {
-              p1 = true;
-              const float x1 = sval[c1 * M + m];
-              const unsigned char* q1 = ring + (size_t)r1 * RSB + f2 * SEGB;
+          for (int u = 0; u < K; ++u) areg[u] = sc[u];
+          p1c = (cb + L.c_pres)[ff1] != 0;
+        }
+      }
+      mbar_wait(&full[xs], par);
+      const unsigned char* sb = slot(xs);
+      if (fixed) {
+        if (valid) {
+          const int c2 = ff2 - Fc, c1 = ff1 - Fc;
+          if (allctx) {
+#pragma unroll 4
+            for (int sub = 0; sub < B; ++sub) {
+              const int r2 = ((const uint16_t*)(sb + L.s_rpos))[sub * FM + c2];
+              const float x2 = ((const float*)(sb + L.s_sval))[sub * FM + c2];
+              const bool p2 = r2 != 0xFFFF;
+              const unsigned char* q2 = ring + (size_t)(p2 ? r2 : 0) * RSB + ff1 * SEGB;
+              float d = 0.f;
 #pragma unroll
               for (int u = 0; u < SEGB / 16; ++u) {
                 float w[PER];
-                unpack16<T>(*(const uint4*)(q1 + u * 16), w, p.dffm);
+                unpack16<T>(*(const uint4*)(q2 + u * 16), w, p.dffm);
 #pragma unroll
-                for (int v = 0; v < PER; ++v) a[u * PER + v] = fmaf(x1, w[v], a[u * PER + v]);
+                for (int v = 0; v < PER; ++v) d = fmaf(areg[u * PER + v], w[v], d);
               }
+              // inactive pairs stay exactly 0 (M:346-351)
+              ((float*)(sb + L.s_xv))[sub * L.xv_stride + tf] =
+                  (p1c && p2) ? (x2 == 1.f ? d : x2 * d) : 0.f;
+            }
+          } else {
+            for (int sub = 0; sub < B; ++sub) {
+              const uint16_t* rpos = (const uint16_t*)(sb + L.s_rpos) + sub * FM;
+              const float* sval = (const float*)(sb + L.s_sval) + sub * FM;
+              const int r2 = rpos[c2];
+              const bool p2 = r2 != 0xFFFF;
+              const unsigned char* q2 = ring + (size_t)(p2 ? r2 : 0) * RSB + ff1 * SEGB;
+              float w2[K];
+#pragma unroll
+              for (int u = 0; u < SEGB / 16; ++u)
+                unpack16<T>(*(const uint4*)(q2 + u * 16), w2 + u * PER, p.dffm);
+              float d = 0.f, xs_ = sval[c2];
+              bool p1 = p1c;
+              if (isctx) {
+#pragma unroll
+                for (int u = 0; u < K; ++u) d = fmaf(areg[u], w2[u], d);
+              } else {
+                const int r1 = rpos[c1];
+                p1 = r1 != 0xFFFF;
+                xs_ *= sval[c1];
+                const unsigned char* q1 = ring + (size_t)(p1 ? r1 : 0) * RSB + ff2 * SEGB;
+#pragma unroll
+                for (int u = 0; u < SEGB / 16; ++u) {
+                  float w[PER];
+                  unpack16<T>(*(const uint4*)(q1 + u * 16), w, p.dffm);
+#pragma unroll
+                  for (int v = 0; v < PER; ++v) d = fmaf(w[v], w2[u * PER + v], d);
+                }
+              }
+              ((float*)(sb + L.s_xv))[sub * L.xv_stride + tf] =
+                  (p1 && p2) ? (xs_ == 1.f ? d : xs_ * d) : 0.f;
             }
           }
         }
-        float pv = 0.f;
-        if (p1 && p2) {  // inactive pairs stay exactly 0 (M:346-351)
+      } else {
+        const float* S = (const float*)(cb + L.c_S);
+        const unsigned char* cpres = cb + L.c_pres;
+        int sub = wi / nch, cc = wi - sub * nch;
+        for (int c = wi; c < nchB; c += npg) {
+          const float* sval = (const float*)(sb + L.s_sval) + sub * FM;
+          const uint16_t* rpos = (const uint16_t*)(sb + L.s_rpos) + sub * FM;
+          float* xv = (float*)(sb + L.s_xv) + sub * L.xv_stride;
+          const int t = cc * CR_CHUNK + lane;
+          if (t < Pc) {
+            const uint32_t pr = ptab[t];
+            const int f1 = pr & 0xFF, f2 = (pr >> 8) & 0xFF;
+            float a[K], bb[K];
 #pragma unroll
-          for (int u = 0; u < K; ++u) pv = fmaf(a[u], bb[u], pv);
+            for (int u = 0; u < K; ++u) { a[u] = 0.f; bb[u] = 0.f; }
+            bool p1 = false, p2 = false;
+            const int c2 = f2 - Fc;
+#pragma unroll
+            for (int m = 0; m < M; ++m) {  // candidate field f2: its slots' segment f1
+              const int r2 = rpos[c2 * M + m];
+              if (r2 != 0xFFFF) {
+                p2 = true;
+                const float x2 = sval[c2 * M + m];
+                const unsigned char* q2 = ring + (size_t)r2 * RSB + f1 * SEGB;
+#pragma unroll
+                for (int u = 0; u < SEGB / 16; ++u) {
+                  float w[PER];
+                  unpack16<T>(*(const uint4*)(q2 + u * 16), w, p.dffm);
+#pragma unroll
+                  for (int v = 0; v < PER; ++v) bb[u * PER + v] = fmaf(x2, w[v], bb[u * PER + v]);
+                }
+              }
+            }
+            if (f1 < Fc) {  // context field: the cached S[x][c]
+              p1 = cpres[f1] != 0;
+              const float* sc = S + (f1 * F + f2) * K;
+#pragma unroll
+              for (int u = 0; u < K; ++u) a[u] = sc[u];
+            } else {
+              const int c1 = f1 - Fc;
+#pragma unroll
+              for (int m = 0; m < M; ++m) {
+                const int r1 = rpos[c1 * M + m];
+                if (r1 != 0xFFFF) {
+                  p1 = true;
+                  const float x1 = sval[c1 * M + m];
+                  const unsigned char* q1 = ring + (size_t)r1 * RSB + f2 * SEGB;
+#pragma unroll
+                  for (int u = 0; u < SEGB / 16; ++u) {
+                    float w[PER];
+                    unpack16<T>(*(const uint4*)(q1 + u * 16), w, p.dffm);
+#pragma unroll
+                    for (int v = 0; v < PER; ++v) a[u * PER + v] = fmaf(x1, w[v], a[u * PER + v]);
+                  }
+                }
+              }
+            }
+            float pv = 0.f;
+            if (p1 && p2) {  // inactive pairs stay exactly 0 (M:346-351)
+#pragma unroll
+              for (int u = 0; u < K; ++u) pv = fmaf(a[u], bb[u], pv);
+            }
+            xv[t] = pv;
+          }
+          cc += npg;
+          while (cc >= nch) { cc -= nch; ++sub; }
         }
-        xv[t] = pv;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&pdone[xs]);
-      c += npg;
-      if (c >= nch) {
-        c = wi;
-        i += G;
-        xs += G;
-        if (xs >= NX) { xs -= NX; par ^= 1u; }
-      }
+      xs += G;
+      if (xs >= NX) { xs -= NX; par ^= 1u; }
     }
   }
 }
