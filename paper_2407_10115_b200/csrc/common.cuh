@@ -189,6 +189,21 @@ __device__ __forceinline__ float load_elem<uint16_t>(const uint16_t* p, const De
   return deq(*p, d);
 }
 
+// Raw table element -> float (the conversion split from the load, so a warp can
+// keep the load in flight and convert where the value is consumed)
+template <typename T>
+__device__ __forceinline__ float elem_to_float(T raw, const Deq& d);
+template <>
+__device__ __forceinline__ float elem_to_float<float>(float raw, const Deq&) { return raw; }
+template <>
+__device__ __forceinline__ float elem_to_float<__nv_bfloat16>(__nv_bfloat16 raw, const Deq&) {
+  return __bfloat162float(raw);
+}
+template <>
+__device__ __forceinline__ float elem_to_float<uint16_t>(uint16_t raw, const Deq& d) {
+  return deq(raw, d);
+}
+
 // Unpack one 16-byte chunk of T into floats
 template <typename T>
 __device__ __forceinline__ void unpack16(const uint4& u, float* o, const Deq& d);

@@ -315,20 +315,22 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
     const double rD = 1.0 / (double)D;
     CrCursor cu{0, 0};
     cu.advance(mw, C);
-    float lw = 0.f, lx = 0.f;
+    T lraw = T();  // this lane's LR weight as stored (converted where it is consumed)
+    float lx = 0.f;
+    bool lp = false;
     auto lr_terms = [&](int64_t i) {  // LR weight / value of lane's slot of candidate i
       const int64_t ib = i >> lgB;
       const int xs = (int)(ib & (NX - 1));
       const unsigned char* sb = slot(xs);
       mbar_wait(&meta[xs], (uint32_t)((ib >> lgNX) & 1));
-      lw = 0.f;
-      lx = 0.f;
+      lp = false;
       if (lane < FM) {
         const int sub = (int)(i & (B - 1));
         const int j = ((const int*)(sb + L.s_sidx))[sub * FM + lane];
         if (j >= 0) {
+          lp = true;
           lx = ((const float*)(sb + L.s_sval))[sub * FM + lane];
-          lw = load_elem<T>(lrt + j, p.dlr);
+          lraw = __ldg(lrt + j);
         }
       }
     };
@@ -354,7 +356,8 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
         ps += (double)v;
         pbad |= !isfinite(v);
       }
-      const double lrc = warp_sum((double)lx * (double)lw);
+      const double lrc =
+          warp_sum(lp ? (double)lx * (double)elem_to_float<T>(lraw, p.dlr) : 0.0);
       const double psum = warp_sum(ps) + cst[1];
       pbad = __any_sync(0xffffffffu, pbad) | (cst[3] != 0.0);
       const double lr_out = (double)bias + cst[0] + lrc;  // M:327
@@ -403,6 +406,10 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
     }
   } else if (warp > CR_NPW) {
     // ================================================================ TMA issue warps
+    // (measured alternative, not kept: the bundle's rows as 16-byte cp.async chunks,
+    // lanes along the row, completing on full[xs] through
+    // cp.async.mbarrier.arrive.noinc -- cfg4 2.43 ms per step against 2.20 ms with
+    // one bulk copy per 384-byte row, 2 and 4 issue warps alike)
     const int iw = warp - CR_NPW - 1;
     int xs = 0;
     uint32_t par = 0;

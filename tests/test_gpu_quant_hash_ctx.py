@@ -161,13 +161,20 @@ def test_context_cache_equals_uncached_forward_u16(ctx_mlp, monkeypatch):
     assert np.abs(p.reshape(-1) - ref).max() <= 1e-6
 
 
-@pytest.mark.parametrize("wdtype,Mc,Md,C", [("f32", 2, 2, 40), ("bf16", 1, 3, 33), ("u16", 3, 1, 64)])
-def test_context_ring_edge_cases_match_oracle(wdtype, Mc, Md, C, monkeypatch):
+@pytest.mark.parametrize("wdtype,Mc,Md,C,Fc,Fd", [
+    ("f32", 2, 2, 40, 10, 6), ("bf16", 1, 3, 33, 10, 6),  # C < 64: K3 v1
+    ("u16", 3, 1, 64, 10, 6),    # ring, bundles of 4, several chunks per pair warp
+    ("f32", 2, 2, 72, 10, 6),    # ring, 2 slots per candidate field, bundles of 2
+    ("bf16", 1, 3, 65, 10, 6),   # ring, 3 slots per candidate field, odd C: no bundling
+    ("u16", 2, 1, 96, 16, 8),    # ring, cfg4 field split: one chunk per pair warp (register-resident context segments), bundles of 4
+    ("f32", 1, 1, 66, 16, 8),    # the same path, bundles of 2
+])
+def test_context_ring_edge_cases_match_oracle(wdtype, Mc, Md, C, Fc, Fd, monkeypatch):
     """K3 v2 with multi-slot context and candidate fields, absent context and
-    candidate fields, empty candidates; every table dtype; vs the oracle."""
+    candidate fields, empty candidates; every table dtype and every bundle size;
+    vs the oracle."""
     monkeypatch.delenv("DFFM_CTX_MLP", raising=False)
     bits = 12
-    Fc, Fd = 10, 6
     F = Fc + Fd
     ost = fo.random_store(F, 8, (32, 16), bits, seed=Mc * 10 + Md)
     cfg = ModelConfig(n_fields=F, k=8, hidden_sizes=(32, 16), hash_bits=bits)
@@ -194,6 +201,8 @@ def test_context_ring_edge_cases_match_oracle(wdtype, Mc, Md, C, monkeypatch):
     ci[2] = -1  # a request without context features
     di = slots((R, C, Fd), Md)
     di[:, ::7] = -1  # empty candidates
+    di[:, 1::5, Fd // 2] = -1  # an absent candidate field
+    ci[4, Fc // 3] = -1  # an absent context field
     cv = np.where(ci >= 0, rng.lognormal(size=ci.shape), 0).astype(np.float32)
     dv = np.where(di >= 0, rng.lognormal(size=di.shape), 0).astype(np.float32)
     p = inference.score_requests(ci, cv, di, dv, st).cpu().numpy()
