@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from .errors import ContractError, StaleCacheError
-from .model import WeightStore, _as_device, _status
+from .model import StatusWord, WeightStore, _as_device, _status
 
 
 @dataclass
@@ -119,7 +119,98 @@ def score_requests(ctx_idx, ctx_val, cand_idx, cand_val, store: WeightStore,
     return _score(None, ctx_idx, ctx_val, cand_idx, cand_val, store, out, check)
 
 
-def _score(blob, ctx_idx, ctx_val, cand_idx, cand_val, store, out, check):
+class HostRequestScorer:
+    """Host-buffer entry point of K3: pinned host requests in, host probabilities out.
+
+    The requests are cut into chunks (multiples of the SM count, so every CTA of the
+    ring kernel gets the same number of requests); chunk j+1's contexts and
+    candidates cross PCIe on the copy stream while K3 scores chunk j on the compute
+    stream and chunk j-1's probabilities return on a third stream (two device
+    staging buffers in flight).  ``bench.py --workload cfg4`` reports its ``e2e``
+    through this call."""
+
+    def __init__(self, store: WeightStore, n_ctx_fields: int, ctx_m: int, n_cand: int,
+                 cand_m: int, chunk_requests: int = 296):
+        self.store = store
+        dev = store.device
+        Fd = store.config.n_fields - n_ctx_fields
+        if n_ctx_fields < 1 or Fd < 1:
+            raise ContractError("context fields must be a non-empty proper prefix of the model's")
+        self.shape = (n_ctx_fields, ctx_m, n_cand, Fd, cand_m)
+        self.chunk = max(1, int(chunk_requests))
+        q = self.chunk
+        self.ci = [torch.empty((q, n_ctx_fields, ctx_m), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.cv = [torch.empty((q, n_ctx_fields, ctx_m), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.di = [torch.empty((q, n_cand, Fd, cand_m), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.dv = [torch.empty((q, n_cand, Fd, cand_m), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.prob = [torch.empty((q, n_cand), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(dev)
+        self.compute_stream = torch.cuda.Stream(dev)
+        self.out_stream = torch.cuda.Stream(dev)
+        self.status = StatusWord(dev)
+
+    def __call__(self, ctx_idx: torch.Tensor, ctx_val: torch.Tensor, cand_idx: torch.Tensor,
+                 cand_val: torch.Tensor, out_host: torch.Tensor, check: bool = True) -> torch.Tensor:
+        Fc, Mc, C, Fd, Md = self.shape
+        R = int(ctx_idx.shape[0])
+        if tuple(ctx_idx.shape) != (R, Fc, Mc) or tuple(cand_idx.shape) != (R, C, Fd, Md):
+            raise ContractError(f"request layout {tuple(ctx_idx.shape)} / {tuple(cand_idx.shape)} does "
+                                f"not match [R, {Fc}, {Mc}] / [R, {C}, {Fd}, {Md}]")
+        lib = _lib.lib()
+        cm = self.store.c_model_ref()
+        cs, ks, os_ = self.copy_stream, self.compute_stream, self.out_stream
+        ks.wait_stream(torch.cuda.current_stream(self.store.device))
+        with torch.cuda.stream(ks):
+            self.status.clear()
+        cs.wait_stream(ks)
+        h2d = [torch.cuda.Event(), torch.cuda.Event()]
+        scored = [torch.cuda.Event(), torch.cuda.Event()]
+        drained = [torch.cuda.Event(), torch.cuda.Event()]
+        # a short first chunk, so the first (unoverlapped) copy is short
+        bounds, r0 = [], 0
+        first = max(1, self.chunk // 2)
+        while r0 < R:
+            r1 = min(R, r0 + (first if not bounds else self.chunk))
+            bounds.append((r0, r1))
+            r0 = r1
+        for j, (r0, r1) in enumerate(bounds):
+            b, n = j & 1, r1 - r0
+            with torch.cuda.stream(cs):
+                if j >= 2:
+                    cs.wait_event(scored[b])  # the staging buffers of chunk j-2 are free
+                self.ci[b][:n].copy_(ctx_idx[r0:r1], non_blocking=True)
+                self.cv[b][:n].copy_(ctx_val[r0:r1], non_blocking=True)
+                self.di[b][:n].copy_(cand_idx[r0:r1], non_blocking=True)
+                self.dv[b][:n].copy_(cand_val[r0:r1], non_blocking=True)
+                h2d[b].record(cs)
+            with torch.cuda.stream(ks):
+                ks.wait_event(h2d[b])
+                if j >= 2:
+                    ks.wait_event(drained[b])  # prob[b] of chunk j-2 has left
+                rc = lib.dffm_ctx_score(cm, self.ci[b].data_ptr(), self.cv[b].data_ptr(), Fc, Mc,
+                                        self.di[b].data_ptr(), self.dv[b].data_ptr(), Md, n, C,
+                                        self.prob[b].data_ptr(), self.status.ptr(), ks.cuda_stream)
+                _lib.check(rc, "dffm_ctx_score")
+                scored[b].record(ks)
+            with torch.cuda.stream(os_):
+                os_.wait_event(scored[b])
+                out_host[r0:r1].copy_(self.prob[b][:n], non_blocking=True)
+                drained[b].record(os_)
+        ks.wait_stream(os_)
+        with torch.cuda.stream(ks):
+            self.status.fetch_async()
+        ks.synchronize()
+        if check and int(self.status.host.item()) != -1:
+            # the status word holds chunk-local candidate numbers: find the first
+            # failing chunk again, serially, and report the stream-global candidate
+            for r0, r1 in bounds:
+                _score(None, ctx_idx[r0:r1], ctx_val[r0:r1], cand_idx[r0:r1], cand_val[r0:r1],
+                       self.store, None, True, base=r0 * C)
+            self.status.raise_if_set("context scorer: ")
+        return out_host
+
+
+def _score(blob, ctx_idx, ctx_val, cand_idx, cand_val, store, out, check, base=0):
     dev = store.device
     ci = _as_device(ctx_idx, torch.int32, dev)
     cv = _as_device(ctx_val, torch.float32, dev)
@@ -148,7 +239,7 @@ def _score(blob, ctx_idx, ctx_val, cand_idx, cand_val, store, out, check):
     if check:
         st.fetch_async()
         s.synchronize()
-        st.raise_if_set("context scorer: ")
+        st.raise_if_set("context scorer: ", base)
     return out
 
 

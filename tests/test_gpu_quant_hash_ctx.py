@@ -276,3 +276,31 @@ def test_prebuilt_context_cache_is_reused_without_a_context_pass():
     bad[3, 0] = 1 << (bits + 2)
     with pytest.raises(ContractError):
         inference.build_context_cache(bad, cv[0], st)
+
+
+def test_host_request_scorer_matches_device_path_and_reports_global_candidate():
+    """inference.HostRequestScorer (pinned host requests, chunked over three streams)
+    returns the bits of score_requests on device tensors; a bad candidate bucket in
+    a later chunk raises ContractError at its stream-global candidate number."""
+    bits = 12
+    F, Fc, C = 24, 16, 68
+    ost = fo.random_store(F, 8, (64, 32), bits, seed=9)
+    cfg = ModelConfig(n_fields=F, k=8, hidden_sizes=(64, 32), hash_bits=bits)
+    st = WeightStore.from_flat(cfg, ost.flat(False), DEV, with_optimizer=False)
+    rng = np.random.default_rng(11)
+    R = 50
+    ci = torch.from_numpy(rng.integers(0, 1 << bits, (R, Fc, 1)).astype(np.int32)).pin_memory()
+    cv = torch.ones((R, Fc, 1)).pin_memory()
+    di = torch.from_numpy(rng.integers(0, 1 << bits, (R, C, F - Fc, 1)).astype(np.int32)).pin_memory()
+    dv = torch.from_numpy(rng.lognormal(size=(R, C, F - Fc, 1)).astype(np.float32)).pin_memory()
+    ref = inference.score_requests(ci, cv, di, dv, st).cpu()
+    hs = inference.HostRequestScorer(st, Fc, 1, C, 1, chunk_requests=12)
+    out = torch.empty((R, C)).pin_memory()
+    hs(ci, cv, di, dv, out)
+    assert torch.equal(out, ref)
+    hs(ci, cv, di, dv, out)  # reusable
+    assert torch.equal(out, ref)
+    di[31, 5, 2, 0] = 1 << bits
+    with pytest.raises(ContractError) as ei:
+        hs(ci, cv, di, dv, out)
+    assert ei.value.example == 31 * C + 5
