@@ -44,7 +44,7 @@ constexpr int TR_CLUSTER = 8;  // CTAs per cluster for the split trainer
 // Phase timestamps (debug builds only, -DDFFM_TR_TRACE): SM clock of thread 0
 // of rank 0 at each phase boundary, for examples [TR_T0, TR_T0 + TR_TN).
 #ifdef DFFM_TR_TRACE
-constexpr int TR_T0 = 16, TR_TN = 64, TR_NPH = 16;
+constexpr int TR_T0 = 16, TR_TN = 64, TR_NPH = 40;
 __device__ long long g_tr_trace[TR_TN * TR_NPH];
 #define TR_MARK(ph)                                                            \
   do {                                                                         \
@@ -91,6 +91,14 @@ struct TrSmem {
 
 __host__ __device__ inline int a16(int x) { return (x + 15) & ~15; }
 
+// S[f][g][c] in shared memory (f64): segment stride k + 1 and an odd row stride, so
+// the strided walks -- pairs read S[f1][f2] / S[f2][f1] with lanes along f2, the
+// backward reads S[g][f] with lanes along g -- spread over the banks.  (With the dense
+// [F][F][k] layout a row is F*k*8 = 1,536 B at cfg3, a multiple of 128: 32-way conflicts
+// made the pair loop 5.2k cycles and the dp/fact loop 5.3k of the 70k per example.)
+__host__ __device__ inline int tr_s_seg(int k) { return k + 1; }
+__host__ __device__ inline int tr_s_row(int F, int k) { return (F * (k + 1)) | 1; }
+
 __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int hsum, int dmax,
                                                  int mlp_floats) {
   TrSmem s;
@@ -100,7 +108,7 @@ __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int
   s.off_sval = o; o = a16(o + FM * 8);
   s.off_pres = o; o = a16(o + F * 4);
   s.off_lrp = o; o = a16(o + F * 8);
-  s.off_S = o; o = a16(o + F * F * k * 8);
+  s.off_S = o; o = a16(o + F * tr_s_row(F, k) * 8);
   s.off_v = o; o = a16(o + D * 8);
   s.off_merged = o; o = a16(o + D * 8);
   s.off_pre = o; o = a16(o + (hsum + 1) * 8);
@@ -214,6 +222,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
   int* pres = (int*)(smem + L.off_pres);
   double* lrp = (double*)(smem + L.off_lrp);
   double* S = (double*)(smem + L.off_S);
+  const int SK = tr_s_seg(p.k), SR = tr_s_row(p.F, p.k);  // segment / row stride of S
   double* v = (double*)(smem + L.off_v);
   double* merged = (double*)(smem + L.off_merged);
   double* pre = (double*)(smem + L.off_pre);
@@ -422,7 +431,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
 #pragma unroll
             for (int m = 0; m < 4; ++m)
               if (js[m] >= 0) s += xs[m] * (double)v[m][i];
-            S[f * Fk + gk] = s;
+            S[f * SR + gkg[gk] * SK + (gk - gkg[gk] * k)] = s;
           }
         }
       }
@@ -434,7 +443,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
             const int j = sidx[f * M + m];
             if (j >= 0) s += sval[f * M + m] * (double)__ldcg(p.ffm + (int64_t)j * Fk + gk);
           }
-          S[f * Fk + gk] = s;
+          S[f * SR + gkg[gk] * SK + (gk - gkg[gk] * k)] = s;
         }
       }
     }
@@ -483,22 +492,26 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       const int f1 = ptab[pp] & 0xFF, f2 = ptab[pp] >> 8;
       double pv = 0.0;
       if (pres[f1] && pres[f2]) {  // M:346-351
-        const double* a = S + (f1 * F + f2) * k;
-        const double* b = S + (f2 * F + f1) * k;
+        const double* a = S + f1 * SR + f2 * SK;
+        const double* b = S + f2 * SR + f1 * SK;
         for (int c = 0; c < k; ++c) pv += a[c] * b[c];
       }
       v[1 + pp] = pv;
       psum_part += pv;
       ffm_bad |= !isfinite(pv);
     }
+    TR_MARK(16);
     if (tid == 0) {
       double lo = (double)__ldcg(p.lr + p.n_buckets);  // bias, M:327
       for (int f = 0; f < F; ++f)
         if (pres[f]) lo += lrp[f];
       v[0] = lo;
     }
+    TR_MARK(17);
     const double psum = block_sum<TR_WARPS>(psum_part, red, bsc);
+    TR_MARK(18);
     ffm_bad = __syncthreads_or(ffm_bad);
+    TR_MARK(19);
     const double lr_out = v[0];
     const double mu = (psum + lr_out) / D;
     double sq_part = 0.0;
@@ -508,6 +521,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
     }
     const double sd = sqrt(block_sum<TR_WARPS>(sq_part, red, bsc) / D);  // np.std (population)
     const double denom = sd + 1e-6;
+    TR_MARK(20);
     int merge_bad = 0;
     for (int i = tid; i < D; i += TR_THREADS) {
       merged[i] = (v[i] - mu) / denom;
@@ -592,6 +606,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       for (int off = 0; off < row_bytes; off += 128) prefetch_l2(wr + off);
       prefetch_l2(p.lr + pf_j);
     }
+    TR_MARK(21);
     const double p_raw = sigmoid_raw(logit);
     const double g = p_raw - (double)label;  // M:456-457
     if (tid == 0 && rank == 0) p.prob_out[e] = fmin(fmax(p_raw, 1e-7), 1.0 - 1e-7);
@@ -600,8 +615,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
     if (NL > 0) {
       double* dcur = d0;
       double* dnext = d1;
+      TR_MARK(22);
       if (tid == 0) dcur[0] = g;
       __syncthreads();
+      TR_MARK(23);
       int hoff = p.hsum;
       for (int l = NL - 1; l >= 0; --l) {
         const int I = p.dims[l], O = p.dims[l + 1];
@@ -636,7 +653,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
             dnext[r] = s;
           }
         }
+        TR_MARK(24 + 4 * l);
         __syncthreads();
+        TR_MARK(25 + 4 * l);
         // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554):
         // warp per row (dead-ReLU rows skipped warp-uniformly), lanes along c
         if (Ow <= 8) {  // narrow slice: flat (row, column) per thread
@@ -658,10 +677,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
             }
           }
         }
+        TR_MARK(26 + 4 * l);
         for (int c = tid; c < Ow; c += TR_THREADS) {  // M:557-572
           const double gr = dcur[cb + c];
           if (gr != 0.0 || !p.sparse) adagrad_m(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt, mg);
         }
+        TR_MARK(27 + 4 * l);
         if (l > 0) {
           hoff -= I;
           for (int r = tid; r < I; r += TR_THREADS)
@@ -706,7 +727,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       if (gg != f) dpv = g + dv[1 + (gg < f ? tr_pair_pos(gg, f, F) : tr_pair_pos(f, gg, F))];
       dpm[t] = dpv;
       if (gg == f || !pres[f]) continue;
-      const double* sgf = S + (gg * F + f) * k;
+      const double* sgf = S + gg * SR + f * SK;
       int any = 0;
       for (int c = 0; c < k; ++c) any |= (dpv * sgf[c]) != 0.0;
       if (any) atomicOr(&fact[f], 1);
@@ -734,7 +755,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
         for (int s2 = s; s2 >= 0; s2 = nxt[s2]) {
           const int f = sfield[s2];
           if (!fact[f]) continue;
-          const double tv = dpm[f * F + gg] * S[(gg * F + f) * k + c];  // t[g][c] (M:501)
+          const double tv = dpm[f * F + gg] * S[gg * SR + f * SK + c];  // t[g][c] (M:501)
           ug += sval[s2] * tv;  // x * t (M:505), add.at order
           touched = true;
         }

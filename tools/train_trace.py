@@ -14,9 +14,10 @@ exec(open("tools/train_profile.py").read())  # runs 200 warm-up + 400 examples
 from paper_2407_10115_b200 import _lib  # noqa: E402
 
 h = _lib.lib()
-buf = (ctypes.c_longlong * (64 * 16))()
+NPH = 40
+buf = (ctypes.c_longlong * (64 * NPH))()
 h.dffm_tr_trace_read(buf)
-t = np.array(buf, dtype=np.int64).reshape(64, 16)
+t = np.array(buf, dtype=np.int64).reshape(64, NPH)
 names = ["start", "staged", "S+lr loaded", "dup lists", "pairs+norm", "mlp l0 fwd", "mlp l1 fwd",
          "mlp out", "bwd l>0", "bwd l0", "norm bwd", "dp/fact", "ffm upd", "lr upd", "cl.sync"]
 per = np.median(np.diff(t[:, :15], axis=1), axis=0)
@@ -24,3 +25,13 @@ tot = np.median(t[1:, 0] - t[:-1, 0])
 for i, d in enumerate(per):
     print(f"{names[i]:>12s} -> {names[i+1]:<12s} {d:8.0f} cyc")
 print(f"example period {tot:.0f} cycles")
+
+fine = [(3, 16, "pairs loop"), (16, 17, "lr_out by thread 0"), (17, 18, "block_sum(pairs)"), (18, 19, "syncthreads_or"),
+        (19, 20, "mu, var block_sum, sqrt"), (20, 4, "merged[] + syncthreads_or"), (7, 21, "logit, prefetch"),
+        (21, 22, "sigmoid"), (22, 23, "sync"), (23, 32, "l2 upstream"), (32, 33, "l2 sync"), (33, 34, "l2 W update"),
+        (34, 35, "l2 b update"), (35, 28, "l2 mask+sync -> l1 upstream"), (28, 29, "l1 sync"), (29, 30, "l1 W update"),
+        (30, 31, "l1 b update"), (31, 8, "l1 mask+sync"), (8, 24, "l0 upstream + cluster reduce"), (24, 25, "l0 sync"),
+        (25, 26, "l0 W update"), (26, 27, "l0 b update"), (27, 9, "l0 sync")]
+for a, b, nm in fine:
+    d = np.median(t[:, b] - t[:, a])
+    print(f"{nm:>34s} {d:8.0f} cyc")
