@@ -69,6 +69,7 @@ struct TrainParams {
   int hsum;      // sum of hidden sizes
   int dmax;      // max layer width incl. D
   int mlp_size;  // floats in W+b over all layers
+  int mlp_dup;   // floats in W+b of layers >= 1 (second weight buffer of the cluster trainer)
   int mlp_smem;  // 1: MLP weights + accumulators resident in shared memory
   int hogwild;   // K6: each CTA is an independent worker over examples blockIdx.x + i*gridDim.x
   float* lr;
@@ -141,9 +142,13 @@ __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int
 #ifndef DFFM_FAST_INVSQRT
 #define DFFM_FAST_INVSQRT 0
 #endif
+// The general power is kept out of line: inlined at every Adagrad call site it made the
+// trainer 166 KB of SASS, more than the SM's instruction cache, and every phase of the
+// per-example chain then started with instruction-fetch misses.
+__device__ __noinline__ double inv_pow_general(double acc, double pt) { return pow(acc, -pt); }
 __device__ __forceinline__ double inv_pow(double acc, double pt) {
   if (pt == 0.5) return DFFM_FAST_INVSQRT ? rsqrt(acc) : __ddiv_rn(1.0, __dsqrt_rn(acc));
-  return pow(acc, -pt);
+  return inv_pow_general(acc, pt);
 }
 
 // One Adagrad element step with the reference's rounding (M:510-513).
@@ -152,6 +157,15 @@ __device__ __forceinline__ void adagrad(float* w, float* acc, double g, double l
   *acc = __double2float_rn(a64);
   const double step = __dmul_rn(__dmul_rn(lr, g), inv_pow(a64, pt));
   *w = __double2float_rn(__dsub_rn((double)*w, step));
+}
+
+// The same step on a weight held in a register: returns the new weight (the caller
+// publishes it); the accumulator is updated in place.
+__device__ __forceinline__ float adagrad_val(float w, float* acc, double g, double lr, double pt) {
+  const double a64 = __dadd_rn((double)*acc, __dmul_rn(g, g));
+  *acc = __double2float_rn(a64);
+  const double step = __dmul_rn(__dmul_rn(lr, g), inv_pow(a64, pt));
+  return __double2float_rn(__dsub_rn((double)w, step));
 }
 
 // MLP element of the working copy: shared memory, or global (L2-only reads so
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int F = p.F, M = p.M, k = p.k, P = p.P, D = p.D, FM = F * M, Fk = F * k;
   const TrSmem L =
-      tr_smem_layout(F, M, k, D, p.hsum, p.dmax, p.mlp_smem ? 2 * p.mlp_size : 0);
+      tr_smem_layout(F, M, k, D, p.hsum, p.dmax, p.mlp_smem ? 2 * p.mlp_size + p.mlp_dup : 0);
   int* sidx = (int*)(smem + L.off_sidx);
   double* sval = (double*)(smem + L.off_sval);
   int* pres = (int*)(smem + L.off_pres);
@@ -271,10 +285,24 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
   float* Wal[DFFM_MAX_LAYERS];
   float* bal[DFFM_MAX_LAYERS];
   int ldw[DFFM_MAX_LAYERS];  // row stride of the working copy
+  // Cluster trainer: the replicated layers (l >= 1) are UPDATED by one owner CTA per
+  // row (row r on rank r % C; bias element c on rank c % C) instead of by every CTA --
+  // the Adagrad step is FP64 division / square-root / conversion throughput
+  // (tools/fp64_bench.cu), so 8 copies of it cost 8x the pipe time of one.  The owner
+  // publishes the new weights to every CTA's copy through DSMEM.  Other CTAs may
+  // still be reading the old values (upstream gradients use the PRE-update weights,
+  // M:473-475), so the layers' weights are double-buffered: example e reads buffer
+  // wp, the owners write every element of their rows (updated or not) into buffer
+  // wp ^ 1 of all CTAs, and the end-of-example cluster barrier flips wp.
+  const bool dsplit = C > 1 && p.mlp_smem && NL > 1;
+  int wp = 0;
+  float* Wl2[DFFM_MAX_LAYERS];  // second buffers (dsplit, l >= 1)
+  float* bl2[DFFM_MAX_LAYERS];
   {
     float* mw = (float*)(smem + L.off_mlp);
     float* ma = mw + p.mlp_size;
-    int off = 0;
+    float* md = ma + p.mlp_size;
+    int off = 0, off2 = 0;
     for (int l = 0; l < NL; ++l) {
       const int I = p.dims[l], O = p.dims[l + 1];
       const bool split = (C > 1 && l == 0 && NL > 1);
@@ -290,8 +318,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
         }
         for (int t = tid; t < Ow; t += TR_THREADS) { bl[l][t] = p.b[l][cb + t]; bal[l][t] = p.b_acc[l][cb + t]; }
         off += I * Ow + Ow;
+        Wl2[l] = Wl[l];
+        bl2[l] = bl[l];
+        if (dsplit && l > 0) {
+          Wl2[l] = md + off2;
+          bl2[l] = md + off2 + I * O;
+          off2 += I * O + O;
+        }
       } else {
         Wl[l] = p.W[l] + cb; bl[l] = p.b[l] + cb; Wal[l] = p.W_acc[l] + cb; bal[l] = p.b_acc[l] + cb;
+        Wl2[l] = Wl[l];
+        bl2[l] = bl[l];
       }
     }
   }
@@ -539,7 +576,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
         const int I = p.dims[l], O = p.dims[l + 1];
         const bool split = (C > 1 && l == 0);
         const int Ow = split ? W0 : O, ld = ldw[l];
-        const float* W = Wl[l];
+        const float* W = wp ? Wl2[l] : Wl[l];
+        const float* bcur = wp ? bl2[l] : bl[l];
         // split-K: thread (part, o), o fastest -> conflict-free W reads;
         // partials reduced in fixed part order (deterministic)
         const int G = Ow <= TR_THREADS ? TR_THREADS / Ow : 1;
@@ -559,7 +597,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
           } else {
             for (int i = 0; i < I; ++i) z += a[i] * ldm(W + (int64_t)i * ld + o, mg);
           }
-          z += ldm(&bl[l][o], mg);  // M:368
+          z += ldm(&bcur[o], mg);  // M:368
           if (split) {
             // owner broadcasts its columns' pre-activations to every CTA (DSMEM)
             for (int rk = 0; rk < C; ++rk)
@@ -586,8 +624,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       }
       const int I = p.dims[NL - 1];
       double s = 0.0;
-      for (int i = tid; i < I; i += TR_THREADS) s += a[i] * ldm(&Wl[NL - 1][i], mg);
-      nn_out = block_sum<TR_WARPS>(s, red, bsc) + ldm(&bl[NL - 1][0], mg);  // M:372-373
+      const float* Wo = wp ? Wl2[NL - 1] : Wl[NL - 1];
+      for (int i = tid; i < I; i += TR_THREADS) s += a[i] * ldm(&Wo[i], mg);
+      nn_out = block_sum<TR_WARPS>(s, red, bsc) + ldm(wp ? &bl2[NL - 1][0] : &bl[NL - 1][0], mg);  // M:372-373
       nn_bad = __syncthreads_or(nn_bad);
     }
     TR_MARK(7);
@@ -624,7 +663,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
         const int I = p.dims[l], O = p.dims[l + 1];
         const bool split = (C > 1 && l == 0);
         const int Ow = split ? W0 : O, cb = split ? c0 : 0, ld = ldw[l];
-        float* W = Wl[l];
+        float* W = wp ? Wl2[l] : Wl[l];
         float* Wa = Wal[l];
         const double* a_in = l == 0 ? merged : act + (hoff - I);
         // upstream gradient from the PRE-update weights (M:473-475): warp per row
@@ -658,7 +697,34 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
         TR_MARK(25 + 4 * l);
         // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554):
         // warp per row (dead-ReLU rows skipped warp-uniformly), lanes along c
-        if (Ow <= 8) {  // narrow slice: flat (row, column) per thread
+        if (dsplit && l > 0) {
+          // owner rows r = rank, rank + C, ...: one element per thread, the new (or
+          // unchanged) weight stored into buffer wp ^ 1 of every CTA
+          auto cl = cooperative_groups::this_cluster();
+          float* Wn = wp ? Wl[l] : Wl2[l];
+          const int nown = (I - rank + C - 1) / C;
+          for (int t = tid; t < nown * Ow; t += TR_THREADS) {
+            const int ro = t / Ow, c = t - ro * Ow, r = rank + C * ro;
+            const double ar = a_in[r];
+            const double gr = __dmul_rn(ar, dcur[c]);
+            // the same skips as the replicated update: zero-gradient slots (M:536-554),
+            // and whole dead-ReLU rows when the row is walked by a warp (Ow > 8)
+            const bool skip = p.sparse && (gr == 0.0 || (Ow > 8 && ar == 0.0));
+            float w = W[r * ld + c];
+            if (!skip) w = adagrad_val(w, &Wa[r * ld + c], gr, p.lr_nn, pt);
+            for (int rk = 0; rk < C; ++rk) cl.map_shared_rank(Wn, rk)[r * ld + c] = w;
+          }
+          // bias element c on rank c % C, from the top threads (the low ones hold rows)
+          float* bc = wp ? bl2[l] : bl[l];
+          float* bn = wp ? bl[l] : bl2[l];
+          const int tb = TR_THREADS - 1 - tid, cbias = rank + C * tb;
+          if (cbias < Ow) {
+            const double gr = dcur[cbias];
+            float w = bc[cbias];
+            if (gr != 0.0 || !p.sparse) w = adagrad_val(w, &bal[l][cbias], gr, p.lr_nn, pt);
+            for (int rk = 0; rk < C; ++rk) cl.map_shared_rank(bn, rk)[cbias] = w;
+          }
+        } else if (Ow <= 8) {  // narrow slice: flat (row, column) per thread
           for (int t = tid; t < I * Ow; t += TR_THREADS) {
             const int r = t / Ow, c = t - r * Ow;
             const double gr = __dmul_rn(a_in[r], dcur[cb + c]);
@@ -678,10 +744,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
           }
         }
         TR_MARK(26 + 4 * l);
-        for (int c = tid; c < Ow; c += TR_THREADS) {  // M:557-572
-          const double gr = dcur[cb + c];
-          if (gr != 0.0 || !p.sparse) adagrad_m(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt, mg);
-        }
+        if (!(dsplit && l > 0))
+          for (int c = tid; c < Ow; c += TR_THREADS) {  // M:557-572
+            const double gr = dcur[cb + c];
+            if (gr != 0.0 || !p.sparse) adagrad_m(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt, mg);
+          }
         TR_MARK(27 + 4 * l);
         if (l > 0) {
           hoff -= I;
@@ -780,6 +847,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
     TR_MARK(13);
     if (C > 1) cooperative_groups::this_cluster().sync();
     else __syncthreads();
+    if (dsplit) wp ^= 1;
     TR_MARK(14);
   }
 
@@ -790,6 +858,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
     for (int l = 0; l < NL; ++l) {
       const int I = p.dims[l], O = p.dims[l + 1];
       const bool split = (C > 1 && l == 0 && NL > 1);
+      if (dsplit && l > 0) {
+        // weights: identical in every CTA (buffer wp), rank 0 writes; accumulators:
+        // each owner writes its rows / bias elements
+        const float* Wc = wp ? Wl2[l] : Wl[l];
+        const float* bc = wp ? bl2[l] : bl[l];
+        for (int t = tid; t < I * O; t += TR_THREADS) {
+          if (rank == 0) p.W[l][t] = Wc[t];
+          if ((t / O) % C == rank) p.W_acc[l][t] = Wal[l][t];
+        }
+        for (int t = tid; t < O; t += TR_THREADS) {
+          if (rank == 0) p.b[l][t] = bc[t];
+          if (t % C == rank) p.b_acc[l][t] = bal[l][t];
+        }
+        continue;
+      }
       if (!split && rank != 0) continue;  // replicated layers: one writer
       const int Ow = split ? W0 : O, cb = split ? c0 : 0;
       for (int t = tid; t < I * Ow; t += TR_THREADS) {
@@ -847,7 +930,10 @@ static int tr_validate(const dffm_model* m, int32_t M, int C, TrainParams& p, in
     p.b[l] = (float*)m->b[l];
   }
   const int smax = max_smem_optin_current();
-  TrSmem L = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 2 * p.mlp_size);
+  p.mlp_dup = 0;
+  if (C > 1)
+    for (int l = 1; l < p.n_layers; ++l) p.mlp_dup += m->dims[l] * m->dims[l + 1] + m->dims[l + 1];
+  TrSmem L = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 2 * p.mlp_size + p.mlp_dup);
   p.mlp_smem = L.total <= smax;
   if (!p.mlp_smem) L = tr_smem_layout(p.F, p.M, p.k, p.D, p.hsum, p.dmax, 0);
   if (L.total > smax) {
