@@ -60,10 +60,13 @@ def hash_ranks(field_ids: torch.Tensor, ranks: torch.Tensor, hash_bits: int) -> 
 
 
 def zipf_cdf(n: int, alpha: float, device) -> torch.Tensor:
-    r = torch.arange(1, n + 1, dtype=torch.float64, device=device)
+    # always summed on the host: a device cumsum is a parallel scan whose f64 rounding
+    # varies from process to process (a handful of the 10^8 ranks of a cfg5 batch
+    # moved between runs), and the seeded inputs are meant to be reproducible
+    r = torch.arange(1, n + 1, dtype=torch.float64)
     w = r.pow(-alpha)
     c = torch.cumsum(w, 0)
-    return c / c[-1]
+    return (c / c[-1]).to(device)
 
 
 def sample_ranks(shape, n: int, dist: str, alpha: float, gen: torch.Generator, device,

@@ -383,3 +383,27 @@ def test_forward_row_ring_nonfinite_and_bad_index():
             predict_batch(ix, (ix >= 0).astype(np.float32), store_from_oracle(ost))
     finally:
         _lib.lib().dffm_set_forward_family(-1)
+
+
+@pytest.mark.parametrize("cfgname", ["cfg2", "cfg5"])
+def test_forward_is_bit_reproducible_across_launches(cfgname):
+    """Race detector for the warp-specialised row ring and the tcgen05 MLP: the same
+    batch scored four times (hot and cold L2, the ring and the TMEM regions in
+    different phases) gives identical bits; so do the seeded inputs when they are
+    generated twice (the Zipf CDF is summed on the host)."""
+    wl = {"cfg2": configs.CFG2, "cfg5": configs.CFG5}[cfgname]
+    bits = 16
+    F, k, M = wl.n_fields, wl.k, wl.max_per_field
+    ost = fo.random_store(F, k, tuple(wl.hidden), bits, seed=3)
+    st = store_from_oracle(ost, "bf16" if cfgname == "cfg5" else "f32")
+    n = 150_000
+    idx, val = synth.make_examples(wl, n, seed=5, device=DEV, hash_bits=bits)
+    idx2, val2 = synth.make_examples(wl, n, seed=5, device=DEV, hash_bits=bits)
+    assert torch.equal(idx, idx2) and torch.equal(val, val2)
+    ref = predict_batch(idx, val, st).clone()
+    flush = torch.empty(160 << 20, dtype=torch.uint8, device=DEV)
+    for r in range(3):
+        if r & 1:
+            flush.zero_()
+        p = predict_batch(idx, val, st)
+        assert torch.equal(p, ref), f"launch {r}: {(p != ref).sum().item()} examples differ"
