@@ -87,7 +87,7 @@ struct TrainParams {
 struct TrSmem {
   int off_sidx, off_sval, off_pres, off_lrp, off_S, off_v, off_merged, off_pre, off_act, off_d0,
       off_d1, off_dv, off_nxt, off_lead, off_fact, off_red, off_part, off_dpm, off_ptab, off_ulist,
-      off_gkg, off_sfield, off_zbuf, off_dpart, off_mlp, total;
+      off_gkg, off_sfield, off_zbuf, off_dpart, off_dg, off_mlp, total;
 };
 
 __host__ __device__ inline int a16(int x) { return (x + 15) & ~15; }
@@ -129,6 +129,7 @@ __host__ __device__ inline TrSmem tr_smem_layout(int F, int M, int k, int D, int
   s.off_sfield = o; o = a16(o + FM);
   s.off_zbuf = o; o = a16(o + dmax * 8);
   s.off_dpart = o; o = a16(o + D * 8);
+  s.off_dg = o; o = a16(o + (hsum + 1) * 8);
   s.off_mlp = o; o = a16(o + mlp_floats * 4);
   s.total = o;
   return s;
@@ -218,6 +219,22 @@ __device__ double block_sum(double v, double* red, int& ctr) {
   return t;
 }
 
+// block_sum that also or-reduces a per-thread flag in its one barrier
+template <int NW = TR_WARPS>
+__device__ double block_sum_or(double v, int& flag, double* red, int& ctr) {
+  constexpr int TR_WARPS = NW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  double* slot = red + (++ctr & 1) * TR_WARPS;
+  if (lane == 0) slot[warp] = v;
+  flag = __syncthreads_or(flag);
+  double t = lane < TR_WARPS ? slot[lane] : 0.0;  // the same fixed-order fold as block_sum
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
 __device__ __forceinline__ int tr_pair_pos(int a, int b, int F) {
   return a * F - a * (a + 1) / 2 + (b - a - 1);
 }
@@ -284,6 +301,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
   const int c0 = (C > 1 && NL > 1) ? rank * W0 : 0;
   double* zbuf = (double*)(smem + L.off_zbuf);
   double* dpart = (double*)(smem + L.off_dpart);
+  double* dg = (double*)(smem + L.off_dg);  // gradients w.r.t. the layers' pre-activations
 
   // ---- MLP working copies: shared memory for the whole launch when they fit.
   // Layer 0 is stored as its [I][W0] column slice (W0 = O when C == 1).
@@ -552,18 +570,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       v[0] = lo;
     }
     TR_MARK(17);
-    const double psum = block_sum<TR_WARPS>(psum_part, red, bsc);
+    const double psum = block_sum_or<TR_WARPS>(psum_part, ffm_bad, red, bsc);
     TR_MARK(18);
-    ffm_bad = __syncthreads_or(ffm_bad);
     TR_MARK(19);
     const double lr_out = v[0];
-    const double mu = (psum + lr_out) / D;
+    // the f64 divisions / square root below are computed by the warps that use them
+    // (tid < D rounded up to a warp), not by all 32
+    const bool dw = warp < (D + 31) / 32;
+    const double mu = dw ? (psum + lr_out) / D : 0.0;
     double sq_part = 0.0;
     for (int i = tid; i < D; i += TR_THREADS) {
       const double c = v[i] - mu;
       sq_part += c * c;
     }
-    const double sd = sqrt(block_sum<TR_WARPS>(sq_part, red, bsc) / D);  // np.std (population)
+    const double sq_sum = block_sum<TR_WARPS>(sq_part, red, bsc);
+    const double sd = dw ? sqrt(sq_sum / D) : 0.0;  // np.std (population)
     const double denom = sd + 1e-6;
     TR_MARK(20);
     int merge_bad = 0;
@@ -633,8 +654,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       double s = 0.0;
       const float* Wo = wp ? Wl2[NL - 1] : Wl[NL - 1];
       for (int i = tid; i < I; i += TR_THREADS) s += a[i] * ldm(&Wo[i], mg);
-      nn_out = block_sum<TR_WARPS>(s, red, bsc) + ldm(wp ? &bl2[NL - 1][0] : &bl[NL - 1][0], mg);  // M:372-373
-      nn_bad = __syncthreads_or(nn_bad);
+      nn_out = block_sum_or<TR_WARPS>(s, nn_bad, red, bsc) +
+               ldm(wp ? &bl2[NL - 1][0] : &bl[NL - 1][0], mg);  // M:372-373
     }
     TR_MARK(7);
     const double logit = nn_out + lr_out + psum;  // M:377
@@ -653,33 +674,43 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       prefetch_l2(p.lr + pf_j);
     }
     TR_MARK(21);
-    const double p_raw = sigmoid_raw(logit);
-    const double g = p_raw - (double)label;  // M:456-457
-    if (tid == 0 && rank == 0) p.prob_out[e] = fmin(fmax(p_raw, 1e-7), 1.0 - 1e-7);
+    // sigmoid and g = p - y (M:456-457) once per CTA, broadcast through shared memory
+    // (32 warps each evaluating an f64 exp and a division is ~1.5k cycles of FP64 pipe)
+    if (tid == 0) {
+      const double p_raw = sigmoid_raw(logit);
+      dg[p.hsum] = p_raw - (double)label;
+      if (rank == 0) p.prob_out[e] = fmin(fmax(p_raw, 1e-7), 1.0 - 1e-7);
+    }
+    __syncthreads();
+    const double g = dg[p.hsum];
     // ---------------------------------------------------------- MLP backward + update
+    // Pass 1: the gradient chain top layer down, every upstream gradient from the
+    // PRE-update weights (M:473-475); dg holds the gradient w.r.t. each layer's
+    // pre-activations (hidden layer j at its pre/act offset, g at hsum).
+    // Pass 2: every layer's Adagrad updates in ONE barrier-free phase -- the updates
+    // have no consumer before the next example, and as separate phases each small
+    // layer cost a barrier plus a full Adagrad latency (~1.2-2.4k cycles each in the
+    // phase trace) that now hides under layer 0's rounds.
     double* dmerged = d1;
     if (NL > 0) {
-      double* dcur = d0;
-      double* dnext = d1;
       TR_MARK(22);
-      if (tid == 0) dcur[0] = g;
-      __syncthreads();
       TR_MARK(23);
-      int hoff = p.hsum;
+      int oout = p.hsum;  // offset in dg of layer l's output gradient
       for (int l = NL - 1; l >= 0; --l) {
-        const int I = p.dims[l], O = p.dims[l + 1];
+        const int I = p.dims[l];
         const bool split = (C > 1 && l == 0);
-        const int Ow = split ? W0 : O, cb = split ? c0 : 0, ld = ldw[l];
-        float* W = wp ? Wl2[l] : Wl[l];
-        float* Wa = Wal[l];
-        const double* a_in = l == 0 ? merged : act + (hoff - I);
-        // upstream gradient from the PRE-update weights (M:473-475): warp per row
-        // (split layer: partial over this CTA's columns, reduced across the cluster)
+        const int Ow = split ? W0 : p.dims[l + 1], cb = split ? c0 : 0, ld = ldw[l];
+        const float* W = wp ? Wl2[l] : Wl[l];
+        const double* dcur = dg + oout;
+        const int oin = oout - I;  // offset of layer l's input (pre / act / dg), l > 0
+        // warp per row (split layer: partial over this CTA's columns, reduced across
+        // the cluster); the ReLU mask of the layer below (M:479) applied on the way out
         if (Ow <= 8) {  // narrow (cluster-split) slice: thread per row
           for (int r = tid; r < I; r += TR_THREADS) {
             double s = 0.0;
             for (int c = 0; c < Ow; ++c) s += ldm(W + (int64_t)r * ld + c, mg) * dcur[cb + c];
-            (split ? dpart : dnext)[r] = s;
+            if (l > 0) dg[oin + r] = pre[oin + r] > 0.0 ? s : 0.0;
+            else (split ? dpart : dmerged)[r] = s;
           }
         } else {
           for (int r = warp; r < I; r += TR_WARPS) {
@@ -687,7 +718,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
             for (int c = lane; c < Ow; c += 32) s += ldm(W + (int64_t)r * ld + c, mg) * dcur[cb + c];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) (split ? dpart : dnext)[r] = s;
+            if (lane == 0) {
+              if (l > 0) dg[oin + r] = pre[oin + r] > 0.0 ? s : 0.0;
+              else (split ? dpart : dmerged)[r] = s;
+            }
           }
         }
         if (split) {
@@ -696,21 +730,39 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
             double s = 0.0;
             for (int rk = 0; rk < C; ++rk)
               s += cooperative_groups::this_cluster().map_shared_rank(dpart, rk)[r];
-            dnext[r] = s;
+            dmerged[r] = s;
           }
         }
-        TR_MARK(24 + 4 * l);
         __syncthreads();
-        TR_MARK(25 + 4 * l);
-        // W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554):
-        // warp per row (dead-ReLU rows skipped warp-uniformly), lanes along c
+        TR_MARK(24 + l);
+        oout = oin;
+      }
+      TR_MARK(8);
+      // ---- pass 2: W[r][c] with grad = a_in[r]*d[c]; zero gradients skipped (M:536-554)
+      const int rt = TR_THREADS - 1 - tid;  // the small jobs start from the top threads:
+      int uo = 0;                           // the low ones have layer 0's extra round
+      auto first_item = [&](int n) {  // item of this thread in a job of n items dealt from rt = uo
+        const int t = rt - uo + (rt < uo ? TR_THREADS : 0);
+        uo = (uo + n) % TR_THREADS;
+        return t;
+      };
+      oout = p.hsum;
+      for (int l = NL - 1; l >= 0; --l) {
+        const int I = p.dims[l];
+        const bool split = (C > 1 && l == 0);
+        const int Ow = split ? W0 : p.dims[l + 1], cb = split ? c0 : 0, ld = ldw[l];
+        float* W = wp ? Wl2[l] : Wl[l];
+        float* Wa = Wal[l];
+        const double* dcur = dg + oout;
+        const int oin = oout - I;
+        const double* a_in = l == 0 ? merged : act + oin;
         if (dsplit && l > 0) {
           // owner rows r = rank, rank + C, ...: one element per thread, the new (or
           // unchanged) weight stored into buffer wp ^ 1 of every CTA
           auto cl = cooperative_groups::this_cluster();
           float* Wn = wp ? Wl[l] : Wl2[l];
           const int nown = (I - rank + C - 1) / C;
-          for (int t = tid; t < nown * Ow; t += TR_THREADS) {
+          for (int t = first_item(nown * Ow); t < nown * Ow; t += TR_THREADS) {
             const int ro = t / Ow, c = t - ro * Ow, r = rank + C * ro;
             const double ar = a_in[r];
             const double gr = __dmul_rn(ar, dcur[c]);
@@ -721,52 +773,46 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
             if (!skip) w = adagrad_val(w, &Wa[r * ld + c], gr, p.lr_nn, pt);
             for (int rk = 0; rk < C; ++rk) cl.map_shared_rank(Wn, rk)[r * ld + c] = w;
           }
-          // bias element c on rank c % C, from the top threads (the low ones hold rows)
+          // bias element c on rank c % C
           float* bc = wp ? bl2[l] : bl[l];
           float* bn = wp ? bl[l] : bl2[l];
-          const int tb = TR_THREADS - 1 - tid, cbias = rank + C * tb;
-          if (cbias < Ow) {
+          const int nbo = (Ow - rank + C - 1) / C;
+          for (int t = first_item(nbo); t < nbo; t += TR_THREADS) {
+            const int cbias = rank + C * t;
             const double gr = dcur[cbias];
             float w = bc[cbias];
             if (gr != 0.0 || !p.sparse) w = adagrad_val(w, &bal[l][cbias], gr, p.lr_nn, pt);
             for (int rk = 0; rk < C; ++rk) cl.map_shared_rank(bn, rk)[cbias] = w;
           }
-        } else if (Ow <= 8) {  // narrow slice: flat (row, column) per thread
-          for (int t = tid; t < I * Ow; t += TR_THREADS) {
-            const int r = t / Ow, c = t - r * Ow;
-            const double gr = __dmul_rn(a_in[r], dcur[cb + c]);
-            if (gr != 0.0 || !p.sparse) adagrad_m(&W[(int64_t)r * ld + c], &Wa[(int64_t)r * ld + c],
-                                                  gr, p.lr_nn, pt, mg);
-          }
         } else {
-          for (int r = warp; r < I; r += TR_WARPS) {
-            const double ar = a_in[r];
-            if (ar == 0.0 && p.sparse) continue;
-            float* wr = W + (int64_t)r * ld;
-            float* war = Wa + (int64_t)r * ld;
-            for (int c = lane; c < Ow; c += 32) {
-              const double gr = __dmul_rn(ar, dcur[cb + c]);
-              if (gr != 0.0 || !p.sparse) adagrad_m(&wr[c], &war[c], gr, p.lr_nn, pt, mg);
+          if (Ow <= 8) {  // narrow slice: flat (row, column) per thread
+            for (int t = tid; t < I * Ow; t += TR_THREADS) {
+              const int r = t / Ow, c = t - r * Ow;
+              const double gr = __dmul_rn(a_in[r], dcur[cb + c]);
+              if (gr != 0.0 || !p.sparse) adagrad_m(&W[(int64_t)r * ld + c], &Wa[(int64_t)r * ld + c],
+                                                    gr, p.lr_nn, pt, mg);
+            }
+          } else {  // warp per row (dead-ReLU rows skipped warp-uniformly), lanes along c
+            for (int r = warp; r < I; r += TR_WARPS) {
+              const double ar = a_in[r];
+              if (ar == 0.0 && p.sparse) continue;
+              float* wr = W + (int64_t)r * ld;
+              float* war = Wa + (int64_t)r * ld;
+              for (int c = lane; c < Ow; c += 32) {
+                const double gr = __dmul_rn(ar, dcur[cb + c]);
+                if (gr != 0.0 || !p.sparse) adagrad_m(&wr[c], &war[c], gr, p.lr_nn, pt, mg);
+              }
             }
           }
-        }
-        TR_MARK(26 + 4 * l);
-        if (!(dsplit && l > 0))
-          for (int c = tid; c < Ow; c += TR_THREADS) {  // M:557-572
+          // bias (M:557-572); in the cluster trainer from the top threads
+          for (int c = C > 1 ? first_item(Ow) : tid; c < Ow; c += TR_THREADS) {
             const double gr = dcur[cb + c];
             if (gr != 0.0 || !p.sparse) adagrad_m(&bl[l][c], &bal[l][c], gr, p.lr_nn, pt, mg);
           }
-        TR_MARK(27 + 4 * l);
-        if (l > 0) {
-          hoff -= I;
-          for (int r = tid; r < I; r += TR_THREADS)
-            dnext[r] = pre[hoff + r] > 0.0 ? dnext[r] : 0.0;  // M:479 ReLU mask
         }
-        __syncthreads();
-        TR_MARK(l == 0 ? 9 : 8);
-        double* tmp = dcur; dcur = dnext; dnext = tmp;
+        oout = oin;
       }
-      dmerged = dcur;
+      TR_MARK(9);
     }
     // ---------------------------------------------------------- MergeNorm backward (M:413-421)
     double d_lr;
@@ -776,12 +822,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
         s_d += dmerged[i];
         s_dc += dmerged[i] * (v[i] - mu);
       }
-      const double mean_d = block_sum<TR_WARPS>(s_d, red, bsc) / D;
+      const double sum_d = block_sum<TR_WARPS>(s_d, red, bsc);
       const double dot_dc = block_sum<TR_WARPS>(s_dc, red, bsc);
-      for (int i = tid; i < D; i += TR_THREADS) {
-        double x = (dmerged[i] - mean_d) / denom;
-        if (sd > 0.0) x = x - (v[i] - mu) * (dot_dc / (D * sd * denom * denom));
-        dv[i] = x;
+      if (dw) {
+        const double mean_d = sum_d / D;
+        const double coef = sd > 0.0 ? dot_dc / (D * sd * denom * denom) : 0.0;
+        for (int i = tid; i < D; i += TR_THREADS) {
+          double x = (dmerged[i] - mean_d) / denom;
+          if (sd > 0.0) x = x - (v[i] - mu) * coef;
+          dv[i] = x;
+        }
       }
       __syncthreads();
       TR_MARK(10);

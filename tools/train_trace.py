@@ -28,10 +28,9 @@ print(f"example period {tot:.0f} cycles")
 
 fine = [(3, 16, "pairs loop"), (16, 17, "lr_out by thread 0"), (17, 18, "block_sum(pairs)"), (18, 19, "syncthreads_or"),
         (19, 20, "mu, var block_sum, sqrt"), (20, 4, "merged[] + syncthreads_or"), (7, 21, "logit, prefetch"),
-        (21, 22, "sigmoid"), (22, 23, "sync"), (23, 32, "l2 upstream"), (32, 33, "l2 sync"), (33, 34, "l2 W update"),
-        (34, 35, "l2 b update"), (35, 28, "l2 mask+sync -> l1 upstream"), (28, 29, "l1 sync"), (29, 30, "l1 W update"),
-        (30, 31, "l1 b update"), (31, 8, "l1 mask+sync"), (8, 24, "l0 upstream + cluster reduce"), (24, 25, "l0 sync"),
-        (25, 26, "l0 W update"), (26, 27, "l0 b update"), (27, 9, "l0 sync")]
+        (21, 22, "sigmoid"), (22, 23, "g -> dg, sync"), (23, 26, "out layer upstream + sync"),
+        (26, 25, "l1 upstream + sync"), (25, 24, "l0 upstream + cluster reduce + sync"),
+        (8, 9, "all MLP updates (thread 0)")]
 for a, b, nm in fine:
     d = np.median(t[:, b] - t[:, a])
     print(f"{nm:>34s} {d:8.0f} cyc")
