@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
       ffm_bad |= !isfinite(pv);
     }
     TR_MARK(16);
-    if (tid == 0) {
+    if (tid == TR_THREADS - 1) {  // a thread without a pair: the serial chain runs beside the pair loop
       double lo = (double)__ldcg(p.lr + p.n_buckets);  // bias, M:327
       for (int f = 0; f < F; ++f)
         if (pres[f]) lo += lrp[f];
