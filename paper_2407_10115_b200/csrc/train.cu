@@ -51,8 +51,14 @@ __device__ long long g_tr_trace[TR_TN * TR_NPH];
     if (threadIdx.x == 0 && rank == 0 && e >= TR_T0 && e < TR_T0 + TR_TN)      \
       g_tr_trace[(e - TR_T0) * TR_NPH + (ph)] = clock64();                     \
   } while (0)
+#define TR_MARK_T(ph, thr)                                                     \
+  do {                                                                         \
+    if (threadIdx.x == (thr) && rank == 0 && e >= TR_T0 && e < TR_T0 + TR_TN)  \
+      g_tr_trace[(e - TR_T0) * TR_NPH + (ph)] = clock64();                     \
+  } while (0)
 #else
 #define TR_MARK(ph) do { } while (0)
+#define TR_MARK_T(ph, thr) do { } while (0)
 #endif
 
 struct TrainParams {
@@ -438,24 +444,23 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
     // latency per example instead of one per 32-wide column step), sums in
     // slot order as before.
     // Spare warps (warp >= F) build the duplicate lists meanwhile (below).
-    const bool dup_split = Fk <= 256 && M <= 4 && TR_WARPS - F >= 4;
+    const bool dup_split = Fk <= 256 && M <= 4 && (k & 3) == 0 && TR_WARPS - F >= 4;
     if (dup_split && warp >= F) {
       const int dt = tid - F * 32, dn = (TR_WARPS - F) * 32;
+      // thread per slot: one pass over the slots (broadcast reads) gives the first slot
+      // holding the same bucket (lead) and the next one after it (nxt)
       for (int s = dt; s < FM; s += dn) {
-        lead[s] = sidx[s] >= 0 ? s : -1;
-        nxt[s] = 0x7fffffff;
+        const int js = sidx[s];
+        int ld_ = js >= 0 ? s : -1, nx = 0x7fffffff;
+        if (js >= 0)
+          for (int s2 = 0; s2 < FM; ++s2) {
+            const bool eq = s2 != s && sidx[s2] == js;
+            if (eq && s2 < s) ld_ = min(ld_, s2);
+            if (eq && s2 > s) nx = min(nx, s2);
+          }
+        lead[s] = ld_;
+        nxt[s] = nx == 0x7fffffff ? -1 : nx;
       }
-      named_bar_sync(2, dn);
-      for (int t = dt; t < FM * FM; t += dn) {
-        const int s = t / FM, s2 = t - s * FM;
-        if (s2 != s && sidx[s] >= 0 && sidx[s2] == sidx[s]) {
-          if (s2 < s) atomicMin(&lead[s], s2);
-          else atomicMin(&nxt[s], s2);
-        }
-      }
-      named_bar_sync(2, dn);
-      for (int s = dt; s < FM; s += dn)
-        if (nxt[s] == 0x7fffffff) nxt[s] = -1;
       named_bar_sync(2, dn);
       if (warp == F) {
         int cnt = 0;
@@ -468,35 +473,52 @@ __global__ void __launch_bounds__(NT, 1024 / NT) train_kernel(TrainParams p) {
         }
         if (lane == 0) *nuniq = cnt;
       }
-    } else if (Fk <= 256 && M <= 4) {
+      TR_MARK_T(36, F * 32);
+    } else if (Fk <= 256 && M <= 4 && (k & 3) == 0) {
+      // 16-byte row loads, lanes along the row: an `ld.cg` is a strong GPU-scope load
+      // and the SM issues a thread's strong loads one at a time (~290 cycles each:
+      // the 18 scalar loads of a field warp took 5.2k cycles to issue), so the
+      // fewer, wider loads are what shortens the gather
+      const int nv = Fk >> 2;  // float4 vectors per row (<= 64: two per lane)
       for (int f = warp; f < F; f += TR_WARPS) {
         int js[4];
         double xs[4];
-        float v[4][8];
+        float4 v[4][2];
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           js[m] = m < M ? sidx[f * M + m] : -1;
           xs[m] = m < M ? sval[f * M + m] : 0.0;
         }
+        TR_MARK_T(30, 32);
 #pragma unroll
         for (int m = 0; m < 4; ++m)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int gk = lane + 32 * i;
-            v[m][i] = (js[m] >= 0 && gk < Fk) ? __ldcg(p.ffm + (int64_t)js[m] * Fk + gk) : 0.f;
+          for (int i = 0; i < 2; ++i) {
+            const int q = lane + 32 * i;
+            v[m][i] = (js[m] >= 0 && q < nv)
+                          ? __ldcg((const float4*)(p.ffm + (int64_t)js[m] * Fk) + q)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
           }
+        TR_MARK_T(31, 32);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int gk = lane + 32 * i;
-          if (gk < Fk) {
-            double s = 0.0;
+        for (int i = 0; i < 2; ++i) {
+          const int q = lane + 32 * i;
+          if (q < nv) {
+            const int gk = 4 * q, gg = gkg[gk];
+            double* dst = S + f * SR + gg * SK + (gk - gg * k);
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-              if (js[m] >= 0) s += xs[m] * (double)v[m][i];
-            S[f * SR + gkg[gk] * SK + (gk - gkg[gk] * k)] = s;
+            for (int t = 0; t < 4; ++t) {
+              double s = 0.0;
+#pragma unroll
+              for (int m = 0; m < 4; ++m)
+                if (js[m] >= 0) s += xs[m] * (double)(&v[m][i].x)[t];
+              dst[t] = s;
+            }
           }
         }
       }
+      TR_MARK_T(37, 32);
+      TR_MARK_T(38, 0);
     } else {
       for (int f = warp; f < F; f += TR_WARPS) {
         for (int gk = lane; gk < Fk; gk += 32) {

@@ -26,7 +26,10 @@ for i, d in enumerate(per):
     print(f"{names[i]:>12s} -> {names[i+1]:<12s} {d:8.0f} cyc")
 print(f"example period {tot:.0f} cycles")
 
-fine = [(3, 16, "pairs loop"), (16, 17, "lr_out by thread 0"), (17, 18, "block_sum(pairs)"), (18, 19, "syncthreads_or"),
+fine = [(1, 30, "staged -> field warp 1 starts its loads"), (30, 31, "field warp 1: loads issued"),
+        (31, 37, "field warp 1: loads landed, sums, S stores"), (1, 36, "staged -> spare warps: dup lists done"), (1, 37, "staged -> field warp 1: S written"),
+        (1, 38, "staged -> field warp 0: lr partials + S written"), (1, 3, "staged -> barrier passed"),
+        (3, 16, "pairs loop"), (16, 17, "lr_out by thread 0"), (17, 18, "block_sum(pairs)"), (18, 19, "syncthreads_or"),
         (19, 20, "mu, var block_sum, sqrt"), (20, 4, "merged[] + syncthreads_or"), (7, 21, "logit, prefetch"),
         (21, 22, "sigmoid"), (22, 23, "g -> dg, sync"), (23, 26, "out layer upstream + sync"),
         (26, 25, "l1 upstream + sync"), (25, 24, "l0 upstream + cluster reduce + sync"),
