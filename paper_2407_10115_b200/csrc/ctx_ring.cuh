@@ -12,23 +12,22 @@
 //   allocator warp   streams candidate slots (cp.async, IDXD ahead), allocates
 //                    their present rows in the ring, publishes meta[i]
 //   issue warps      one 1-D bulk copy per candidate row (full[i])
-//   pair warps       per request, first build the context cache together
-//                    (double-buffered by request parity, behind a
-//                    named barrier): Sctx[x][g][:] = sum_m x_m w_m[g] (f32 fma
-//                    over the context slots, as K3 v1), the ctx x ctx pair
-//                    values and the context lr partial; then per candidate
-//                    the pairs that involve a candidate field:
-//                    <S[c][x], Sctx[x][c]> and <S[c1][c2], S[c2][c1]>, in
+//   builder warp     build_context_cache per request, one or two requests
+//                    ahead of the candidates, double-buffered by request parity:
+//                    Sctx[x][g][:] = sum_m x_m w_m[g] (f32 fma over the context
+//                    slots, as K3 v1), the ctx x ctx pair values and their moments,
+//                    the context lr partial; published on cready[t & 1]
+//   pair warps       per candidate the pairs that involve a candidate field
+//                    (S:263-265): <S[c][x], Sctx[x][c]> and <S[c1][c2], S[c2][c1]>, in
 //                    32-pair chunks; G groups of warps take alternate bundles
 //                    (phase-safe waits: G divides NX)
 //   merge warps      lr_out = bias + ctx lr partial + candidate lr terms;
 //                    MergeNorm over [lr_out, all P pairs] (ctx x ctx from the
 //                    cache: never cached past MergeNorm) in f64 ->
 //                    staged row, residual, stage bits.
-// The cache of request t is built (buffer t & 1) only after every pair warp
-// is done with request t-1, and a pair warp starts candidate i only after the
-// merge of candidate i-NX (the allocator waits mfree before publishing i), so
-// with C >= NX no merge warp still reads a buffer that is being rebuilt.
+// The cache of request t is built (buffer t & 1) only after every candidate of request
+// t - 2 is merged (cfree[t & 1] counts the merge warps' arrivals), so no pair or merge
+// warp still reads a buffer that is being rebuilt.
 #pragma once
 
 #include "forward_kernel.cuh"
@@ -50,7 +49,7 @@ namespace dffm {
 #endif
 constexpr int CR_NPW = DFFM_CR_NPW, CR_NISS = DFFM_CR_NISS, CR_NMW = DFFM_CR_NMW;
 constexpr int CR_GT = DFFM_CR_GT;  // candidate groups of pair warps (power of 2)
-constexpr int CR_THREADS = (CR_NPW + 1 + CR_NISS + CR_NMW) * 32;
+constexpr int CR_THREADS = (CR_NPW + 1 + CR_NISS + CR_NMW + 1) * 32;  // + the context builder warp
 constexpr int CR_MAXX = 64;   // candidate slots in flight
 constexpr int CR_MAXFM = 32;  // candidate slots per candidate (Fd * Md)
 constexpr int CR_CHUNK = 32;  // pairs per chunk (lane per pair)
@@ -101,7 +100,7 @@ __host__ __device__ inline CrSmem cr_smem_layout(int F, int Fc, int Mc, int Fd, 
   s.s_xv = q; q = align16(q + B * s.Pc * 4);
   s.slot_bytes = q;
   int o = 0;
-  s.off_bar = o; o = align16(o + 4 * CR_MAXX * 8);
+  s.off_bar = o; o = align16(o + (4 * CR_MAXX + 4) * 8);  // + cready[2], cfree[2]
   s.off_ptab = o; o = align16(o + s.Pc * 4);
   s.off_stab = o; o = align16(o + Kp * 2);
   s.off_cnt = o; o = align16(o + CR_MAXX * 4);
@@ -253,6 +252,8 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
   uint64_t* pdone = full + CR_MAXX;
   uint64_t* mfree = pdone + CR_MAXX;
   uint64_t* meta = mfree + CR_MAXX;
+  uint64_t* cready = meta + CR_MAXX;  // [2] builder -> pair / merge warps: cache buffer built
+  uint64_t* cfree = cready + 2;       // [2] merge warps -> builder: every candidate of the request merged
   uint32_t* ptab = (uint32_t*)(smem + L.off_ptab);  // candidate pairs: f1 | f2 << 8 | pos << 16
   uint16_t* stab = (uint16_t*)(smem + L.off_stab);  // staged column -> source (see merge warps)
   int* my_cnt = (int*)(smem + L.off_cnt);
@@ -290,6 +291,10 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
       mbar_init(&pdone[b], pd_count);
       mbar_init(&mfree[b], B);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&cready[b], 1);
+      mbar_init(&cfree[b], C);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -300,7 +305,27 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
   auto slot = [&](int xs) { return slots + (size_t)xs * L.slot_bytes; };
   auto cache = [&](int64_t t) { return smem + L.off_cache + (size_t)(t & 1) * L.cache_bytes; };
 
-  if (warp >= CR_NPW + 1 + CR_NISS) {
+  if (warp == CR_NPW + 1 + CR_NISS + CR_NMW) {
+    // ================================================================ context builder warp
+    // build_context_cache one or two requests AHEAD of the candidates: the
+    // cache of request t goes to buffer t & 1 as soon as every candidate of request
+    // t - 2 is merged (cfree), and is published on cready.  (Built by the pair warps
+    // at each request boundary it was ~10% of their time -- they are the stage the
+    // merge warps wait on.)
+    for (int64_t t = 0; t < my_req; ++t) {
+      if (t >= 2) mbar_wait(&cfree[t & 1], (uint32_t)(((t >> 1) - 1) & 1));
+      const int64_t r = (int64_t)blockIdx.x + t * gridDim.x;
+      unsigned char* wb = cache(t);
+      if (q.cache_in) {  // prebuilt (dffm_ctx_build): copy the request's cache blob
+        const uint4* src = (const uint4*)(q.cache_in + (size_t)r * L.cache_bytes);
+        for (int v = lane; v < L.cache_bytes / 16; v += 32) ((uint4*)wb)[v] = __ldg(src + v);
+      } else {
+        cr_build_cache<T>(wb, q, L, r, p.status_base + r * C, lane, 32);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cready[t & 1]);
+    }
+  } else if (warp >= CR_NPW + 1 + CR_NISS) {
     // ================================================================ merge warps
     // one candidate per warp; its bundle's slot / phase follow from the bundle
     // number (a warp never waits on a phase it has no candidate in, and a slot
@@ -402,7 +427,10 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
         p.fout[e] = (!isfinite(lr_out) ? 1 : 0) | (pbad ? 2 : 0) | (mbad ? 4 : 0);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&mfree[xs]);
+      if (lane == 0) {
+        mbar_arrive(&mfree[xs]);
+        mbar_arrive(&cfree[cu.t & 1]);  // one of the request's C candidates is done with the cache
+      }
     }
   } else if (warp > CR_NPW) {
     // ================================================================ TMA issue warps
@@ -522,7 +550,6 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
     CrCursor cu{0, 0};  // in bundles: w = bundle within the request
     cu.advance(gw, CB);
     const unsigned char* cb = nullptr;
-    const int tid = warp * 32 + lane, nthr = G * npg * 32;
     constexpr int PER = 16 / (int)sizeof(T);
     // One slot per candidate field and one warp per chunk (npg == nch): warp wi
     // owns pairs wi*32 .. wi*32+31 of EVERY candidate, so the pair's fields and,
@@ -542,20 +569,10 @@ __global__ void __launch_bounds__(CR_THREADS, 1) ctx_ring_kernel(CtxParams q, Cr
 #pragma unroll
     for (int u = 0; u < K; ++u) areg[u] = 0.f;
     for (int64_t i = gw; i < my_nb; i += G, cu.advance(G, CB)) {
-      if (cu.t != cur_req) {
-        // ---- build_context_cache for request t, buffer t & 1
+      if (cu.t != cur_req) {  // the builder warp has request t's cache in buffer t & 1
         cur_req = cu.t;
-        const int64_t r = (int64_t)blockIdx.x + cur_req * gridDim.x;
-        unsigned char* wb = cache(cur_req);
-        named_bar_sync(1, nthr);  // every pair warp is past request t-1
-        if (q.cache_in) {  // prebuilt (dffm_ctx_build): copy the request's cache blob
-          const uint4* src = (const uint4*)(q.cache_in + (size_t)r * L.cache_bytes);
-          for (int v = tid; v < L.cache_bytes / 16; v += nthr) ((uint4*)wb)[v] = __ldg(src + v);
-          named_bar_sync(1, nthr);
-        } else {
-          cr_build_cache<T>(wb, q, L, r, p.status_base + r * C, tid, nthr);
-        }
-        cb = wb;
+        mbar_wait(&cready[cur_req & 1], (uint32_t)((cur_req >> 1) & 1));
+        cb = cache(cur_req);
         if (valid && isctx) {
           const float* sc = (const float*)(cb + L.c_S) + (ff1 * F + ff2) * K;
 #pragma unroll
