@@ -42,7 +42,7 @@ namespace dffm {
 #define DFFM_CR_NPW 10
 #endif
 #ifndef DFFM_CR_NMW
-#define DFFM_CR_NMW 12
+#define DFFM_CR_NMW 10
 #endif
 #ifndef DFFM_CR_NISS
 #define DFFM_CR_NISS 2

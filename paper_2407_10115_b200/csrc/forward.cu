@@ -176,9 +176,20 @@ static bool try_rsw_forward(const dffm_model* m, FwdParams& p, int smax, cudaStr
   }
 
   const int row_bytes = p.F * k * esz;
-  for (int nx = std::max(nx_env, RSW_NMW); nx >= std::max(2, RSW_NMW); --nx) {
-    const RswSmem L = rsw_smem_layout(p.F, p.M, p.P, row_bytes, nx, smax);
+  int npw = RSW_NPW, nmw = RSW_NMW;
+  {
+    static int roles_env = -1;  // DFFM_RSW_ROLES=0: the fixed 16 / 6 layout (A/B knob)
+    if (roles_env < 0) {
+      const char* v = getenv("DFFM_RSW_ROLES");
+      roles_env = v ? atoi(v) : 1;
+    }
+    if (roles_env) rsw_role_layout((p.P + 31) / 32, &npw, &nmw);
+  }
+  for (int nx = std::max(nx_env, nmw); nx >= std::max(2, nmw); --nx) {
+    RswSmem L = rsw_smem_layout(p.F, p.M, p.P, row_bytes, nx, smax);
     if (L.R < p.F * p.M || L.R < 2 * p.F) continue;
+    L.npw = npw;
+    L.nmw = nmw;
     switch (m->wdtype) {
       case DFFM_W_F32: *rc = launch_forward_rsw_t<float>(p, L, k, s); break;
       case DFFM_W_BF16: *rc = launch_forward_rsw_t<__nv_bfloat16>(p, L, k, s); break;

@@ -105,7 +105,8 @@ int launch_forward_rsw_t(const FwdParams& p, const RswSmem& L, int K, cudaStream
   RswKernel kern = select_rsw<T>(K, p.M);
   if (!kern) { set_error("no row-ring kernel for k=%d M=%d", K, p.M); return DFFM_SIZING; }
   int occ = 0;
-  int rc = kernel_occupancy((const void*)kern, RSW_THREADS, L.total, &occ);
+  const int threads = (L.npw + RSW_NPROD + L.nmw) * 32;
+  int rc = kernel_occupancy((const void*)kern, threads, L.total, &occ);
   if (rc) return rc;
   static int grid_env = -1;  // DFFM_RSW_GRID: SMs given to the gather (measurement knob)
   if (grid_env < 0) {
@@ -115,7 +116,7 @@ int launch_forward_rsw_t(const FwdParams& p, const RswSmem& L, int K, cudaStream
   const int64_t sms = grid_env > 0 ? std::min(grid_env, sm_count_current()) : sm_count_current();
   const int64_t grid = std::min<int64_t>(p.n, sms);
   if (grid <= 0) return DFFM_OK;
-  note_launches(1), kern<<<(unsigned)grid, RSW_THREADS, L.total, s>>>(p, L);
+  note_launches(1), kern<<<(unsigned)grid, threads, L.total, s>>>(p, L);
   DFFM_CUDA_TRY(cudaGetLastError(), "launch(forward_rsw)");
   return DFFM_OK;
 }

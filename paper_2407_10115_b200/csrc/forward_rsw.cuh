@@ -62,7 +62,8 @@ constexpr int RSW_NMW = DFFM_RSW_NMW;
 constexpr int RSW_GT = DFFM_RSW_GT;  // example groups of pair warps (power of 2)
 constexpr int RSW_IDXD = DFFM_RSW_IDXD;  // examples of idx/val in flight per producer (power of 2)
 static_assert((RSW_IDXD & (RSW_IDXD - 1)) == 0, "RSW_IDXD must be a power of two");
-constexpr int RSW_THREADS = (RSW_NPW + RSW_NPROD + RSW_NMW) * 32;
+constexpr int RSW_THREADS = (RSW_NPW + RSW_NPROD + RSW_NMW) * 32;  // default role layout
+constexpr int RSW_MAXWARPS = 28;  // CTA size bound (the role layout is chosen per shape, below)
 constexpr int RSW_MAXX = 8;     // example slots (metadata + pair values)
 constexpr int RSW_MAXFM = 128;  // padded slots per example (4 per producer lane)
 
@@ -70,6 +71,7 @@ struct RswSmem {
   int off_bar, off_pair, off_cnt, off_pidx, off_slot, off_ring, total;
   int slot_bytes, off_sidx, off_sval, off_rpos, off_xv;  // within a slot
   int row_stride, R, NX, nch;
+  int npw, nmw;  // pair warps (= the allocator's warp number) and merge warps of this launch
 };
 
 // Example-slot block: sidx[FM] i32, sval[FM] f32, rpos[FM] u16, xv[P+1] f32;
@@ -97,11 +99,28 @@ __host__ __device__ inline RswSmem rsw_smem_layout(int F, int M, int P, int row_
   s.R = (smem_max - o) / s.row_stride;
   if (s.R > 65535) s.R = 65535;
   s.total = o + (s.R > 0 ? s.R : 0) * s.row_stride;
+  s.npw = RSW_NPW;
+  s.nmw = RSW_NMW;
   return s;
 }
 
+// Role layout per shape.  A warp's SMSP is its number mod 4, so the layout decides which
+// warps share an issue port with the allocator warp -- the one serial stage of the kernel.
+// Measured on B200 (tools/fwd_quick.py, ms per 1,048,576 cfg2 / 2,424,832 cfg5 examples):
+//   pair / merge warps   16 / 6   17 / 6   16 / 7   17 / 7   21 / 6
+//   cfg2 (9 chunks)       5.62     5.13     5.60     5.48     5.26
+//   cfg5 (25 chunks)     20.68    20.85    19.99    20.58    21.40
+// With few pair chunks only the first nch pair warps work (the others exit), and moving
+// the allocator from warp 16 (SMSP 0, beside pair warps 0, 4, 8) to warp 17 (SMSP 1,
+// beside 1 and 5) is worth 9%; with every pair warp busy a seventh merge warp (28 warps:
+// seven per SMSP) is worth 3%.
+__host__ __device__ inline void rsw_role_layout(int nch, int* npw, int* nmw) {
+  if (nch < RSW_NPW) { *npw = RSW_NPW + 1; *nmw = RSW_NMW; }
+  else { *npw = RSW_NPW; *nmw = RSW_NMW + 1; }
+}
+
 template <int K, typename T, int MU>
-__global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, RswSmem L) {
+__global__ void __launch_bounds__(RSW_MAXWARPS * 32, 1) fwd_rsw_kernel(FwdParams p, RswSmem L) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int F = p.F, P = p.P, D = p.D;
   constexpr int M = MU;
@@ -109,6 +128,7 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
   constexpr int SEGB = K * (int)sizeof(T);
   const int row_bytes = F * SEGB;
   const int RSB = L.row_stride, R = L.R, NX = L.NX, nch = L.nch;
+  const int NPW = L.npw, NMW = L.nmw;  // role layout of this launch (rsw_role_layout)
   uint64_t* full = (uint64_t*)(smem + L.off_bar);  // [NX] producers -> pair/merge warps
   uint64_t* pdone = full + RSW_MAXX;               // [NX] pair chunks -> producers/merge
   uint64_t* mfree = pdone + RSW_MAXX;              // [NX] merge warp -> producers
@@ -120,7 +140,7 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const T* lrt = (const T*)p.lr;
 
-  for (int f1 = threadIdx.x; f1 < F; f1 += RSW_THREADS) {
+  for (int f1 = threadIdx.x; f1 < F; f1 += blockDim.x) {
     const int base = f1 * F - f1 * (f1 + 1) / 2;
     for (int f2 = f1 + 1; f2 < F; ++f2) pairtab[base + f2 - f1 - 1] = (uint16_t)(f1 | (f2 << 8));
   }
@@ -138,13 +158,13 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
   const int64_t my_n = p.n > blockIdx.x ? (p.n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   auto slot = [&](int xs) { return slots + (size_t)xs * L.slot_bytes; };
 
-  if (warp >= RSW_NPW + RSW_NPROD) {
+  if (warp >= NPW + RSW_NPROD) {
     // ================================================================ merge warps
-    const int mw = warp - RSW_NPW - RSW_NPROD;
+    const int mw = warp - NPW - RSW_NPROD;
     const float bias = load_elem<T>(lrt + p.n_buckets, p.dlr);
     int xs = mw % NX;
     uint32_t par = (uint32_t)((mw / NX) & 1);
-    for (int64_t i = mw; i < my_n; i += RSW_NMW) {
+    for (int64_t i = mw; i < my_n; i += NMW) {
       const int64_t e = blockIdx.x + i * gridDim.x;
       unsigned char* sb = slot(xs);
       const int* sidx = (const int*)(sb + L.off_sidx);
@@ -210,17 +230,17 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&mfree[xs]);
-      xs += RSW_NMW;
+      xs += NMW;
       while (xs >= NX) { xs -= NX; par ^= 1u; }
     }
-  } else if (warp > RSW_NPW) {
+  } else if (warp > NPW) {
     // ================================================================ TMA issue warps
     // Slot s of example i is issued by warp s % NISS, lane s / NISS, from the
     // metadata the allocator published on meta[i]; each warp arrives on
     // full[i] once with the bytes of its rows.  Issuing is spread over several
     // warps because a 1-D bulk copy per row is the step that limits how fast
     // the ring refills (measured: 2 -> 4 issuing warps, cfg5 +5%, cfg2 +20%).
-    const int iw = warp - RSW_NPW - 1;
+    const int iw = warp - NPW - 1;
     int xs = 0;
     uint32_t par = 0;
     for (int64_t i = 0; i < my_n; ++i) {
@@ -252,7 +272,7 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
       }
       if (++xs == NX) { xs = 0; par ^= 1u; }
     }
-  } else if (warp == RSW_NPW) {
+  } else if (warp == NPW) {
     // ================================================================ allocator warp
     constexpr int SPL = RSW_MAXFM / 32;
     // idx / val of examples i+1 .. i+IDXD-1 stream into a shared ring by
@@ -373,7 +393,7 @@ __global__ void __launch_bounds__(RSW_THREADS, 1) fwd_rsw_kernel(FwdParams p, Rs
     // merge warps wait on meta[i], published only after the merge of i-NX.)
     int G = 1;
     while (2 * G <= RSW_GT && NX % (2 * G) == 0) G *= 2;
-    const int npg = RSW_NPW / G < nch ? RSW_NPW / G : nch;
+    const int npg = NPW / G < nch ? NPW / G : nch;
     const int gw = warp / npg, wi = warp - gw * npg;
     int64_t i = gw < G ? gw : my_n;
     int c = wi;
